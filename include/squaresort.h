@@ -1,0 +1,161 @@
+/*
+ * squaresort.h -- C ABI of the B200-native SquareSort library (libsquaresort.so).
+ *
+ * SquareSort (arXiv 2407.14801) views n keys as an m x m column-major matrix,
+ * m = ceil(sqrt(n)), sorts every column, samples
+ * m-1 random pivots, computes the bucket positions
+ * (P:283), moves every key into its bucket with SkewTranspose
+ * (Alg 2/3) and sorts every bucket.  This library runs
+ * each recursion level as batched sm_100a kernels on one B200.
+ *
+ * Citations: "P:n" = PAPER.md line n; "S:n" = SPEC.md line n; "L#" = a reading
+ * of the paper listed in DESIGN.md section 3.
+ *
+ * Conventions (all entry points):
+ *  - Data pointers of the sq_sort_* / sq_skew_transpose calls are caller-owned
+ *    CUDA DEVICE memory (cudaMalloc or a torch CUDA tensor's data_ptr()),
+ *    naturally aligned (4 B for u32, 8 B for u64); 16-byte alignment is not
+ *    required.  The library never frees them or keeps them after return.
+ *    The *_host variants take caller-owned HOST memory (pinned memory gives
+ *    full copy bandwidth) and copy it to and from the device themselves.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *    enqueued on it; the call also blocks the host on it once per recursion
+ *    level (a device->host read of the bucket sizes that plans the next
+ *    level), and the result is complete when the call returns.
+ *  - Scratch: n keys (+ n values) plus O(n / 32) metadata (the paper's O(n)
+ *    extra space), allocated stream-ordered from the device's
+ *    default memory pool (cudaMallocAsync) and released before return.
+ *  - Errors are return codes only (sq_status); nothing is printed, no
+ *    exception crosses the ABI.  sq_last_error_message() gives detail for the
+ *    calling thread's last non-OK return.
+ *  - n = 0 and n = 1 return SQ_OK without touching memory.
+ *  - Limits: n <= 2^30 for u32 keys and pairs, n <= 2^28 for u64 keys (the
+ *    pivot sample of m-1 keys is sorted on chip by one CTA).
+ *  - The sorted keys do not depend on `seed` (the sorted order is unique);
+ *    pairs are sorted stably (equal keys keep their input order, L16), so
+ *    their output does not depend on `seed` either.  Only internal pivots do.
+ *  - Concurrent calls on different streams with disjoint buffers are allowed.
+ */
+#ifndef SQUARESORT_H
+#define SQUARESORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SQ_OK = 0,
+  SQ_ERR_INVALID_ARGUMENT = 1,   /* NULL with n > 0, aliasing, size limits, bad params   */
+  SQ_ERR_OUT_OF_MEMORY = 2,      /* scratch allocation failed                             */
+  SQ_ERR_CUDA = 3,               /* a CUDA runtime call or kernel failed                  */
+  SQ_ERR_PRECONDITION = 4,       /* SQ_FLAG_VALIDATE found unsorted columns / pivots      */
+  SQ_ERR_UNSUPPORTED_DEVICE = 5  /* the current device is not sm_100 (B200)               */
+} sq_status;
+
+/* ------------------------------------------------------------------------- */
+/* Sorting (Alg 1).  In place from the caller's view: keys[0..n)  */
+/* (and vals) hold the ascending result on return.                           */
+/* ------------------------------------------------------------------------- */
+
+/* Sort n 32-bit unsigned keys ascending (unsigned order; L15). */
+int sq_sort_u32(uint32_t *keys, size_t n, uint64_t seed, void *stream);
+
+/* Sort n 64-bit unsigned keys ascending. */
+int sq_sort_u64(uint64_t *keys, size_t n, uint64_t seed, void *stream);
+
+/* Sort n (key, value) pairs by key, stably; vals[i] travels with keys[i].
+ * keys and vals must not overlap. */
+int sq_sort_pairs_u32_u32(uint32_t *keys, uint32_t *vals, size_t n, uint64_t seed, void *stream);
+
+/* Same operations on HOST buffers: copy in, sort on the device, copy out,
+ * synchronize.  The end-to-end path the bench's `e2e` figure measures. */
+int sq_sort_u32_host(uint32_t *keys, size_t n, uint64_t seed, void *stream);
+int sq_sort_u64_host(uint64_t *keys, size_t n, uint64_t seed, void *stream);
+int sq_sort_pairs_u32_u32_host(uint32_t *keys, uint32_t *vals, size_t n, uint64_t seed,
+                               void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* SkewTranspose exactly as Alg 2/3 define it.        */
+/* ------------------------------------------------------------------------- */
+#define SQ_FLAG_VALIDATE 1u /* check columns sorted and pivots non-decreasing first */
+
+typedef struct {
+  /* Device pointer: the k-1 finite pivots p_1 <= ... <= p_{k-1},
+   * non-decreasing.  Bucket j (0-based) takes the keys x with
+   * bucket(x) = #{p < x} + [x is a pivot] = j (Alg 3 with strict '<' and the
+   * equal-pivot rule, L2/L4).  The last bucket is unbounded; +infinity is
+   * implicit and is never a stored value (L3).  May be NULL when k = 1. */
+  const uint32_t *pivots;
+  uint32_t k;               /* number of buckets, >= 1 */
+  uint64_t n;               /* keys present; 0 means rows*cols.  Column c is
+                               src[c*rows, min((c+1)*rows, n)). */
+  const uint32_t *buc_in;   /* device, k entries: initial write cursors (0-based
+                               offsets into dst), or NULL: the bucket starts are
+                               computed (analysis convention P:461, L1):
+                               buc[0] = 0, buc[j] = #{x : bucket(x) < j}. */
+  uint32_t *buc_out;        /* device, k entries, required: final cursors
+                               buc_in[j] + size_j -- the "shifted by one
+                               position" state of Alg 1. */
+  uint32_t naive_threshold; /* Alg 2 leaf threshold (default 4), >= 2.
+                               Alg 2 and Alg 3 give identical results for any
+                               threshold, so it never changes the output. */
+  uint32_t flags;           /* SQ_FLAG_VALIDATE or 0 */
+} sq_skew_params;
+
+/* dst[buc[j] + r] = the r-th key of bucket j in column-major order of src
+ * (stable: column order, then position in the column).  src holds
+ * `cols` sorted columns of `rows` keys (the last ones ragged or empty when
+ * n < rows*cols).  src and dst are device buffers of at least n keys and must
+ * not overlap.  Errors: SQ_ERR_INVALID_ARGUMENT for NULL src/dst/buc_out with
+ * n > 0, NULL pivots with k > 1, k = 0, threshold < 2, rows*cols overflow,
+ * n > rows*cols, n >= 2^32, or overlapping src/dst; SQ_ERR_PRECONDITION
+ * (with SQ_FLAG_VALIDATE) for an unsorted column or decreasing pivots; without
+ * the flag, unsorted input gives unspecified (but memory-safe) dst contents. */
+int sq_skew_transpose(const uint32_t *src, uint32_t *dst, size_t rows, size_t cols,
+                      const sq_skew_params *params, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Introspection and test hooks.                                             */
+/* ------------------------------------------------------------------------- */
+const char *sq_status_string(int status);
+const char *sq_last_error_message(void);
+
+typedef struct {
+  uint32_t levels;          /* SquareSort levels run (recursion into oversize segments) */
+  uint32_t kernel_launches; /* kernels this library launched in the last call          */
+  uint32_t host_syncs;      /* device->host planning reads                             */
+  uint32_t top_round;       /* accepted sampling round of the top level (0-based)      */
+  uint32_t top_degenerate;  /* 1 if the top level hit the resample cap          */
+  uint32_t top_m;           /* m of the top level (0 if the input fit on chip)         */
+  uint64_t oversize_keys;   /* keys in buckets that needed another level               */
+} sq_stats;
+
+/* Statistics of the calling thread's last sort / transpose call. */
+void sq_get_stats(sq_stats *out);
+
+/* Tuning/test knob: the largest segment sorted on chip by one CTA (a power of
+ * two between 64 and the key type's maximum, 32768 for u32 and 16384 for
+ * 64-bit sorts).  Lowering it forces more SquareSort levels on small inputs.
+ * 0 restores the default.  Process-wide; returns SQ_ERR_INVALID_ARGUMENT for
+ * other values. */
+int sq_set_max_tile(uint32_t max_tile);
+
+/* One SquareSort level of u32 keys, stopped after the SkewTranspose (for
+ * intermediate-state parity tests): src (device, n keys, unchanged) is copied,
+ * its m = ceil(sqrt(n)) columns are sorted, pivots are sampled from the
+ * sorted columns at node key mix(seed), and the SkewTranspose result
+ * is written to dst (device, n keys).  pivots_out (device, m-1 entries),
+ * bucend_out (device, m entries: the final cursors) and info_out
+ * (device, 2 entries: accepted round, degenerate flag) may not be NULL.
+ * Requires 5 <= n and m <= the maximum tile. */
+int sq_debug_level_u32(const uint32_t *src, uint32_t *dst, size_t n, uint64_t seed,
+                       uint32_t *pivots_out, uint32_t *bucend_out, uint32_t *info_out,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SQUARESORT_H */

@@ -1,0 +1,187 @@
+"""B200-native SquareSort (arXiv 2407.14801): a thin ctypes binding over
+libsquaresort.so (include/squaresort.h).  Argument marshalling only -- every
+step of the sort runs in the library's CUDA kernels.  PyTorch supplies device
+memory (tensor.data_ptr()) and streams; nothing here computes on the data.
+
+There is no CPU fallback: if the library is missing or the device is not a
+B200, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsquaresort.so")
+_lib = None
+
+SQ_OK = 0
+SQ_FLAG_VALIDATE = 1
+STATUS = {0: "SQ_OK", 1: "SQ_ERR_INVALID_ARGUMENT", 2: "SQ_ERR_OUT_OF_MEMORY", 3: "SQ_ERR_CUDA",
+          4: "SQ_ERR_PRECONDITION", 5: "SQ_ERR_UNSUPPORTED_DEVICE"}
+EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_host",
+           "sq_sort_u64_host", "sq_sort_pairs_u32_u32_host", "sq_skew_transpose",
+           "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
+           "sq_debug_level_u32"]
+
+
+class SqError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class SkewParams(ctypes.Structure):
+    _fields_ = [("pivots", ctypes.c_void_p), ("k", ctypes.c_uint32), ("n", ctypes.c_uint64),
+                ("buc_in", ctypes.c_void_p), ("buc_out", ctypes.c_void_p),
+                ("naive_threshold", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint32),
+                ("host_syncs", ctypes.c_uint32), ("top_round", ctypes.c_uint32),
+                ("top_degenerate", ctypes.c_uint32), ("top_m", ctypes.c_uint32),
+                ("oversize_keys", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def lib():
+    """Load libsquaresort.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2407_14801_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, u64, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32
+        for f in ("sq_sort_u32", "sq_sort_u64", "sq_sort_u32_host", "sq_sort_u64_host"):
+            getattr(L, f).argtypes = [vp, sz, u64, vp]
+            getattr(L, f).restype = ctypes.c_int
+        for f in ("sq_sort_pairs_u32_u32", "sq_sort_pairs_u32_u32_host"):
+            getattr(L, f).argtypes = [vp, vp, sz, u64, vp]
+            getattr(L, f).restype = ctypes.c_int
+        L.sq_skew_transpose.argtypes = [vp, vp, sz, sz, ctypes.POINTER(SkewParams), vp]
+        L.sq_skew_transpose.restype = ctypes.c_int
+        L.sq_status_string.argtypes = [ctypes.c_int]
+        L.sq_status_string.restype = ctypes.c_char_p
+        L.sq_last_error_message.argtypes = []
+        L.sq_last_error_message.restype = ctypes.c_char_p
+        L.sq_get_stats.argtypes = [ctypes.POINTER(Stats)]
+        L.sq_get_stats.restype = None
+        L.sq_set_max_tile.argtypes = [u32]
+        L.sq_set_max_tile.restype = ctypes.c_int
+        L.sq_debug_level_u32.argtypes = [vp, vp, sz, u64, vp, vp, vp, vp]
+        L.sq_debug_level_u32.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != SQ_OK:
+        raise SqError(rc, lib().sq_last_error_message().decode())
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(t, dtype_name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+        raise TypeError("expected a contiguous CUDA tensor")
+    if str(t.dtype) != dtype_name:
+        raise TypeError(f"expected {dtype_name}, got {t.dtype}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _seed(seed):
+    return ctypes.c_uint64(int(seed) & (2**64 - 1))
+
+
+# ------------------------------------------------------------------ device-buffer calls
+def sort_u32(keys, seed: int = 0, stream=None):
+    """Sort a contiguous torch.uint32 CUDA tensor in place (sq_sort_u32)."""
+    _check(lib().sq_sort_u32(_dev(keys, "torch.uint32"), keys.numel(), _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_u64(keys, seed: int = 0, stream=None):
+    """Sort a contiguous torch.uint64 CUDA tensor in place (sq_sort_u64)."""
+    _check(lib().sq_sort_u64(_dev(keys, "torch.uint64"), keys.numel(), _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_pairs_u32_u32(keys, vals, seed: int = 0, stream=None):
+    """Stable sort of (keys, vals) uint32 CUDA tensors by key, in place."""
+    if vals.numel() != keys.numel():
+        raise ValueError("keys and vals differ in length")
+    _check(lib().sq_sort_pairs_u32_u32(_dev(keys, "torch.uint32"), _dev(vals, "torch.uint32"),
+                                       keys.numel(), _seed(seed), _stream(stream)))
+    return keys, vals
+
+
+def skew_transpose(src, dst, rows: int, cols: int, pivots=None, k: int | None = None,
+                   n: int = 0, buc_in=None, buc_out=None, naive_threshold: int = 4,
+                   flags: int = 0, stream=None):
+    """sq_skew_transpose on torch.uint32 CUDA tensors.  Returns buc_out."""
+    import torch
+    k = (pivots.numel() + 1 if pivots is not None else 1) if k is None else k
+    if buc_out is None:
+        buc_out = torch.empty(k, dtype=torch.uint32, device=src.device)
+    p = SkewParams(pivots.data_ptr() if pivots is not None and pivots.numel() else None, k, n,
+                   buc_in.data_ptr() if buc_in is not None else None, buc_out.data_ptr(),
+                   naive_threshold, flags)
+    _check(lib().sq_skew_transpose(ctypes.c_void_p(src.data_ptr()) if src.numel() else None,
+                                   ctypes.c_void_p(dst.data_ptr()) if dst.numel() else None,
+                                   rows, cols, ctypes.byref(p), _stream(stream)))
+    return buc_out
+
+
+def debug_level_u32(src, dst, seed: int, pivots_out, bucend_out, info_out, stream=None):
+    _check(lib().sq_debug_level_u32(_dev(src, "torch.uint32"), _dev(dst, "torch.uint32"),
+                                    src.numel(), _seed(seed), _dev(pivots_out, "torch.uint32"),
+                                    _dev(bucend_out, "torch.uint32"), _dev(info_out, "torch.uint32"),
+                                    _stream(stream)))
+
+
+# ------------------------------------------------------------------ host-buffer calls
+def _host_ptr(a, dtype):
+    import numpy as np
+    if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
+        raise TypeError(f"expected a contiguous numpy {dtype} array")
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def sort_u32_host(keys, seed: int = 0, stream=None):
+    import numpy as np
+    _check(lib().sq_sort_u32_host(_host_ptr(keys, np.uint32), keys.size, _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_u64_host(keys, seed: int = 0, stream=None):
+    import numpy as np
+    _check(lib().sq_sort_u64_host(_host_ptr(keys, np.uint64), keys.size, _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_pairs_u32_u32_host(keys, vals, seed: int = 0, stream=None):
+    import numpy as np
+    _check(lib().sq_sort_pairs_u32_u32_host(_host_ptr(keys, np.uint32), _host_ptr(vals, np.uint32),
+                                            keys.size, _seed(seed), _stream(stream)))
+    return keys, vals
+
+
+# ------------------------------------------------------------------ introspection
+def get_stats() -> dict:
+    s = Stats()
+    lib().sq_get_stats(ctypes.byref(s))
+    return s.as_dict()
+
+
+def set_max_tile(t: int):
+    _check(lib().sq_set_max_tile(t))

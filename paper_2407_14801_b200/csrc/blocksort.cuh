@@ -1,0 +1,182 @@
+// blocksort.cuh -- on-chip sort of one segment by one CTA (the GPU's simple_sort).
+//
+// The paper's base case sorts small arrays directly (Alg 1; the
+// experiments use std::sort below 1000 items).  On B200 the base case is
+// whatever one CTA can hold on chip: the segment is staged in shared memory,
+// each thread sorts V keys in registers with Batcher's odd-even merge network,
+// and log2(NT) merge-path passes (runs of V -> NT*V) merge through shared
+// memory into registers.  Keys only need a correct sort (the result is
+// unique); pairs sort 64-bit composites (key << 32 | position) so the result is
+// the stable order (L16) and the payload is gathered once at the end.
+#pragma once
+#include <utility>
+#include "common.cuh"
+
+namespace sq {
+
+template <typename K>
+__device__ __forceinline__ void cas(K& a, K& b) {
+  K lo = a < b ? a : b;
+  K hi = a < b ? b : a;
+  a = lo;
+  b = hi;
+}
+
+// Batcher's odd-even merge sort network on V (a power of two) registers,
+// generated at compile time and applied with a fold so every index is static
+// (the registers never spill to local memory).
+template <int V>
+struct OddEvenNet {
+  static constexpr int count() {
+    int c = 0;
+    for (int p = 1; p < V; p += p)
+      for (int k = p; k > 0; k /= 2)
+        for (int j = k % p; j < V - k; j += 2 * k)
+          for (int i = 0; i < k; i++)
+            if (i + j + k < V && (i + j) / (p + p) == (i + j + k) / (p + p)) c++;
+    return c;
+  }
+  static constexpr int N = count();
+  int a[N > 0 ? N : 1], b[N > 0 ? N : 1];
+  constexpr OddEvenNet() : a{}, b{} {
+    int c = 0;
+    for (int p = 1; p < V; p += p)
+      for (int k = p; k > 0; k /= 2)
+        for (int j = k % p; j < V - k; j += 2 * k)
+          for (int i = 0; i < k; i++)
+            if (i + j + k < V && (i + j) / (p + p) == (i + j + k) / (p + p)) {
+              a[c] = i + j;
+              b[c] = i + j + k;
+              c++;
+            }
+  }
+};
+
+template <typename K, int V, int... I>
+__device__ __forceinline__ void apply_net(K (&r)[V], std::integer_sequence<int, I...>) {
+  constexpr OddEvenNet<V> net{};
+  (cas(r[net.a[I]], r[net.b[I]]), ...);
+}
+
+template <typename K, int V>
+__device__ __forceinline__ void thread_sort(K (&r)[V]) {
+  if constexpr (V > 1) apply_net<K, V>(r, std::make_integer_sequence<int, OddEvenNet<V>::N>{});
+}
+
+template <typename K, int NT_, int V_>
+struct BlockSort {
+  static constexpr int NT = NT_;
+  static constexpr int V = V_;
+  static constexpr int TILE = NT * V;
+  static constexpr int PER = 128 / sizeof(K);  // elements per 128-byte pad period
+  static constexpr int SMEM_ELEMS = TILE + TILE / PER + 1;
+  static constexpr size_t SMEM_BYTES = size_t(SMEM_ELEMS) * sizeof(K);
+
+  __device__ __forceinline__ static int pad(int i) { return i + i / PER; }
+
+  // Sort the TILE keys held in s[pad(0..TILE-1)] (padding slots hold KeyTraits::kMax).
+  // On return s holds the sorted tile (padded layout); a __syncthreads() has
+  // been executed so all threads may read it.
+  __device__ static void sort_smem(K* s) {
+    const int t = threadIdx.x;
+    K r[V];
+#pragma unroll
+    for (int j = 0; j < V; j++) r[j] = s[pad(t * V + j)];
+    thread_sort<K, V>(r);
+#pragma unroll 1
+    for (int w = V; w < TILE; w *= 2) {
+      __syncthreads();  // previous readers of s are done
+#pragma unroll
+      for (int j = 0; j < V; j++) s[pad(t * V + j)] = r[j];
+      __syncthreads();
+      const int g = (t * V) & ~(2 * w - 1);  // first index of the run pair
+      const int diag = t * V - g;
+      const K* A = s;  // indices g .. g+w-1   (through pad())
+      const int a0 = g, b0 = g + w;
+      // merge path: smallest i with A[i] > B[diag-1-i] (ties taken from A first)
+      int lo = diag > w ? diag - w : 0;
+      int hi = diag < w ? diag : w;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        K a = A[pad(a0 + mid)];
+        K b = A[pad(b0 + diag - 1 - mid)];
+        if (a <= b) lo = mid + 1; else hi = mid;
+      }
+      int i = lo, jj = diag - lo;
+      K a = i < w ? A[pad(a0 + i)] : KeyTraits<K>::kMax;
+      K b = jj < w ? A[pad(b0 + jj)] : KeyTraits<K>::kMax;
+      // Serial merge.  Exhausted runs read as kMax: a real kMax key and the
+      // sentinel are equal values, so which one is emitted never matters.
+#pragma unroll
+      for (int k = 0; k < V; k++) {
+        bool takeA = a <= b;
+        r[k] = takeA ? a : b;
+        if (takeA) {
+          i++;
+          a = i < w ? A[pad(a0 + i)] : KeyTraits<K>::kMax;
+        } else {
+          jj++;
+          b = jj < w ? A[pad(b0 + jj)] : KeyTraits<K>::kMax;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < V; j++) s[pad(t * V + j)] = r[j];
+    __syncthreads();
+  }
+};
+
+// ------------------------------------------------------------------------
+// Segment descriptors for batched sorts.
+struct SegDesc {
+  uint32_t off;  // first element
+  uint32_t len;  // number of elements (<= the class's TILE)
+};
+
+// Keys-only batched sort: CTA b sorts segment segs[b] from src into dst (same
+// offsets; src may equal dst).
+template <typename K, int NT, int V>
+__global__ void __launch_bounds__(NT)
+k_blocksort(const SegDesc* __restrict__ segs, const K* __restrict__ src, K* __restrict__ dst) {
+  using BS = BlockSort<K, NT, V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* s = reinterpret_cast<K*>(smem_raw);
+  const SegDesc d = segs[blockIdx.x];
+  const K* in = src + d.off;
+  for (int i = threadIdx.x; i < BS::TILE; i += NT) s[BS::pad(i)] = i < (int)d.len ? in[i] : KeyTraits<K>::kMax;
+  __syncthreads();
+  BS::sort_smem(s);
+  K* out = dst + d.off;
+  for (int i = threadIdx.x; i < (int)d.len; i += NT) out[i] = s[BS::pad(i)];
+}
+
+// Pairs batched sort (u32 keys, u32 payload), stable: composites key<<32 | pos.
+template <int NT, int V>
+__global__ void __launch_bounds__(NT)
+k_blocksort_pairs(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ ksrc,
+                  const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ kdst,
+                  uint32_t* __restrict__ vdst) {
+  using BS = BlockSort<uint64_t, NT, V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* s = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  const SegDesc d = segs[blockIdx.x];
+  for (int i = threadIdx.x; i < BS::TILE; i += NT) {
+    uint64_t c = KeyTraits<uint64_t>::kMax;
+    if (i < (int)d.len) {
+      c = (uint64_t(ksrc[d.off + i]) << 32) | uint32_t(i);
+      vs[i] = vsrc[d.off + i];
+    }
+    s[BS::pad(i)] = c;
+  }
+  __syncthreads();
+  BS::sort_smem(s);
+  for (int i = threadIdx.x; i < (int)d.len; i += NT) {
+    uint64_t c = s[BS::pad(i)];
+    kdst[d.off + i] = uint32_t(c >> 32);
+    vdst[d.off + i] = vs[uint32_t(c)];
+  }
+}
+
+}  // namespace sq

@@ -1,0 +1,316 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element, on the seeded BASELINE configs and edge cases.  Integer work, so
+the bar is bit-exact everywhere."""
+import numpy as np
+import pytest
+
+import oracle as O
+import sqinputs as S
+from tests import closed_forms as CF
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2407_14801_b200 as sq  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def _reset_tile():
+    sq.set_max_tile(0)
+    yield
+    sq.set_max_tile(0)
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def to_host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def gpu_sort(keys, seed=0, vals=None):
+    k = to_dev(keys)
+    if vals is not None:
+        v = to_dev(vals)
+        sq.sort_pairs_u32_u32(k, v, seed)
+        return to_host(k), to_host(v)
+    if keys.dtype == np.uint32:
+        sq.sort_u32(k, seed)
+    else:
+        sq.sort_u64(k, seed)
+    return to_host(k)
+
+
+def oracle_sort(keys, seed, vals=None):
+    d, dv, st = O.square_sort(keys, vals, seed=seed)
+    return d.astype(keys.dtype), (None if dv is None else dv)
+
+
+# ---------------------------------------------------------------- configs vs oracle
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_config_vs_oracle(cfg):
+    keys, _ = S.config(cfg)
+    seed = S.CONFIGS[cfg][2]
+    want, _ = oracle_sort(keys, seed)
+    got = gpu_sort(keys, seed)
+    assert got.dtype == keys.dtype and np.array_equal(got, want)
+
+
+def test_cfg3_u64_duplicates_vs_oracle():
+    keys, _ = S.config("cfg3")
+    want, _ = oracle_sort(keys, 3)
+    got = gpu_sort(keys, 3)
+    assert np.array_equal(got, want)
+    st = sq.get_stats()
+    assert st["top_degenerate"] == 1 and st["top_round"] == 31  # 4095 draws from 1000 values
+
+
+@pytest.mark.parametrize("cfg", ["cfg4_sorted", "cfg4_reverse", "cfg4_swapped", "cfg4_nonsquare"])
+def test_cfg4_variants(cfg):
+    keys, _ = S.config(cfg)
+    got = gpu_sort(keys, 4)
+    want = np.sort(keys)  # closed form: the unique ascending permutation
+    assert np.array_equal(got, want)
+    if cfg == "cfg4_sorted":
+        assert np.array_equal(got, keys)
+    if cfg == "cfg4_reverse":
+        assert np.array_equal(got, keys[::-1])
+
+
+def test_cfg4_scaled_vs_oracle():
+    # the same recipes at 2^20, where the oracle itself runs in seconds
+    for cfg in ("cfg4_sorted", "cfg4_reverse", "cfg4_swapped"):
+        keys, _ = S.config(cfg, n=1 << 20)
+        want, _ = oracle_sort(keys, 4)
+        assert np.array_equal(gpu_sort(keys, 4), want), cfg
+    keys, _ = S.config("cfg4_nonsquare", n=(1 << 20) - 12345)
+    want, _ = oracle_sort(keys, 4)
+    assert np.array_equal(gpu_sort(keys, 4), want)
+
+
+def test_cfg5_full_size():
+    keys, _ = S.config("cfg5")
+    got = gpu_sort(keys, 5)
+    assert np.all(got[1:] >= got[:-1])
+    want = np.sort(keys)
+    assert np.array_equal(got, want)
+    # sampled order statistics straight from the definition (rank of out[i])
+    rng = np.random.default_rng(0)
+    for i in rng.integers(0, len(keys), 3):
+        x = got[i]
+        assert (keys < x).sum() <= i < (keys <= x).sum()
+
+
+def test_cfg5p_pairs_full_size():
+    keys, vals = S.config("cfg5p")
+    gk, gv = gpu_sort(keys, 5, vals)
+    n = len(keys)
+    assert np.array_equal(gk, np.arange(n, dtype=np.uint32))
+    inv = np.empty(n, np.uint32)
+    inv[keys] = np.arange(n, dtype=np.uint32)  # vals_out[k] = input position of key k
+    assert np.array_equal(gv, inv)
+
+
+def test_pairs_scaled_vs_oracle():
+    keys, vals = S.config("cfg5p", n=1 << 18)
+    want_k, want_v = oracle_sort(keys, 5, vals)
+    gk, gv = gpu_sort(keys, 5, vals)
+    assert np.array_equal(gk, want_k) and np.array_equal(gv, want_v)
+
+
+# ---------------------------------------------------------------- edge cases
+EDGE_N = [0, 1, 2, 3, 4, 5, 16, 17, 63, 64, 65, 255, 256, 257, 1000, 4095, 4096, 4097,
+          32767, 32768, 32769, 65535, 65536, 65537, 100000, 250001]
+
+
+@pytest.mark.parametrize("n", EDGE_N)
+def test_sizes_u32(n):
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    assert np.array_equal(gpu_sort(keys, n), np.sort(keys))
+
+
+@pytest.mark.parametrize("n", [0, 1, 5, 17, 1000, 16384, 16385, 70000])
+def test_sizes_u64(n):
+    rng = np.random.default_rng(n + 1)
+    keys = rng.integers(0, 2**64, n, dtype=np.uint64)
+    assert np.array_equal(gpu_sort(keys, 7), np.sort(keys))
+
+
+@pytest.mark.parametrize("tile", [64, 256, 1024])
+@pytest.mark.parametrize("n", [5000, 70001, 300000])
+def test_forced_multilevel_vs_oracle(tile, n):
+    # a small on-chip tile forces SquareSort levels inside columns and buckets
+    sq.set_max_tile(tile)
+    rng = np.random.default_rng(tile * 7 + n)
+    for card in (2**32, 1000, 3):
+        keys = rng.integers(0, card, n, dtype=np.uint64).astype(np.uint32)
+        want, _ = oracle_sort(keys, 11)
+        got = gpu_sort(keys, 11)
+        assert np.array_equal(got, want), card
+        if card == 2**32 and n >= 16 * tile:
+            assert sq.get_stats()["levels"] >= 2
+
+
+@pytest.mark.parametrize("tile", [64, 512])
+def test_forced_multilevel_pairs_and_u64(tile):
+    sq.set_max_tile(tile)
+    rng = np.random.default_rng(tile)
+    n = 50000
+    k = rng.integers(0, 50, n, dtype=np.uint64).astype(np.uint32)
+    v = np.arange(n, dtype=np.uint32)
+    gk, gv = gpu_sort(k, 3, v)
+    ek, ev = CF.stable_pairs_sort(k, v)
+    assert np.array_equal(gk, ek) and np.array_equal(gv, ev)
+    k64 = rng.integers(0, 2**64, n, dtype=np.uint64)
+    assert np.array_equal(gpu_sort(k64, 3), np.sort(k64))
+
+
+def test_special_values():
+    n = 200000
+    rng = np.random.default_rng(3)
+    for keys in (np.full(n, 0xFFFFFFFF, np.uint32), np.zeros(n, np.uint32),
+                 np.where(rng.random(n) < 0.5, 0xFFFFFFFF, 0).astype(np.uint32),
+                 rng.integers(0xFFFFFFF0, 2**32, n, dtype=np.uint64).astype(np.uint32)):
+        assert np.array_equal(gpu_sort(keys, 1), np.sort(keys))
+    k64 = np.full(70000, 2**64 - 1, np.uint64)
+    k64[::7] = 0
+    assert np.array_equal(gpu_sort(k64, 1), np.sort(k64))
+
+
+def test_pairs_stability_with_duplicates():
+    rng = np.random.default_rng(5)
+    for n, card in ((1000, 3), (100000, 100), (300000, 2**32)):
+        k = rng.integers(0, card, n, dtype=np.uint64).astype(np.uint32)
+        v = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+        gk, gv = gpu_sort(k, 9, v)
+        ek, ev = CF.stable_pairs_sort(k, v)
+        assert np.array_equal(gk, ek) and np.array_equal(gv, ev)
+
+
+def test_seed_invariance():
+    keys, _ = S.config("cfg2")
+    ref = gpu_sort(keys, 2)
+    for seed in (0, 12345, 2**63 + 5):
+        assert np.array_equal(gpu_sort(keys, seed), ref)
+
+
+def test_host_entry_points():
+    keys, _ = S.config("cfg2")
+    h = keys.copy()
+    sq.sort_u32_host(h, 2)
+    assert np.array_equal(h, np.sort(keys))
+    k, v = S.config("cfg5p", n=1 << 16)
+    hk, hv = k.copy(), v.copy()
+    sq.sort_pairs_u32_u32_host(hk, hv, 5)
+    ek, ev = CF.stable_pairs_sort(k, v)
+    assert np.array_equal(hk, ek) and np.array_equal(hv, ev)
+    k64, _ = S.config("cfg3", n=1 << 16)
+    h64 = k64.copy()
+    sq.sort_u64_host(h64, 3)
+    assert np.array_equal(h64, np.sort(k64))
+
+
+# ---------------------------------------------------------------- one level vs the oracle's level
+@pytest.mark.parametrize("n,card", [(1 << 16, 2**32), (1 << 20, 2**32), (100003, 2**32),
+                                    (1 << 16, 1000), (50000, 7)])
+def test_level_intermediate_parity(n, card):
+    """Pivots, accepted round, bucket ends and the post-SkewTranspose array of
+    one level equal the oracle's (paper-literal sampling from D)."""
+    rng = np.random.default_rng(n ^ card)
+    keys = rng.integers(0, card, n, dtype=np.uint64).astype(np.uint32)
+    seed = 77
+    post, _, P, be, r, deg = O.level(keys, seed=seed, sample_from_input=False)
+    m = O.ceil_sqrt(n)
+    src = to_dev(keys)
+    dst = torch.empty_like(src)
+    piv = torch.empty(m - 1, dtype=torch.uint32, device="cuda")
+    bend = torch.empty(m, dtype=torch.uint32, device="cuda")
+    info = torch.empty(2, dtype=torch.uint32, device="cuda")
+    sq.debug_level_u32(src, dst, seed, piv, bend, info)
+    assert np.array_equal(to_host(piv).astype(np.uint64), P)
+    assert np.array_equal(to_host(bend).astype(np.uint64), be)
+    assert to_host(info).tolist() == [r, deg]
+    assert np.array_equal(to_host(dst).astype(np.uint64), post)
+    assert np.array_equal(to_host(src), keys)  # src untouched
+
+
+# ---------------------------------------------------------------- sq_skew_transpose
+def _sorted_cols(x, rows, n):
+    x = x.copy()
+    for a in range(0, n, rows):
+        x[a:min(a + rows, n)] = np.sort(x[a:min(a + rows, n)])
+    return x
+
+
+def gpu_skew(src, rows, cols, pivots, k=None, n=0, buc_in=None, T=4, flags=0):
+    s = to_dev(src.astype(np.uint32))
+    d = torch.zeros_like(s) if len(src) else torch.zeros(1, dtype=torch.uint32, device="cuda")
+    pv = to_dev(np.asarray(pivots, np.uint32)) if len(pivots) else None
+    bi = to_dev(np.asarray(buc_in, np.uint32)) if buc_in is not None else None
+    bo = sq.skew_transpose(s, d, rows, cols, pv, k, n, bi, None, T, flags)
+    return to_host(d), to_host(bo)
+
+
+@pytest.mark.parametrize("T", [4, 10, 2])
+def test_cfg2_skew_transpose_check(T):
+    """BASELINE config 2's SkewTranspose check: the 2^20 keys as a 1024x1024
+    matrix, columns sorted, pivots from the oracle's sampler at root mix(2)."""
+    keys, _ = S.config("cfg2")
+    n, m = len(keys), 1024
+    D = _sorted_cols(keys.astype(np.uint64), m, n)
+    P, r, deg = O.sample_pivots(O.root_key(2), D, D)
+    want, _, wbo = O.skew_transpose_matrix(D, m, m, P, T=T)
+    got, gbo = gpu_skew(D, m, m, P, T=T)
+    assert np.array_equal(got.astype(np.uint64), want)
+    assert np.array_equal(gbo.astype(np.uint64), wbo)
+
+
+def test_skew_transpose_special_case_is_transpose():
+    m = 300  # one item of every bucket per column -> plain transpose
+    src = np.array([c + r * m for c in range(m) for r in range(m)], np.uint64)
+    P = np.array([j * m for j in range(1, m)], np.uint64)
+    got, _ = gpu_skew(src, m, m, P)
+    assert np.array_equal(got.reshape(m, m), src.reshape(m, m).T.astype(np.uint32))
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_skew_transpose_random_shapes(case):
+    rng = np.random.default_rng(1000 + case)
+    rows = int(rng.integers(1, 3000))
+    cols = int(rng.integers(1, 300))
+    n = int(rng.integers(0, rows * cols + 1)) if case % 3 == 0 else rows * cols
+    k = int(rng.choice([1, 2, cols, cols + 1, max(1, cols // 2), int(rng.integers(1, 5000))]))
+    card = int(rng.choice([3, 100, 2**32]))
+    x = rng.integers(0, card, rows * cols, dtype=np.uint64)
+    if case % 5 == 0:
+        x[rng.random(len(x)) < 0.3] = 0xFFFFFFFF
+    x = _sorted_cols(x, rows, n)
+    if case % 2:
+        P = np.sort(rng.choice(x[:max(n, 1)], k - 1)) if k > 1 else np.zeros(0, np.uint64)
+    else:
+        P = np.sort(rng.integers(0, card, k - 1, dtype=np.uint64))
+    buc_in = None
+    if case % 4 == 1:  # explicit cursors, buckets laid out in reverse order
+        _, _, bc = CF.skew_transpose(x, P, k, n=n)
+        sizes = bc - np.concatenate([[0], bc[:-1]]).astype(np.uint64)
+        buc_in = np.concatenate([[0], np.cumsum(sizes[::-1])[:-1]])[::-1].astype(np.uint64)
+    want, _, wbo = O.skew_transpose_matrix(x, rows, cols, P, k, n=n, buc_in=buc_in)
+    got, gbo = gpu_skew(x, rows, cols, P, k=k, n=n, buc_in=buc_in, T=int(rng.integers(2, 12)))
+    assert np.array_equal(got[:n].astype(np.uint64), want[:n])
+    assert np.array_equal(gbo.astype(np.uint64), wbo)
+
+
+def test_skew_transpose_validate_flag():
+    x = np.array([3, 1, 2, 4], np.uint64)  # column 0 unsorted
+    with pytest.raises(sq.SqError) as e:
+        gpu_skew(x, 2, 2, [2], flags=sq.SQ_FLAG_VALIDATE)
+    assert e.value.code == 4
+    x = np.array([1, 3, 2, 4], np.uint64)
+    with pytest.raises(sq.SqError) as e:
+        gpu_skew(x, 2, 2, [3, 2], flags=sq.SQ_FLAG_VALIDATE)
+    assert e.value.code == 4
+    got, bo = gpu_skew(x, 2, 2, [2, 3], flags=sq.SQ_FLAG_VALIDATE)
+    assert got.tolist() == [1, 2, 3, 4] and bo.tolist() == [1, 2, 4]
