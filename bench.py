@@ -1,0 +1,295 @@
+#!/usr/bin/env python3
+"""SquareSort throughput on B200 -- BASELINE.json's metric:
+"Gkeys/s for SquareSort of 2^28 uint32 keys; fraction of 8 TB/s HBM roofline".
+
+One step = one sq_sort_u32 call (the whole hot path: column sort, pivot
+sampling, bucket count, SkewTranspose, bucket sorts, oversize levels) on
+config 5 (2^28 uniform uint32 keys, seed 5; BASELINE configs[4]).  The input
+(1 GiB) is restored from a pristine device copy before every step, outside the
+step's CUDA events; it is larger than the 126 MB L2, so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): every rank sorts its own 2^28 keys -- replicas, no
+collective on the data path; value = all ranks' keys / the max
+over ranks of the summed step time.  `--impl reference` times the CPU oracle
+(the reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gkeys/s for SquareSort of 2^28 uint32 keys; fraction of 8 TB/s HBM roofline"
+UNIT = "Gkeys/s"
+CFG = "cfg5"
+NOMINAL_HBM_GBS = 8000.0
+W = 4  # bytes per key
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", float(p.get("sm_max_mhz", 1965))
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)", 1965.0
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(keys, seconds_hint=True):
+    """The oracle as it stands, single-threaded, on a bounded sample of the workload."""
+    import oracle as O
+    n = 1 << 22
+    sample = keys[:n].copy()
+    t0 = time.perf_counter()
+    O.square_sort(sample, seed=5)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first 2^22 keys of the cfg5 input (uniform u32, seed 5), oracle SquareSort "
+                      f"cutoff 16 / threshold 4, one run, {dt:.2f} s on 1 host core",
+            "host_cpu": _cpu_model(), "host_nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import oracle as O
+    import sqinputs as S
+    n = 1 << 21
+    kind, _, seed = S.CONFIGS[CFG]
+    keys, _ = S.generate(kind, n, seed)
+    for _ in range(args.warmup):
+        O.square_sort(keys, seed=seed)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.square_sort(keys, seed=seed)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = n / (ms / 1e3) / 1e9
+    sample = (f"2^21 keys of the cfg5 recipe (uniform u32, seed 5) per step; oracle SquareSort "
+              f"(oracle/squaresort_oracle.c, cutoff 16, threshold 4), single-threaded")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg5 sample: 2^21 uniform uint32 keys (seed 5) on 1 host core",
+                   "n": n, "parallelism": "none (CPU oracle)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample, "host_cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2407_14801_b200 as sq
+    import sqinputs as S
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    kind, n, seed = S.CONFIGS[CFG]
+    keys, _ = S.generate(kind, n, seed)
+    pristine = torch.from_numpy(keys).cuda()
+    work = torch.empty_like(pristine)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 0)):
+        work.copy_(pristine)
+        sq.sort_u32(work, seed)
+    torch.cuda.synchronize()
+
+    sq.profile(True)
+    sq.profile_read()
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    evs, launches, stats = [], 0, None
+    for _ in range(args.steps):
+        work.copy_(pristine)  # restore: outside the step's events
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sq.sort_u32(work, seed)
+        b.record(stream)
+        evs.append((a, b))
+        stats = sq.get_stats()
+        launches += stats["kernel_launches"]
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    sq.profile(False)
+    prof = sq.profile_read()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = world * n / (ms / 1e3) / 1e9
+
+    # sanity: the last step's output is sorted and a permutation (sum check)
+    w64 = work.to(torch.int64)
+    ok = bool((w64[1:] >= w64[:-1]).all().item()) and \
+        int(w64.sum().item()) == int(pristine.to(torch.int64).sum().item())
+    del w64
+
+    hbm, hbm_src, _ = peaks()
+    b_alg = 6 * W * n  # column pass + SkewTranspose + bucket pass, read + write
+    # dominant kernel role and its HBM roofline (algorithmic bytes per launch / mean duration)
+    role_bytes = {"colsort": 2 * W * n, "bucketsort": 2 * W * n, "transpose": 2 * W * n,
+                  "count": W * n, "smallsort": 2 * W * n}
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
+    dname, (dlaunch, dms) = dom
+    per_step_launch = dlaunch / args.steps
+    bytes_per_launch = role_bytes.get(dname, 0) / max(per_step_launch, 1)
+    achieved = bytes_per_launch / (dms / dlaunch / 1e3) / 1e9 if dms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dname)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch,
+                "launches_per_step": per_step_launch,
+                "share_of_step": dms / total_ms if total_ms > 0 else None}
+    step_gbs = b_alg / (ms / 1e3) / 1e9
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg5: 2^28 uniform uint32 keys, seed 5 (BASELINE configs[4])",
+                   "n": n, "seed": seed, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs (1 GiB) exceed the 126 MB L2; no flush needed",
+                   "restore": "D2D copy of the pristine input before each step, outside the events"},
+        "hbm_roofline_step": {"b_alg_bytes": b_alg, "achieved_gbs": step_gbs,
+                              "frac_of_8TBs": step_gbs / NOMINAL_HBM_GBS, "frac_of_measured": step_gbs / hbm},
+        "roofline": roofline,
+        "kernels_ms_per_step": {k: v[1] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "sort_stats": stats,
+        "output_check": "sorted+sum" if ok else "FAILED",
+    }
+    if not args.no_e2e:
+        hp = torch.empty(n, dtype=torch.uint32).pin_memory()
+        hn = hp.numpy()
+        e_ms = []
+        esteps = max(1, min(args.steps, 10))
+        for i in range(esteps + 1):
+            np.copyto(hn, keys)  # restore (untimed)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sq.sort_u32_host(hn, seed)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:  # first one is a warm-up
+                e_ms.append(a.elapsed_time(b))
+        em = sum(e_ms) / len(e_ms)
+        out["e2e"] = {"value": world * n / (em / 1e3) / 1e9, "unit": UNIT, "ms_per_step": em,
+                      "steps": esteps, "h2d_bytes_per_step": n * W, "d2h_bytes_per_step": n * W,
+                      "api": "sq_sort_u32_host (pinned host buffer; H2D + sort + D2H per step)"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(keys)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -112,8 +112,11 @@ typedef struct {
  * not overlap.  Errors: SQ_ERR_INVALID_ARGUMENT for NULL src/dst/buc_out with
  * n > 0, NULL pivots with k > 1, k = 0, threshold < 2, rows*cols overflow,
  * n > rows*cols, n >= 2^32, or overlapping src/dst; SQ_ERR_PRECONDITION
- * (with SQ_FLAG_VALIDATE) for an unsorted column or decreasing pivots; without
- * the flag, unsorted input gives unspecified (but memory-safe) dst contents. */
+ * (with SQ_FLAG_VALIDATE) for an unsorted column or decreasing pivots (without
+ * the flag these are the caller's preconditions, as in Alg 2's input
+ * specification P:406, and violating them is undefined behaviour);
+ * SQ_ERR_INVALID_ARGUMENT also when a caller-given cursor range
+ * [buc_in[j], buc_in[j] + size_j) does not fit in dst[0, n). */
 int sq_skew_transpose(const uint32_t *src, uint32_t *dst, size_t rows, size_t cols,
                       const sq_skew_params *params, void *stream);
 
@@ -142,6 +145,14 @@ void sq_get_stats(sq_stats *out);
  * 0 restores the default.  Process-wide; returns SQ_ERR_INVALID_ARGUMENT for
  * other values. */
 int sq_set_max_tile(uint32_t max_tile);
+
+/* Per-kernel device timing: when enabled, every kernel the library launches is
+ * bracketed by CUDA events on its stream and the elapsed times accumulate per
+ * kernel role (colsort, bucketsort, smallsort, sample, count, transpose, ...).
+ * sq_profile_read writes {"role": [launches, total_ms], ...} (JSON) into buf
+ * and clears the totals; SQ_ERR_INVALID_ARGUMENT if buf is too small. */
+int sq_profile(int enable);
+int sq_profile_read(char *buf, size_t cap);
 
 /* One SquareSort level of u32 keys, stopped after the SkewTranspose (for
  * intermediate-state parity tests): src (device, n keys, unchanged) is copied,

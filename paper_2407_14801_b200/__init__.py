@@ -22,7 +22,7 @@ STATUS = {0: "SQ_OK", 1: "SQ_ERR_INVALID_ARGUMENT", 2: "SQ_ERR_OUT_OF_MEMORY", 3
 EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_host",
            "sq_sort_u64_host", "sq_sort_pairs_u32_u32_host", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
-           "sq_debug_level_u32"]
+           "sq_debug_level_u32", "sq_profile", "sq_profile_read"]
 
 
 class SqError(RuntimeError):
@@ -72,6 +72,10 @@ def lib():
         L.sq_get_stats.restype = None
         L.sq_set_max_tile.argtypes = [u32]
         L.sq_set_max_tile.restype = ctypes.c_int
+        L.sq_profile.argtypes = [ctypes.c_int]
+        L.sq_profile.restype = ctypes.c_int
+        L.sq_profile_read.argtypes = [ctypes.c_char_p, sz]
+        L.sq_profile_read.restype = ctypes.c_int
         L.sq_debug_level_u32.argtypes = [vp, vp, sz, u64, vp, vp, vp, vp]
         L.sq_debug_level_u32.restype = ctypes.c_int
         _lib = L
@@ -185,3 +189,16 @@ def get_stats() -> dict:
 
 def set_max_tile(t: int):
     _check(lib().sq_set_max_tile(t))
+
+
+def profile(enable: bool = True):
+    """Enable/disable per-kernel CUDA-event timing inside the library."""
+    _check(lib().sq_profile(1 if enable else 0))
+
+
+def profile_read() -> dict:
+    """{role: (launches, total_ms)} accumulated since the last read."""
+    import json
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib().sq_profile_read(buf, len(buf)))
+    return {k: (int(v[0]), float(v[1])) for k, v in json.loads(buf.value.decode()).items()}

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -42,6 +44,66 @@ static void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error(SQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   g_stats.kernel_launches++;
+}
+
+// ------------------------------------------------------------------ per-kernel timing
+// When enabled (sq_profile), every launch is bracketed by CUDA events on its
+// stream; elapsed times accumulate per kernel role after the call's final sync.
+struct ProfEntry {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static std::atomic<bool> g_prof{false};
+static thread_local std::vector<ProfEntry> g_prof_pending;
+static thread_local std::vector<cudaEvent_t> g_event_pool;
+static std::mutex g_prof_mu;
+static std::map<std::string, std::pair<uint64_t, double>> g_prof_acc;
+static thread_local const char* g_role = "blocksort";
+
+static cudaEvent_t pool_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  SQ_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+struct ProfScope {
+  cudaStream_t st;
+  const char* name;
+  cudaEvent_t a = nullptr;
+  ProfScope(const char* n, cudaStream_t s) : st(s), name(n) {
+    if (g_prof.load()) {
+      a = pool_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = pool_event();
+      cudaEventRecord(b, st);
+      g_prof_pending.push_back({name, a, b});
+    }
+  }
+};
+
+static void prof_collect() {  // after a stream sync
+  if (g_prof_pending.empty()) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& e : g_prof_pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) {
+      auto& v = g_prof_acc[e.name];
+      v.first++;
+      v.second += ms;
+    }
+    g_event_pool.push_back(e.a);
+    g_event_pool.push_back(e.b);
+  }
+  g_prof_pending.clear();
 }
 
 // ------------------------------------------------------------------ options
@@ -157,6 +219,7 @@ static void launch_bs(uint32_t nseg, const SegDesc* d, const K* src, K* dst, cud
   using BS = BlockSort<K, NT, V>;
   static bool init = false;
   if (!init) { set_smem(k_blocksort<K, NT, V>, BS::SMEM_BYTES); init = true; }
+  ProfScope ps(g_role, st);
   k_blocksort<K, NT, V><<<nseg, NT, BS::SMEM_BYTES, st>>>(d, src, dst);
   check_launch("k_blocksort");
 }
@@ -168,6 +231,7 @@ static void launch_bsp(uint32_t nseg, const SegDesc* d, const uint32_t* ks, cons
   const size_t smem = BS::SMEM_BYTES + size_t(BS::TILE) * 4;
   static bool init = false;
   if (!init) { set_smem(k_blocksort_pairs<NT, V>, smem); init = true; }
+  ProfScope ps(g_role, st);
   k_blocksort_pairs<NT, V><<<nseg, NT, smem, st>>>(d, ks, vs, kd, vd);
   check_launch("k_blocksort_pairs");
 }
@@ -178,6 +242,7 @@ static void launch_sample(uint32_t ntask, const LevelSeg* segs, const TaskDesc* 
   using BS = BlockSort<K, NT, V>;
   static bool init = false;
   if (!init) { set_smem(k_sample<K, NT, V>, BS::SMEM_BYTES); init = true; }
+  ProfScope ps("sample", st);
   k_sample<K, NT, V><<<ntask, NT, BS::SMEM_BYTES, st>>>(segs, tasks, data, segmin, cand, flags, R);
   check_launch("k_sample");
 }
@@ -320,12 +385,13 @@ struct Engine {
   void copy_ranges(const std::vector<SegDesc>& r, int src, int dst) {
     if (r.empty() || src == dst) return;
     const SegDesc* d = ar.upload(r);
+    ProfScope ps("copy", st);
     k_copy_ranges<K><<<(uint32_t)r.size(), 256, 0, st>>>(d, kb[src], kb[dst], PAIRS ? vb[src] : nullptr,
                                                          PAIRS ? vb[dst] : nullptr);
     check_launch("k_copy_ranges");
   }
 
-  void sort_batch(const std::vector<Seg>& segs, int src, int dst, int depth) {
+  void sort_batch(const std::vector<Seg>& segs, int src, int dst, int depth, const char* role) {
     if (depth > 48) throw Error(SQ_ERR_CUDA, "recursion too deep");
     std::map<uint32_t, std::vector<SegDesc>> cls;
     std::vector<Seg> big;
@@ -336,6 +402,7 @@ struct Engine {
     }
     for (auto& kv : cls) {
       const SegDesc* d = ar.upload(kv.second);
+      g_role = role;
       if constexpr (PAIRS)
         blocksort_pairs(kv.first, (uint32_t)kv.second.size(), d, kb[src], vb[src], kb[dst], vb[dst], st);
       else
@@ -396,13 +463,16 @@ struct Engine {
     if (maxnp > key_max_tile<K>()) throw Error(SQ_ERR_INVALID_ARGUMENT, "pivot sample too large for one CTA");
 
     // 1. sort every column in place
-    sort_batch(cols, X, X, depth + 1);
+    sort_batch(cols, X, X, depth + 1, "colsort");
 
     LevelSeg* dL = ar.upload(L);
     // 2. min(D) from the column heads
     K* segmin = (K*)ar.alloc(ns * sizeof(K));
-    k_colmin<K><<<ns, 256, 0, st>>>(dL, kb[X], segmin);
-    check_launch("k_colmin");
+    {
+      ProfScope ps("colmin", st);
+      k_colmin<K><<<ns, 256, 0, st>>>(dL, kb[X], segmin);
+      check_launch("k_colmin");
+    }
     // 3. pivots
     K* cand = (K*)ar.alloc(std::max<uint64_t>(cand_tot, 1) * sizeof(K));
     uint8_t* flags = (uint8_t*)ar.alloc(uint64_t(ns) * kCap);
@@ -412,8 +482,11 @@ struct Engine {
                        kb[X], segmin, cand, flags, R, st);
     K* piv = (K*)ar.alloc(std::max<uint64_t>(piv_tot, 1) * sizeof(K));
     uint32_t* info = (uint32_t*)ar.alloc(ns * sizeof(uint32_t));
-    k_select<K><<<ns, 256, 0, st>>>(dL, cand, flags, piv, info, R);
-    check_launch("k_select");
+    {
+      ProfScope ps("select", st);
+      k_select<K><<<ns, 256, 0, st>>>(dL, cand, flags, piv, info, R);
+      check_launch("k_select");
+    }
     ar.release(cand);
     // 4. bucket sizes and tile boundaries
     uint32_t* segmat = (uint32_t*)ar.alloc(std::max<uint64_t>(segmat_tot, 1) * sizeof(uint32_t));
@@ -425,13 +498,17 @@ struct Engine {
       const size_t smem = CC::STAGE * sizeof(K) + CC::KSMEM * 4;
       static bool init = false;
       if (!init) { set_smem(k_count<K, CC::NT, CC::STAGE, CC::KSMEM>, smem); init = true; }
+      ProfScope ps("count", st);
       k_count<K, CC::NT, CC::STAGE, CC::KSMEM><<<(uint32_t)ctasks.size(), CC::NT, smem, st>>>(dL, dC, kb[X], piv,
                                                                                               segmat, cnt);
       check_launch("k_count");
     }
     uint8_t* bflag = (uint8_t*)ar.alloc(buck_tot);
-    k_bflags<K><<<ns, 256, 0, st>>>(dL, piv, bflag);
-    check_launch("k_bflags");
+    {
+      ProfScope ps("bflags", st);
+      k_bflags<K><<<ns, 256, 0, st>>>(dL, piv, bflag);
+      check_launch("k_bflags");
+    }
     // 5. read the sizes back and plan (one host sync per level)
     uint32_t* hcnt = (uint32_t*)ar.pinned(buck_tot * 4);
     uint8_t* hflag = (uint8_t*)ar.pinned(buck_tot);
@@ -473,6 +550,7 @@ struct Engine {
       static bool init = false;
       if (!init) { set_smem(f, CF::SMEM); init = true; }
       TaskDesc* dT = ar.upload(ttasks);
+      ProfScope ps("transpose", st);
       f<<<(uint32_t)ttasks.size(), TC::NT, CF::SMEM, st>>>(dL, dT, kb[X], kb[T], PAIRS ? vb[X] : nullptr,
                                                            PAIRS ? vb[T] : nullptr, piv, segmat, dstart);
       check_launch("k_transpose");
@@ -491,7 +569,7 @@ struct Engine {
       ar.release(p);
     // 7. buckets: single-value ones are copied, the rest sorted from T into dst
     copy_ranges(copies, T, dst);
-    sort_batch(buckets, T, dst, depth + 1);
+    sort_batch(buckets, T, dst, depth + 1, "bucketsort");
   }
 };
 
@@ -506,6 +584,7 @@ static int guarded(Fn&& fn) {
   g_stats = sq_stats{};
   try {
     fn();
+    prof_collect();
     return SQ_OK;
   } catch (const Error& e) {
     return fail(e);
@@ -530,7 +609,7 @@ static void sort_device(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaSt
   Arena ar(st);
   Engine<K, PAIRS> eng(st, ar, keys, vals, n);
   std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
-  eng.sort_batch(top, 0, 0, 0);
+  eng.sort_batch(top, 0, 0, 0, "smallsort");
   SQ_CUDA(cudaGetLastError());
 }
 
@@ -648,6 +727,7 @@ int sq_skew_transpose(const uint32_t* src, uint32_t* dst, size_t rows, size_t co
       static bool init = false;
       if (!init) { set_smem(k_count<uint32_t, CC::NT, CC::STAGE, CC::KSMEM>, smem); init = true; }
       TaskDesc* dC = ar.upload(ct);
+      ProfScope ps("count", st);
       k_count<uint32_t, CC::NT, CC::STAGE, CC::KSMEM><<<(uint32_t)ct.size(), CC::NT, smem, st>>>(dL, dC, src, piv,
                                                                                                  segmat, cnt);
       check_launch("k_count");
@@ -663,6 +743,9 @@ int sq_skew_transpose(const uint32_t* src, uint32_t* dst, size_t rows, size_t co
         start[b] = (uint32_t)pre;
         pre += hcnt[b];
       }
+    } else {
+      for (uint32_t b = 0; b < k; b++)
+        need(uint64_t(start[b]) + hcnt[b] <= n, "buc_in[j] + size_j exceeds n");
     }
     uint32_t* dstart = ar.upload(start);
     if (n > 0) {
@@ -672,6 +755,7 @@ int sq_skew_transpose(const uint32_t* src, uint32_t* dst, size_t rows, size_t co
       static bool init = false;
       if (!init) { set_smem(f, CF::SMEM); init = true; }
       TaskDesc* dT = ar.upload(tt);
+      ProfScope ps("transpose", st);
       f<<<(uint32_t)tt.size(), TC::NT, CF::SMEM, st>>>(dL, dT, src, dst, nullptr, nullptr, piv, segmat, dstart);
       check_launch("k_transpose");
     }
@@ -699,6 +783,30 @@ const char* sq_last_error_message(void) { return g_errmsg.c_str(); }
 
 void sq_get_stats(sq_stats* out) {
   if (out) *out = g_stats;
+}
+
+int sq_profile(int enable) {
+  g_prof.store(enable != 0);
+  return SQ_OK;
+}
+
+int sq_profile_read(char* buf, size_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::string out = "{";
+  bool first = true;
+  for (auto& kv : g_prof_acc) {
+    if (!first) out += ",";
+    first = false;
+    char tmp[256];
+    snprintf(tmp, sizeof tmp, "\"%s\":[%llu,%.6f]", kv.first.c_str(), (unsigned long long)kv.second.first,
+             kv.second.second);
+    out += tmp;
+  }
+  out += "}";
+  g_prof_acc.clear();
+  if (!buf || cap == 0) return SQ_ERR_INVALID_ARGUMENT;
+  snprintf(buf, cap, "%s", out.c_str());
+  return out.size() < cap ? SQ_OK : SQ_ERR_INVALID_ARGUMENT;
 }
 
 int sq_set_max_tile(uint32_t t) {
