@@ -154,14 +154,16 @@ int sq_set_max_tile(uint32_t max_tile);
 int sq_profile(int enable);
 int sq_profile_read(char *buf, size_t cap);
 
-/* One SquareSort level of u32 keys, stopped after the SkewTranspose (for
- * intermediate-state parity tests): src (device, n keys, unchanged) is copied,
- * its m = ceil(sqrt(n)) columns are sorted, pivots are sampled from the
- * sorted columns at node key mix(seed), and the SkewTranspose result
- * is written to dst (device, n keys).  pivots_out (device, m-1 entries),
- * bucend_out (device, m entries: the final cursors) and info_out
- * (device, 2 entries: accepted round, degenerate flag) may not be NULL.
- * Requires 5 <= n and m <= the maximum tile. */
+/* One SquareSort level of u32 keys as the sorts run it, stopped after the
+ * SkewTranspose (for intermediate-state parity tests): src (device, n keys,
+ * unchanged) is copied; pivots are sampled at node key mix(seed) from the level
+ * input (reading L9: before the column sort, P:279 draws from D), the
+ * m = ceil(sqrt(n)) columns are sorted, min-exclusion is applied, and
+ * the keys are moved into their buckets; dst (device, n keys) receives the
+ * paper's SkewTranspose result (bucket-contiguous, column order within a
+ * bucket).  pivots_out (device, m-1 entries), bucend_out (device, m entries:
+ * the final cursors) and info_out (device, 2 entries: accepted round,
+ * degenerate flag) may not be NULL.  Requires 5 <= n <= 2^30. */
 int sq_debug_level_u32(const uint32_t *src, uint32_t *dst, size_t n, uint64_t seed,
                        uint32_t *pivots_out, uint32_t *bucend_out, uint32_t *info_out,
                        void *stream);

@@ -19,7 +19,7 @@
 #include <vector>
 
 #include "../../include/squaresort.h"
-#include "level.cuh"
+#include "level2.cuh"
 
 namespace sq {
 
@@ -198,10 +198,11 @@ struct Arena {
 };
 
 // ------------------------------------------------------------------ size classes
-// Tiles (NT x V) for 32-bit keys and for 64-bit keys / pair composites.
+// On-chip tiles (threads x keys per thread) for 32-bit sort keys and for
+// 64-bit sort keys (u64 keys, pair composites).
 static const uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768};
 
-template <typename K> constexpr uint32_t key_max_tile() { return sizeof(K) == 4 ? 32768u : 16384u; }
+template <typename SK> constexpr uint32_t key_max_tile() { return sizeof(SK) == 4 ? 32768u : 16384u; }
 
 static uint32_t tile_for(uint32_t len) {
   for (uint32_t t : kTiles)
@@ -214,120 +215,59 @@ static void set_smem(F f, size_t bytes) {
   SQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-template <typename K, int NT, int V>
-static void launch_bs(uint32_t nseg, const SegDesc* d, const K* src, K* dst, cudaStream_t st) {
-  using BS = BlockSort<K, NT, V>;
-  static bool init = false;
-  if (!init) { set_smem(k_blocksort<K, NT, V>, BS::SMEM_BYTES); init = true; }
-  ProfScope ps(g_role, st);
-  k_blocksort<K, NT, V><<<nseg, NT, BS::SMEM_BYTES, st>>>(d, src, dst);
-  check_launch("k_blocksort");
-}
+template <int N> using IC = std::integral_constant<int, N>;
 
-template <int NT, int V>
-static void launch_bsp(uint32_t nseg, const SegDesc* d, const uint32_t* ks, const uint32_t* vs, uint32_t* kd,
-                       uint32_t* vd, cudaStream_t st) {
-  using BS = BlockSort<uint64_t, NT, V>;
-  const size_t smem = BS::SMEM_BYTES + size_t(BS::TILE) * 4;
-  static bool init = false;
-  if (!init) { set_smem(k_blocksort_pairs<NT, V>, smem); init = true; }
-  ProfScope ps(g_role, st);
-  k_blocksort_pairs<NT, V><<<nseg, NT, smem, st>>>(d, ks, vs, kd, vd);
-  check_launch("k_blocksort_pairs");
-}
-
-template <typename K, int NT, int V>
-static void launch_sample(uint32_t ntask, const LevelSeg* segs, const TaskDesc* tasks, const K* data,
-                          const K* segmin, K* cand, uint8_t* flags, uint32_t R, cudaStream_t st) {
-  using BS = BlockSort<K, NT, V>;
-  static bool init = false;
-  if (!init) { set_smem(k_sample<K, NT, V>, BS::SMEM_BYTES); init = true; }
-  ProfScope ps("sample", st);
-  k_sample<K, NT, V><<<ntask, NT, BS::SMEM_BYTES, st>>>(segs, tasks, data, segmin, cand, flags, R);
-  check_launch("k_sample");
-}
-
-// keys-only block sort dispatch
-template <typename K>
-static void blocksort_keys(uint32_t tile, uint32_t nseg, const SegDesc* d, const K* src, K* dst, cudaStream_t st) {
-  if constexpr (sizeof(K) == 4) {
+// f(IC<NT>, IC<V>) for the block shape of `tile` with sort key type SK.
+template <typename SK, typename F>
+static void with_tile(uint32_t tile, F&& f) {
+  if constexpr (sizeof(SK) == 4) {
     switch (tile) {
-      case 64: return launch_bs<K, 32, 2>(nseg, d, src, dst, st);
-      case 128: return launch_bs<K, 32, 4>(nseg, d, src, dst, st);
-      case 256: return launch_bs<K, 32, 8>(nseg, d, src, dst, st);
-      case 512: return launch_bs<K, 64, 8>(nseg, d, src, dst, st);
-      case 1024: return launch_bs<K, 128, 8>(nseg, d, src, dst, st);
-      case 2048: return launch_bs<K, 128, 16>(nseg, d, src, dst, st);
-      case 4096: return launch_bs<K, 256, 16>(nseg, d, src, dst, st);
-      case 8192: return launch_bs<K, 512, 16>(nseg, d, src, dst, st);
-      case 16384: return launch_bs<K, 512, 32>(nseg, d, src, dst, st);
-      case 32768: return launch_bs<K, 1024, 32>(nseg, d, src, dst, st);
+      case 64: return f(IC<32>{}, IC<2>{});
+      case 128: return f(IC<32>{}, IC<4>{});
+      case 256: return f(IC<32>{}, IC<8>{});
+      case 512: return f(IC<64>{}, IC<8>{});
+      case 1024: return f(IC<128>{}, IC<8>{});
+      case 2048: return f(IC<128>{}, IC<16>{});
+      case 4096: return f(IC<256>{}, IC<16>{});
+      case 8192: return f(IC<512>{}, IC<16>{});
+      case 16384: return f(IC<512>{}, IC<32>{});
+      case 32768: return f(IC<1024>{}, IC<32>{});
     }
   } else {
     switch (tile) {
-      case 64: return launch_bs<K, 32, 2>(nseg, d, src, dst, st);
-      case 128: return launch_bs<K, 32, 4>(nseg, d, src, dst, st);
-      case 256: return launch_bs<K, 32, 8>(nseg, d, src, dst, st);
-      case 512: return launch_bs<K, 64, 8>(nseg, d, src, dst, st);
-      case 1024: return launch_bs<K, 128, 8>(nseg, d, src, dst, st);
-      case 2048: return launch_bs<K, 256, 8>(nseg, d, src, dst, st);
-      case 4096: return launch_bs<K, 256, 16>(nseg, d, src, dst, st);
-      case 8192: return launch_bs<K, 512, 16>(nseg, d, src, dst, st);
-      case 16384: return launch_bs<K, 1024, 16>(nseg, d, src, dst, st);
+      case 64: return f(IC<32>{}, IC<2>{});
+      case 128: return f(IC<32>{}, IC<4>{});
+      case 256: return f(IC<32>{}, IC<8>{});
+      case 512: return f(IC<64>{}, IC<8>{});
+      case 1024: return f(IC<128>{}, IC<8>{});
+      case 2048: return f(IC<256>{}, IC<8>{});
+      case 4096: return f(IC<256>{}, IC<16>{});
+      case 8192: return f(IC<512>{}, IC<16>{});
+      case 16384: return f(IC<1024>{}, IC<16>{});
     }
   }
-  throw Error(SQ_ERR_CUDA, "no block sort class for tile " + std::to_string(tile));
+  throw Error(SQ_ERR_CUDA, "no block shape for tile " + std::to_string(tile));
 }
 
-static void blocksort_pairs(uint32_t tile, uint32_t nseg, const SegDesc* d, const uint32_t* ks, const uint32_t* vs,
-                            uint32_t* kd, uint32_t* vd, cudaStream_t st) {
-  switch (tile) {
-    case 64: return launch_bsp<32, 2>(nseg, d, ks, vs, kd, vd, st);
-    case 128: return launch_bsp<32, 4>(nseg, d, ks, vs, kd, vd, st);
-    case 256: return launch_bsp<32, 8>(nseg, d, ks, vs, kd, vd, st);
-    case 512: return launch_bsp<64, 8>(nseg, d, ks, vs, kd, vd, st);
-    case 1024: return launch_bsp<128, 8>(nseg, d, ks, vs, kd, vd, st);
-    case 2048: return launch_bsp<256, 8>(nseg, d, ks, vs, kd, vd, st);
-    case 4096: return launch_bsp<256, 16>(nseg, d, ks, vs, kd, vd, st);
-    case 8192: return launch_bsp<512, 16>(nseg, d, ks, vs, kd, vd, st);
-    case 16384: return launch_bsp<1024, 16>(nseg, d, ks, vs, kd, vd, st);
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    SQ_CUDA(cudaGetDevice(&dev));
+    SQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  throw Error(SQ_ERR_CUDA, "no pair sort class for tile " + std::to_string(tile));
+  return sms;
 }
 
-template <typename K>
-static void sample_dispatch(uint32_t tile, uint32_t ntask, const LevelSeg* segs, const TaskDesc* tasks,
-                            const K* data, const K* segmin, K* cand, uint8_t* flags, uint32_t R, cudaStream_t st) {
-  if constexpr (sizeof(K) == 4) {
-    switch (tile) {
-      case 64: return launch_sample<K, 32, 2>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 128: return launch_sample<K, 32, 4>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 256: return launch_sample<K, 32, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 512: return launch_sample<K, 64, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 1024: return launch_sample<K, 128, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 2048: return launch_sample<K, 128, 16>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 4096: return launch_sample<K, 256, 16>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 8192: return launch_sample<K, 512, 16>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 16384: return launch_sample<K, 512, 32>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 32768: return launch_sample<K, 1024, 32>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-    }
-  } else {
-    switch (tile) {
-      case 64: return launch_sample<K, 32, 2>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 128: return launch_sample<K, 32, 4>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 256: return launch_sample<K, 32, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 512: return launch_sample<K, 64, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 1024: return launch_sample<K, 128, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 2048: return launch_sample<K, 256, 8>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 4096: return launch_sample<K, 256, 16>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 8192: return launch_sample<K, 512, 16>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-      case 16384: return launch_sample<K, 1024, 16>(ntask, segs, tasks, data, segmin, cand, flags, R, st);
-    }
-  }
-  throw Error(SQ_ERR_CUDA, "no sampler class for tile " + std::to_string(tile));
+// One full wave of resident CTAs for a persistent kernel.
+template <typename F>
+static int wave_grid(F f, int nt, size_t smem) {
+  int occ = 0;
+  SQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, nt, smem));
+  return std::max(1, occ) * num_sms();
 }
 
-// count kernel configuration per key type
+// count kernel configuration per key type (standalone SkewTranspose)
 template <typename K> struct CountCfg;
 template <> struct CountCfg<uint32_t> { static constexpr int NT = 512, STAGE = 16384, KSMEM = 16384; };
 template <> struct CountCfg<uint64_t> { static constexpr int NT = 512, STAGE = 8192, KSMEM = 16384; };
@@ -337,15 +277,11 @@ template <typename K, bool PAIRS> struct TrCfg;
 template <> struct TrCfg<uint32_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
 template <> struct TrCfg<uint32_t, true> { static constexpr int NT = 256, S = 4096, G = 256; };
 template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
-
-// per-bucket single-value flag: bucket b >= 1 with P[b-1] == P[b]
-template <typename K>
-__global__ void k_bflags(const LevelSeg* __restrict__ segs, const K* __restrict__ piv, uint8_t* __restrict__ flag) {
-  const LevelSeg s = segs[blockIdx.x];
-  const K* P = piv + s.piv_base;
-  for (uint32_t b = threadIdx.x; b < s.k; b += blockDim.x)
-    flag[s.buck_base + b] = (b >= 1 && b + 1 < s.k && P[b - 1] == P[b]) ? 1 : 0;
-}
+// piece-major transpose (sort path): threads, piece size, fragments per piece
+template <typename K, bool PAIRS> struct PmTr;
+template <> struct PmTr<uint32_t, false> { static constexpr int NT = 512, S = 8192, F = 256; };
+template <> struct PmTr<uint32_t, true> { static constexpr int NT = 512, S = 4096, F = 256; };
+template <> struct PmTr<uint64_t, false> { static constexpr int NT = 512, S = 4096, F = 256; };
 
 // ------------------------------------------------------------------ the engine
 struct Seg {
@@ -354,6 +290,7 @@ struct Seg {
 };
 
 struct DebugOut {  // sq_debug_level_u32
+  uint32_t* dst;
   uint32_t* pivots;
   uint32_t* bucend;
   uint32_t* info;
@@ -361,6 +298,7 @@ struct DebugOut {  // sq_debug_level_u32
 
 template <typename K, bool PAIRS>
 struct Engine {
+  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;  // on-chip sort key
   cudaStream_t st;
   Arena& ar;
   K* kb[2];
@@ -373,7 +311,7 @@ struct Engine {
     kb[1] = nullptr;
     vb[0] = vals;
     vb[1] = nullptr;
-    cap = key_max_tile<typename std::conditional<PAIRS, uint64_t, K>::type>();
+    cap = key_max_tile<SK>();
     if (g_max_tile && g_max_tile < cap) cap = g_max_tile;
   }
 
@@ -391,50 +329,71 @@ struct Engine {
     check_launch("k_copy_ranges");
   }
 
+  // Contiguous segments of at most `cap` keys: one CTA each, by size class.
+  void blocksort(uint32_t tile, const std::vector<SegDesc>& d, int src, int dst, const char* role) {
+    const SegDesc* dd = ar.upload(d);
+    const uint32_t nseg = (uint32_t)d.size();
+    with_tile<SK>(tile, [&](auto nt, auto v) {
+      constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
+      using BS = BlockSort<SK, NT, V>;
+      ProfScope ps(role, st);
+      if constexpr (PAIRS) {
+        const size_t smem = BS::SMEM_BYTES + size_t(BS::TILE) * 4;
+        static bool init = false;
+        if (!init) { set_smem(k_blocksort_pairs<NT, V>, smem); init = true; }
+        k_blocksort_pairs<NT, V><<<nseg, NT, smem, st>>>(dd, kb[src], vb[src], kb[dst], vb[dst]);
+      } else {
+        static bool init = false;
+        if (!init) { set_smem(k_blocksort<K, NT, V>, BS::SMEM_BYTES); init = true; }
+        k_blocksort<K, NT, V><<<nseg, NT, BS::SMEM_BYTES, st>>>(dd, kb[src], kb[dst]);
+      }
+      check_launch("k_blocksort");
+    });
+  }
+
   void sort_batch(const std::vector<Seg>& segs, int src, int dst, int depth, const char* role) {
     if (depth > 48) throw Error(SQ_ERR_CUDA, "recursion too deep");
     std::map<uint32_t, std::vector<SegDesc>> cls;
     std::vector<Seg> big;
+    std::vector<SegDesc> bigr;
     for (const Seg& s : segs) {
       if (s.len == 0) continue;
-      if (s.len > cap) big.push_back(s);
-      else cls[tile_for(s.len)].push_back({s.off, s.len});
+      if (s.len > cap) {
+        big.push_back(s);
+        bigr.push_back({s.off, s.len});
+      } else {
+        cls[std::max<uint32_t>(64, tile_for(s.len))].push_back({s.off, s.len});
+      }
     }
-    for (auto& kv : cls) {
-      const SegDesc* d = ar.upload(kv.second);
-      g_role = role;
-      if constexpr (PAIRS)
-        blocksort_pairs(kv.first, (uint32_t)kv.second.size(), d, kb[src], vb[src], kb[dst], vb[dst], st);
-      else
-        blocksort_keys<K>(kv.first, (uint32_t)kv.second.size(), d, kb[src], kb[dst], st);
-    }
+    for (auto& kv : cls) blocksort(kv.first, kv.second, src, dst, role);
     if (!big.empty()) {
-      uint64_t ok = 0;
-      for (auto& b : big) ok += b.len;
-      if (depth > 0) g_stats.oversize_keys += ok;
-      run_level(big, src, dst, depth, nullptr);
+      copy_ranges(bigr, src, dst);  // a level sorts a segment where it will end up
+      run_level(big, dst, depth, nullptr);
     }
   }
 
-  // One SquareSort level for a batch of segments living in buffer X; the
-  // sorted result goes to buffer `dst`.  The SkewTranspose writes into the
-  // other buffer T (each segment's range there is free).
-  void run_level(const std::vector<Seg>& segs, int X, int dst, int depth, DebugOut* dbg) {
+  // One SquareSort level (Alg 1) for a batch of segments that live in buffer X,
+  // their final place.  The SkewTranspose writes into the other buffer T; the
+  // bucket sorts gather from T and write the sorted buckets back into X.
+  void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
+    using TC = PmTr<K, PAIRS>;
+    using CF = PmCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
     ensure_scratch();
     g_stats.levels++;
     const int T = 1 - X;
     const uint32_t ns = (uint32_t)segs.size();
-    const uint32_t R = ns == 1 ? kCap : (ns <= 16 ? 4 : 2);
     std::vector<LevelSeg> L(ns);
-    std::vector<Seg> cols;
-    std::vector<TaskDesc> ctasks, stasks, ttasks;
-    uint64_t piv_tot = 0, buck_tot = 0, segmat_tot = 0, cand_tot = 0, totcols = 0;
+    std::vector<uint32_t> tile_base(ns), piece_seg_base(ns);
+    std::vector<TileInfo> tiles;
+    std::map<uint32_t, std::vector<ColDesc>> colcls;
+    std::vector<Seg> allcols;
+    std::vector<TaskDesc> mtasks;
+    bool generic = false;
+    uint64_t piv_tot = 0, buck_tot = 0, segmat_tot = 0, cand_tot = 0, piece_tot = 0;
     uint32_t maxnp = 0;
-    for (uint32_t s = 0; s < ns; s++) totcols += ceil_sqrt(segs[s].len);
-    const uint64_t cg = std::max<uint64_t>(1, (totcols + 295) / 296);
     for (uint32_t s = 0; s < ns; s++) {
       const Seg& g = segs[s];
-      const uint32_t m = (uint32_t)ceil_sqrt(g.len);
+      const uint32_t m = (uint32_t)ceil_sqrt(g.len);  // P:240
       LevelSeg& l = L[s];
       l.off = g.off;
       l.len = g.len;
@@ -450,126 +409,215 @@ struct Engine {
       piv_tot += np;
       buck_tot += m;
       segmat_tot += uint64_t(m) * (l.nbt + 1);
-      cand_tot += uint64_t(R + 1) * np;
-      for (uint32_t c = 0; c < m; c++) {
+      cand_tot += uint64_t(kCap) * np;
+      tile_base[s] = (uint32_t)tiles.size();
+      for (uint32_t bt = 0; bt < l.nbt; bt++) tiles.push_back({s, bt, 0, 0, 0, 0});
+      const uint32_t gpt = (m + TC::F - 1) / TC::F;
+      piece_seg_base[s] = (uint32_t)piece_tot;
+      piece_tot += g.len / TC::S + uint64_t(l.nbt) * (1 + gpt) + 1;
+      for (uint32_t c = 0; c < m; c++) {  // P:271
         const uint64_t a = uint64_t(c) * m;
-        if (a < g.len) cols.push_back({uint32_t(g.off + a), uint32_t(std::min<uint64_t>(m, g.len - a)),
-                                       child_key(g.node, 0, c)});
+        if (a >= g.len) break;
+        const uint32_t lc = (uint32_t)std::min<uint64_t>(m, g.len - a);
+        allcols.push_back({uint32_t(g.off + a), lc, child_key(g.node, 0, c)});
+        if (lc > cap) generic = true;
+        colcls[std::max<uint32_t>(64, tile_for(lc))].push_back({uint32_t(g.off + a), lc, s, c});
       }
-      for (uint32_t j = 0; j < R; j++) stasks.push_back({s, j, 0});
-      for (uint32_t c0 = 0; c0 < m; c0 += (uint32_t)cg) ctasks.push_back({s, c0, (uint32_t)std::min<uint64_t>(m, c0 + cg)});
-      for (uint32_t bt = 0; bt < l.nbt; bt++) ttasks.push_back({s, bt, 0});
+      for (uint32_t c0 = 0; c0 < m; c0 += 64) mtasks.push_back({s, c0, std::min(m, c0 + 64)});
     }
     if (maxnp > key_max_tile<K>()) throw Error(SQ_ERR_INVALID_ARGUMENT, "pivot sample too large for one CTA");
-
-    // 1. sort every column in place
-    sort_batch(cols, X, X, depth + 1, "colsort");
+    const uint32_t ntiles = (uint32_t)tiles.size();
 
     LevelSeg* dL = ar.upload(L);
-    // 2. min(D) from the column heads
-    K* segmin = (K*)ar.alloc(ns * sizeof(K));
-    {
-      ProfScope ps("colmin", st);
-      k_colmin<K><<<ns, 256, 0, st>>>(dL, kb[X], segmin);
-      check_launch("k_colmin");
-    }
-    // 3. pivots
+    TileInfo* dTiles = ar.upload(tiles);
+    uint32_t* dTileBase = ar.upload(tile_base);
+    uint32_t* dPieceBase = ar.upload(piece_seg_base);
+    TaskDesc* dM = ar.upload(mtasks);
     K* cand = (K*)ar.alloc(std::max<uint64_t>(cand_tot, 1) * sizeof(K));
     uint8_t* flags = (uint8_t*)ar.alloc(uint64_t(ns) * kCap);
-    SQ_CUDA(cudaMemsetAsync(flags, 0, uint64_t(ns) * kCap, st));
-    TaskDesc* dS = ar.upload(stasks);
-    sample_dispatch<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), (uint32_t)stasks.size(), dL, dS,
-                       kb[X], segmin, cand, flags, R, st);
+    K* p0s = (K*)ar.alloc(uint64_t(ns) * kCap * sizeof(K));
     K* piv = (K*)ar.alloc(std::max<uint64_t>(piv_tot, 1) * sizeof(K));
-    uint32_t* info = (uint32_t*)ar.alloc(ns * sizeof(uint32_t));
+    uint32_t* info = (uint32_t*)ar.alloc(ns * 4);
+    uint32_t* fix = (uint32_t*)ar.alloc((ns + 1) * 4);
+    K* segmin = (K*)ar.alloc(ns * sizeof(K));
+    uint32_t* segmat = (uint32_t*)ar.alloc(segmat_tot * 4);
+    uint32_t* pout = (uint32_t*)ar.alloc(piece_tot * 4);
+    uint16_t* ppre = (uint16_t*)ar.alloc(piece_tot * kPP * 2);
+    BucketRec* recs = (BucketRec*)ar.alloc(buck_tot * sizeof(BucketRec));
+    SQ_CUDA(cudaMemsetAsync(fix, 0, (ns + 1) * 4, st));
+    SQ_CUDA(cudaMemsetAsync(segmin, 0xff, ns * sizeof(K), st));
+    SQ_CUDA(cudaMemsetAsync(segmat, 0, segmat_tot * 4, st));
+
+    // 1. pivots: all rounds in parallel from the level input (L9)
+    with_tile<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
+      constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
+      using BS = BlockSort<K, NT, V>;
+      static bool init = false;
+      if (!init) { set_smem(k_sample_all<K, NT, V>, BS::SMEM_BYTES); init = true; }
+      ProfScope ps("sample", st);
+      k_sample_all<K, NT, V><<<ns * kCap, NT, BS::SMEM_BYTES, st>>>(dL, kb[X], cand, flags, p0s);
+      check_launch("k_sample_all");
+    });
     {
       ProfScope ps("select", st);
-      k_select<K><<<ns, 256, 0, st>>>(dL, cand, flags, piv, info, R);
-      check_launch("k_select");
+      k_select_round<K><<<ns, 256, 0, st>>>(dL, ns, cand, flags, p0s, segmin, piv, info, fix, 0);
+      check_launch("k_select_round");
+    }
+    // 2. sort every column in place + tile boundaries + min(D)
+    if (!generic) {
+      for (auto& kv : colcls) {
+        const ColDesc* dc = ar.upload(kv.second);
+        with_tile<SK>(kv.first, [&](auto nt, auto v) {
+          constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
+          using BS = BlockSort<SK, NT, V>;
+          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
+          static bool init = false;
+          if (!init) { set_smem(k_colsort<K, NT, V, PAIRS>, smem); init = true; }
+          ProfScope ps("colsort", st);
+          k_colsort<K, NT, V, PAIRS><<<(uint32_t)kv.second.size(), NT, smem, st>>>(
+              dc, dL, kb[X], PAIRS ? vb[X] : nullptr, piv, segmat, segmin);
+          check_launch("k_colsort");
+        });
+      }
+    } else {  // columns longer than a CTA holds: a recursive level sorts them
+      sort_batch(allcols, X, X, depth + 1, "colsort");
+      {
+        ProfScope ps("colmin", st);
+        k_colmin<K><<<ns, 256, 0, st>>>(dL, kb[X], segmin);
+        check_launch("k_colmin");
+      }
+      {
+        ProfScope ps("segmat", st);
+        k_segmat<K><<<(uint32_t)mtasks.size(), 256, 0, st>>>(dL, dM, kb[X], piv, segmat, fix, 0);
+        check_launch("k_segmat");
+      }
+    }
+    // 3. min-exclusion: final round; repair the boundaries if it changed
+    {
+      ProfScope ps("select", st);
+      k_select_round<K><<<ns, 256, 0, st>>>(dL, ns, cand, flags, p0s, segmin, piv, info, fix, 1);
+      check_launch("k_select_round");
+    }
+    {
+      ProfScope ps("segmat", st);
+      k_segmat<K><<<(uint32_t)mtasks.size(), 256, 0, st>>>(dL, dM, kb[X], piv, segmat, fix, 1);
+      check_launch("k_segmat");
     }
     ar.release(cand);
-    // 4. bucket sizes and tile boundaries
-    uint32_t* segmat = (uint32_t*)ar.alloc(std::max<uint64_t>(segmat_tot, 1) * sizeof(uint32_t));
-    uint32_t* cnt = (uint32_t*)ar.alloc(buck_tot * sizeof(uint32_t));
-    SQ_CUDA(cudaMemsetAsync(cnt, 0, buck_tot * sizeof(uint32_t), st));
-    TaskDesc* dC = ar.upload(ctasks);
+    // 4. tile sizes and offsets, then the SkewTranspose X -> T
     {
-      using CC = CountCfg<K>;
-      const size_t smem = CC::STAGE * sizeof(K) + CC::KSMEM * 4;
-      static bool init = false;
-      if (!init) { set_smem(k_count<K, CC::NT, CC::STAGE, CC::KSMEM>, smem); init = true; }
-      ProfScope ps("count", st);
-      k_count<K, CC::NT, CC::STAGE, CC::KSMEM><<<(uint32_t)ctasks.size(), CC::NT, smem, st>>>(dL, dC, kb[X], piv,
-                                                                                              segmat, cnt);
-      check_launch("k_count");
+      ProfScope ps("tiles", st);
+      k_tile_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, segmat);
+      check_launch("k_tile_sizes");
+      k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, TC::F, dPieceBase);
+      check_launch("k_tile_scan");
     }
-    uint8_t* bflag = (uint8_t*)ar.alloc(buck_tot);
     {
-      ProfScope ps("bflags", st);
-      k_bflags<K><<<ns, 256, 0, st>>>(dL, piv, bflag);
-      check_launch("k_bflags");
-    }
-    // 5. read the sizes back and plan (one host sync per level)
-    uint32_t* hcnt = (uint32_t*)ar.pinned(buck_tot * 4);
-    uint8_t* hflag = (uint8_t*)ar.pinned(buck_tot);
-    uint32_t* hinfo = (uint32_t*)ar.pinned(ns * 4);
-    SQ_CUDA(cudaMemcpyAsync(hcnt, cnt, buck_tot * 4, cudaMemcpyDeviceToHost, st));
-    SQ_CUDA(cudaMemcpyAsync(hflag, bflag, buck_tot, cudaMemcpyDeviceToHost, st));
-    SQ_CUDA(cudaMemcpyAsync(hinfo, info, ns * 4, cudaMemcpyDeviceToHost, st));
-    SQ_CUDA(cudaStreamSynchronize(st));
-    g_stats.host_syncs++;
-    SQ_CUDA(cudaGetLastError());
-    if (depth == 0) {
-      g_stats.top_round = hinfo[0] & 0x7fffffffu;
-      g_stats.top_degenerate = hinfo[0] >> 31;
-      g_stats.top_m = L[0].k;
-    }
-    std::vector<uint32_t> bstart(buck_tot);
-    std::vector<Seg> buckets;
-    std::vector<SegDesc> copies;
-    for (uint32_t s = 0; s < ns; s++) {
-      uint64_t pre = L[s].off;
-      for (uint32_t b = 0; b < L[s].k; b++) {
-        const uint64_t i = L[s].buck_base + b;
-        bstart[i] = (uint32_t)pre;
-        const uint32_t c = hcnt[i];
-        if (c) {
-          if (hflag[i]) copies.push_back({(uint32_t)pre, c});  // single-value bucket: no recursion
-          else buckets.push_back({(uint32_t)pre, c, child_key(L[s].node, 1, b)});
-        }
-        pre += c;
-      }
-      if (pre != uint64_t(L[s].off) + L[s].len) throw Error(SQ_ERR_CUDA, "bucket sizes do not add up");
-    }
-    uint32_t* dstart = ar.upload(bstart);
-    // 6. SkewTranspose X -> T
-    {
-      using TC = TrCfg<K, PAIRS>;
-      using CF = TransposeCfg<K, PAIRS, TC::NT, TC::S, TC::G>;
-      auto f = k_transpose<K, PAIRS, TC::NT, TC::S, TC::G>;
+      auto f = k_transpose_pm<K, PAIRS, TC::NT, TC::S, TC::F>;
       static bool init = false;
       if (!init) { set_smem(f, CF::SMEM); init = true; }
-      TaskDesc* dT = ar.upload(ttasks);
       ProfScope ps("transpose", st);
-      f<<<(uint32_t)ttasks.size(), TC::NT, CF::SMEM, st>>>(dL, dT, kb[X], kb[T], PAIRS ? vb[X] : nullptr,
-                                                           PAIRS ? vb[T] : nullptr, piv, segmat, dstart);
-      check_launch("k_transpose");
+      f<<<ntiles, TC::NT, CF::SMEM, st>>>(dL, dTiles, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr,
+                                          piv, segmat, pout, ppre);
+      check_launch("k_transpose_pm");
+    }
+    // 5. bucket plan: sizes, final offsets, work lists
+    PlanOut po{};
+    po.ncls = 0;
+    for (uint32_t t : kTiles)
+      if (t <= cap && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
+    po.max_tile = cap;
+    po.cap_per_list = (uint32_t)buck_tot;
+    po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 2) * buck_tot * 4);
+    po.count = (uint32_t*)ar.alloc((po.ncls + 2) * 4);
+    SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 2) * 4, st));
+    {
+      ProfScope ps("plan", st);
+      uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
+      k_bucket_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, ppre, bsize);
+      check_launch("k_bucket_sizes");
+      k_bucket_plan<K><<<ns, 1024, 0, st>>>(dL, dTileBase, bsize, piv, recs, po);
+      check_launch("k_bucket_plan");
     }
     if (dbg) {
+      k_bucket_gather<K, 256><<<1024, 256, 0, st>>>(recs, dTiles, nullptr, nullptr, (uint32_t)buck_tot, kb[T],
+                                                    (K*)dbg->dst, nullptr, nullptr, pout, ppre);
+      check_launch("k_bucket_gather");
+      std::vector<BucketRec> hr(buck_tot);
+      std::vector<uint32_t> hinfo(ns);
+      SQ_CUDA(cudaMemcpyAsync(hr.data(), recs, buck_tot * sizeof(BucketRec), cudaMemcpyDeviceToHost, st));
+      SQ_CUDA(cudaMemcpyAsync(hinfo.data(), info, ns * 4, cudaMemcpyDeviceToHost, st));
       SQ_CUDA(cudaMemcpyAsync(dbg->pivots, piv, piv_tot * sizeof(K), cudaMemcpyDeviceToDevice, st));
+      SQ_CUDA(cudaStreamSynchronize(st));
       std::vector<uint32_t> be(buck_tot), inf = {hinfo[0] & 0x7fffffffu, hinfo[0] >> 31};
-      for (uint64_t i = 0; i < buck_tot; i++) be[i] = bstart[i] + hcnt[i];
+      for (uint64_t i = 0; i < buck_tot; i++) be[i] = hr[i].out + hr[i].size;
       uint32_t* dbe = ar.upload(be);
       uint32_t* dinf = ar.upload(inf);
       SQ_CUDA(cudaMemcpyAsync(dbg->bucend, dbe, buck_tot * 4, cudaMemcpyDeviceToDevice, st));
       SQ_CUDA(cudaMemcpyAsync(dbg->info, dinf, 8, cudaMemcpyDeviceToDevice, st));
       return;
     }
-    for (void* p : {(void*)segmat, (void*)cnt, (void*)piv, (void*)segmin, (void*)flags, (void*)info, (void*)bflag})
+    // 6. bucket sorts: gather from T, sort on chip, write to X
+    for (uint32_t c = 0; c < po.ncls; c++) {
+      const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
+      with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
+        constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
+        using BS = BlockSort<SK, NT, V>;
+        const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4;
+        auto f = k_bucketsort<K, NT, V, PAIRS>;
+        static int grid = 0;
+        if (!grid) {
+          set_smem(f, smem);
+          grid = wave_grid(f, NT, smem);
+        }
+        ProfScope ps("bucketsort", st);
+        f<<<(uint32_t)std::min<uint64_t>(grid, buck_tot), NT, smem, st>>>(recs, dTiles, lst, po.count + c, kb[T],
+                                                                         kb[X], PAIRS ? vb[T] : nullptr,
+                                                                         PAIRS ? vb[X] : nullptr, pout, ppre);
+        check_launch("k_bucketsort");
+      });
+    }
+    {  // single-value buckets (copied) and oversize buckets (made contiguous)
+      ProfScope ps("gather", st);
+      const uint32_t g = (uint32_t)std::min<uint64_t>(buck_tot, 4 * num_sms());
+      for (uint32_t c = po.ncls; c < po.ncls + 2; c++) {
+        k_bucket_gather<K, 256><<<g, 256, 0, st>>>(recs, dTiles, po.list + uint64_t(c) * po.cap_per_list,
+                                                   po.count + c, 0, kb[T], kb[X], PAIRS ? vb[T] : nullptr,
+                                                   PAIRS ? vb[X] : nullptr, pout, ppre);
+        check_launch("k_bucket_gather");
+      }
+    }
+    // 7. one host read per level: the oversize list (and the round, for stats)
+    uint32_t* hcnt = (uint32_t*)ar.pinned((po.ncls + 2) * 4);
+    uint32_t* hinfo = (uint32_t*)ar.pinned(4);
+    SQ_CUDA(cudaMemcpyAsync(hcnt, po.count, (po.ncls + 2) * 4, cudaMemcpyDeviceToHost, st));
+    SQ_CUDA(cudaMemcpyAsync(hinfo, info, 4, cudaMemcpyDeviceToHost, st));
+    SQ_CUDA(cudaStreamSynchronize(st));
+    g_stats.host_syncs++;
+    if (depth == 0) {
+      g_stats.top_round = hinfo[0] & 0x7fffffffu;
+      g_stats.top_degenerate = hinfo[0] >> 31;
+      g_stats.top_m = L[0].k;
+    }
+    const uint32_t nos = hcnt[po.ncls + 1];
+    std::vector<Seg> over;
+    if (nos) {
+      std::vector<uint32_t> hl(nos);
+      SQ_CUDA(cudaMemcpyAsync(hl.data(), po.list + uint64_t(po.ncls + 1) * po.cap_per_list, nos * 4,
+                              cudaMemcpyDeviceToHost, st));
+      std::vector<BucketRec> hr(buck_tot);
+      SQ_CUDA(cudaMemcpyAsync(hr.data(), recs, buck_tot * sizeof(BucketRec), cudaMemcpyDeviceToHost, st));
+      SQ_CUDA(cudaStreamSynchronize(st));
+      g_stats.host_syncs++;
+      for (uint32_t i : hl) {
+        over.push_back({hr[i].out, hr[i].size, hr[i].node});
+        g_stats.oversize_keys += hr[i].size;
+      }
+    }
+    for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)piv,
+                    (void*)flags, (void*)p0s, (void*)info, (void*)fix, (void*)segmin})
       ar.release(p);
-    // 7. buckets: single-value ones are copied, the rest sorted from T into dst
-    copy_ranges(copies, T, dst);
-    sort_batch(buckets, T, dst, depth + 1, "bucketsort");
+    if (!over.empty()) sort_batch(over, X, X, depth + 1, "bucketsort");
   }
 };
 
@@ -831,10 +879,9 @@ int sq_debug_level_u32(const uint32_t* src, uint32_t* dst, size_t n, uint64_t se
     uint32_t* work = (uint32_t*)ar.alloc(n * 4);
     SQ_CUDA(cudaMemcpyAsync(work, src, n * 4, cudaMemcpyDeviceToDevice, st));
     Engine<uint32_t, false> eng(st, ar, work, nullptr, n);
-    eng.kb[1] = dst;
-    DebugOut dbg{pivots_out, bucend_out, info_out};
+    DebugOut dbg{dst, pivots_out, bucend_out, info_out};
     std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
-    eng.run_level(top, 0, 0, 0, &dbg);
+    eng.run_level(top, 0, 0, &dbg);
     SQ_CUDA(cudaStreamSynchronize(st));
   });
 }

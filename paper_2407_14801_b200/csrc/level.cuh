@@ -222,7 +222,7 @@ struct TransposeCfg {
   static constexpr size_t off_rsrc = al(off_run + (G + 1) * 4);
   static constexpr size_t off_wsum = al(off_rsrc + G * 4);  // NW x 32 u32
   static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);
-  static constexpr size_t off_bval = al(off_misc + (64 + 4 * kTB) * 4);
+  static constexpr size_t off_bval = al(off_misc + (64 + 5 * kTB + 8) * 4);
   static constexpr size_t SMEM = al(off_bval + kTB * sizeof(K));
 };
 

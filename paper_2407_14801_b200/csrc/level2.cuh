@@ -1,0 +1,758 @@
+// level2.cuh -- the fused, host-sync-light SquareSort level used by the sorts.
+//
+// Differences from the paper's sequential structure, none of
+// which changes the sorted result:
+//  * pivots are sampled from the level input before its columns are sorted
+//    (reading L9: same distribution of pivot sets), all 32 rounds in parallel,
+//    so the column sort can emit the bucket-tile boundaries of every column in
+//    its epilogue (no separate bucket-count pass);
+//  * min-exclusion is checked after the column sort (it needs min(D));
+//    in the rare case it rejects the tentative round, the tile boundaries are
+//    recomputed from the sorted columns;
+//  * SkewTranspose writes each bucket tile "piece-major": pieces of S keys, each
+//    the stable bucket-major partition of S consecutive keys of the tile's
+//    column-major stream.  A bucket is the concatenation, in piece order, of its
+//    sub-chunk in every piece of its tile -- exactly the paper's bucket in the
+//    paper's order (column order, then row), only not yet contiguous; the bucket
+//    sort gathers the sub-chunks on chip and writes the sorted bucket to its
+//    final position, so no bucket sizes are needed before the transpose.
+#pragma once
+#include <type_traits>
+#include "level.cuh"
+
+namespace sq {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <typename K>
+__device__ __forceinline__ void cp_async_elem(K* sdst, const K* gsrc) {
+  if constexpr (sizeof(K) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_addr(sdst)), "l"(gsrc));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr(sdst)), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Per-tile bookkeeping of the piece-major transpose.
+struct TileInfo {
+  uint32_t seg, bt;      // segment and bucket tile
+  uint32_t out;          // absolute output offset of the tile's region
+  uint32_t size;         // keys in the tile
+  uint32_t piece_base;   // first entry in the piece tables
+  uint32_t npieces;      // pieces written (set by the transpose)
+};
+
+// Per-bucket record for the bucket phase.
+struct BucketRec {
+  uint32_t tile;   // tile index (TileInfo)
+  uint32_t lane;   // bucket index within the tile (0..31)
+  uint32_t out;    // absolute final offset of the sorted bucket
+  uint32_t size;
+  uint64_t node;   // RNG node key of the bucket (child(node, 1, b)), for deeper levels
+};
+
+constexpr int kPP = kTB + 1;  // prefix entries per piece
+
+// ------------------------------------------------------------------------------
+// All kCap sampling rounds of every segment in parallel (CTA = (segment, round)),
+// drawn from the level input A before the column sort (L9).  Stores the sorted
+// candidates, whether they are strictly increasing, and their smallest value.
+template <typename K, int NT, int V>
+__global__ void __launch_bounds__(NT)
+k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* __restrict__ cand,
+             uint8_t* __restrict__ flags, K* __restrict__ p0s) {
+  using BS = BlockSort<K, NT, V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* s = reinterpret_cast<K*>(smem_raw);
+  const uint32_t seg = blockIdx.x / kCap, r = blockIdx.x % kCap;
+  const LevelSeg sg = segs[seg];
+  const uint32_t np = sg.k - 1;
+  const K* lvl = data + sg.off;
+  for (int i = threadIdx.x; i < BS::TILE; i += NT) {
+    K x = KeyTraits<K>::kMax;
+    if (i < (int)np) x = lvl[draw_index(draw(sg.node, r, (uint32_t)i), sg.len)];
+    s[BS::pad(i)] = x;
+  }
+  __syncthreads();
+  BS::sort_smem(s);
+  int viol = 0;
+  for (int i = threadIdx.x + 1; i < (int)np; i += NT)
+    if (!(s[BS::pad(i - 1)] < s[BS::pad(i)])) viol = 1;
+  const bool distinct = !__syncthreads_or(viol);
+  K* out = cand + sg.cand_base + uint64_t(r) * np;
+  for (int i = threadIdx.x; i < (int)np; i += NT) out[i] = s[BS::pad(i)];
+  if (threadIdx.x == 0) {
+    flags[uint64_t(seg) * kCap + r] = distinct ? 1 : 2;
+    p0s[uint64_t(seg) * kCap + r] = np ? s[BS::pad(0)] : KeyTraits<K>::kMax;
+  }
+}
+
+// Round selection.  mode 0 (before the column sort): the
+// first strictly increasing round -- tentative.  mode 1 (after): the first round
+// that is strictly increasing AND whose smallest pivot exceeds min(D); none ->
+// degenerate (round cap-1).  When the final round differs from the tentative
+// one, the pivots are replaced and fix[seg] / fix[nseg] are raised so the tile
+// boundaries get recomputed.  info = round | degenerate << 31.
+template <typename K>
+__global__ void k_select_round(const LevelSeg* __restrict__ segs, uint32_t nseg, const K* __restrict__ cand,
+                               const uint8_t* __restrict__ flags, const K* __restrict__ p0s,
+                               const K* __restrict__ segmin, K* __restrict__ piv, uint32_t* __restrict__ info,
+                               uint32_t* __restrict__ fix, int mode) {
+  const uint32_t seg = blockIdx.x;
+  const LevelSeg sg = segs[seg];
+  __shared__ uint32_t sel, change;
+  if (threadIdx.x == 0) {
+    uint32_t r = kCap;
+    for (uint32_t q = 0; q < kCap; q++) {
+      const bool ok = flags[uint64_t(seg) * kCap + q] == 1 &&
+                      (mode == 0 || sg.k == 1 || p0s[uint64_t(seg) * kCap + q] > segmin[seg]);
+      if (ok) { r = q; break; }
+    }
+    const uint32_t inf = r < kCap ? r : ((kCap - 1) | 0x80000000u);
+    change = mode == 0 || info[seg] != inf;
+    if (mode == 1 && change) {
+      fix[seg] = 1;
+      fix[nseg] = 1;
+    }
+    info[seg] = inf;
+    sel = r < kCap ? r : kCap - 1;
+  }
+  __syncthreads();
+  if (!change) return;
+  const uint32_t np = sg.k - 1;
+  const K* in = cand + sg.cand_base + uint64_t(sel) * np;
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) piv[sg.piv_base + i] = in[i];
+}
+
+// ------------------------------------------------------------------------------
+// Column sort with the fused epilogue: each CTA sorts one column on chip (the
+// m T(m) term) and, from the sorted column in shared memory, writes the
+// position of every bucket-tile boundary (every kTB-th bucket, with the
+// equal-pivot rule) and folds the column head into min(D).
+struct ColDesc {
+  uint32_t off, len, seg, col;
+};
+
+template <typename K, int NT, int V, bool PAIRS>
+__global__ void __launch_bounds__(NT)
+k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K* __restrict__ keys,
+          uint32_t* __restrict__ vals, const K* __restrict__ piv, uint32_t* __restrict__ segmat,
+          K* __restrict__ segmin) {
+  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using BS = BlockSort<SK, NT, V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SK* s = reinterpret_cast<SK*>(smem_raw);
+  uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  const ColDesc d = cols[blockIdx.x];
+  const LevelSeg sg = segs[d.seg];
+  for (int i = threadIdx.x; i < BS::TILE; i += NT) {
+    SK x = KeyTraits<SK>::kMax;
+    if (i < (int)d.len) {
+      if constexpr (PAIRS) {
+        x = (uint64_t(keys[d.off + i]) << 32) | uint32_t(i);
+        vs[i] = vals[d.off + i];
+      } else {
+        x = keys[d.off + i];
+      }
+    }
+    s[BS::pad(i)] = x;
+  }
+  __syncthreads();
+  BS::sort_smem(s);
+  auto key_at = [&](int i) -> K {
+    if constexpr (PAIRS) return K(s[BS::pad(i)] >> 32);
+    else return s[BS::pad(i)];
+  };
+  for (int i = threadIdx.x; i < (int)d.len; i += NT) {
+    const SK x = s[BS::pad(i)];
+    if constexpr (PAIRS) {
+      keys[d.off + i] = uint32_t(x >> 32);
+      vals[d.off + i] = vs[uint32_t(x)];
+    } else {
+      keys[d.off + i] = x;
+    }
+  }
+  // epilogue: tile boundaries of this column
+  const K* P = piv + sg.piv_base;
+  uint32_t* row = segmat + sg.segmat_base + uint64_t(d.col) * (sg.nbt + 1);
+  for (uint32_t bt = threadIdx.x; bt <= sg.nbt; bt += NT) {
+    uint32_t pos;
+    const uint32_t j = bt * kTB;  // boundary index (bucket j starts here)
+    if (bt == 0) pos = 0;
+    else if (j >= sg.k) pos = d.len;
+    else {
+      const K pj = P[j - 1];
+      const bool dup = j >= 2 && P[j - 2] == pj;
+      uint32_t lo = 0, hi = d.len;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (before_boundary(key_at(mid), pj, dup)) lo = mid + 1; else hi = mid;
+      }
+      pos = lo;
+    }
+    row[bt] = pos;
+  }
+  if (threadIdx.x == 0 && d.len) {
+    if constexpr (sizeof(K) == 4) atomicMin((unsigned int*)&segmin[d.seg], (unsigned int)key_at(0));
+    else atomicMin((unsigned long long*)&segmin[d.seg], (unsigned long long)key_at(0));
+  }
+}
+
+// Tile boundaries from sorted columns in global memory: used when the columns
+// were sorted by a recursive level (too long for one CTA) and to repair the
+// rare min-exclusion rejection (only segments with fix[seg] set, if `only_fix`).
+template <typename K>
+__global__ void k_segmat(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tasks,
+                         const K* __restrict__ data, const K* __restrict__ piv, uint32_t* __restrict__ segmat,
+                         const uint32_t* __restrict__ fix, int only_fix) {
+  const TaskDesc tk = tasks[blockIdx.x];
+  if (only_fix && !fix[tk.seg]) return;
+  const LevelSeg sg = segs[tk.seg];
+  const K* P = piv + sg.piv_base;
+  for (uint32_t c = tk.a; c < tk.b; c++) {
+    const uint64_t a = uint64_t(c) * sg.rows;
+    const uint32_t L = (uint32_t)(a < sg.len ? min((uint64_t)sg.rows, (uint64_t)(sg.len - a)) : 0);
+    const K* col = data + sg.off + a;
+    uint32_t* row = segmat + sg.segmat_base + uint64_t(c) * (sg.nbt + 1);
+    for (uint32_t bt = threadIdx.x; bt <= sg.nbt; bt += blockDim.x) {
+      const uint32_t j = bt * kTB;
+      uint32_t pos;
+      if (bt == 0) pos = 0;
+      else if (j >= sg.k) pos = L;
+      else {
+        const K pj = P[j - 1];
+        const bool dup = j >= 2 && P[j - 2] == pj;
+        uint32_t lo = 0, hi = L;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (before_boundary(col[mid], pj, dup)) lo = mid + 1; else hi = mid;
+        }
+        pos = lo;
+      }
+      row[bt] = pos;
+    }
+  }
+}
+
+// Keys per bucket tile (sum of the tile's run in every column).  CTA per tile.
+__global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
+                             const uint32_t* __restrict__ segmat) {
+  TileInfo ti = tiles[blockIdx.x];
+  const LevelSeg sg = segs[ti.seg];
+  uint32_t sum = 0;
+  for (uint32_t c = threadIdx.x; c < sg.ncols; c += blockDim.x) {
+    const uint32_t* row = segmat + sg.segmat_base + uint64_t(c) * (sg.nbt + 1);
+    sum += row[ti.bt + 1] - row[ti.bt];
+  }
+  __shared__ uint32_t red[32];
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    sum = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (threadIdx.x == 0) tiles[blockIdx.x].size = sum;
+  }
+}
+
+// Per segment: tile output offsets (exclusive scan of sizes) and piece-table
+// bases (capacity ceil(size/S) + ceil(ncols/G) pieces per tile).  Also resets
+// the per-segment bucket bookkeeping.  One CTA per segment (tiles contiguous).
+__global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
+                            TileInfo* __restrict__ tiles, uint32_t S, uint32_t G,
+                            const uint32_t* __restrict__ piece_seg_base) {
+  const LevelSeg sg = segs[blockIdx.x];
+  const uint32_t t0 = tile_base[blockIdx.x], nt = sg.nbt;
+  __shared__ uint32_t carry_out, carry_piece;
+  if (threadIdx.x == 0) {
+    carry_out = sg.off;
+    carry_piece = piece_seg_base[blockIdx.x];
+  }
+  __syncthreads();
+  const uint32_t gpt = (sg.ncols + G - 1) / G;
+  for (uint32_t c0 = 0; c0 < nt; c0 += blockDim.x) {
+    const uint32_t i = c0 + threadIdx.x;
+    uint32_t sz = 0, cp = 0;
+    if (i < nt) {
+      sz = tiles[t0 + i].size;
+      cp = (sz + S - 1) / S + gpt;
+    }
+    // block scan of (sz, cp)
+    __shared__ uint32_t ws[32], wc[32];
+    uint32_t xs = sz, xc = cp;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), yc = __shfl_up_sync(0xffffffffu, xc, o);
+      if (lane >= o) { xs += ys; xc += yc; }
+    }
+    if (lane == 31) { ws[w] = xs; wc[w] = xc; }
+    __syncthreads();
+    if (w == 0) {
+      const int nw = blockDim.x >> 5;
+      uint32_t a = lane < nw ? ws[lane] : 0, b = lane < nw ? wc[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+        if (lane >= o) { a += ya; b += yb; }
+      }
+      if (lane < nw) { ws[lane] = a; wc[lane] = b; }
+    }
+    __syncthreads();
+    const uint32_t es = xs - sz + (w ? ws[w - 1] : 0), ec = xc - cp + (w ? wc[w - 1] : 0);
+    if (i < nt) {
+      tiles[t0 + i].out = carry_out + es;
+      tiles[t0 + i].piece_base = carry_piece + ec;
+      tiles[t0 + i].npieces = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) {
+      carry_out += es + sz;
+      carry_piece += ec + cp;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------
+// SkewTranspose, piece-major (see the header).  CTA per bucket tile; the tile's
+// stream is the concatenation over columns c = 0..ncols-1 of the column's run
+// of this tile (sorted, contiguous).  A piece = up to S keys from up to F runs
+// ("fragments"); per piece: cp.async the fragments into shared memory, find
+// each key's bucket among the tile's kTB boundaries, rank it stably within its
+// (fragment, bucket) group -- in a sorted fragment a bucket is one contiguous
+// group -- and scan group sizes down the fragments per bucket.  The piece's
+// bucket-major image is written contiguously; its bucket prefix goes to the
+// piece tables.  Shared arrays are padded (one word per 32) so the blocked
+// per-thread loops are bank-conflict free.
+template <typename K, bool PAIRS, int NT, int S, int F>
+struct PmCfg {
+  static constexpr int NW = NT / 32;
+  static constexpr int VS = S / NT;
+  static constexpr int PADK = 128 / sizeof(K);  // elements per pad period for K arrays
+  static constexpr int SK = S + S / PADK + 1;   // padded K-array length
+  static constexpr int SW = S + S / 32 + 1;     // padded u32-array length
+  static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t off_stage = 0;
+  static constexpr size_t off_vstage = al(off_stage + SK * sizeof(K));
+  static constexpr size_t off_code = al(off_vstage + (PAIRS ? SW * 4 : 0));
+  static constexpr size_t off_out = al(off_code + SW * 4);
+  static constexpr size_t off_vout = al(off_out + S * sizeof(K));
+  static constexpr size_t off_table = al(off_vout + (PAIRS ? S * 4 : 0));  // F x kTB u16
+  static constexpr size_t off_fstart = al(off_table + F * kTB * 2);          // F+1 u32
+  static constexpr size_t off_fsrc = al(off_fstart + (F + 1) * 4);           // F u32
+  static constexpr size_t off_wsum = al(off_fsrc + F * 4);                   // NW x 32 u32
+  static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);             // 64 + 3*32+1 u32
+  static constexpr size_t off_bval = al(off_misc + (64 + 3 * kTB + 8) * 4);
+  static constexpr size_t SMEM = al(off_bval + kTB * sizeof(K));
+  __device__ __forceinline__ static int pk(int i) { return i + i / PADK; }
+  __device__ __forceinline__ static int pw(int i) { return i + (i >> 5); }
+};
+
+template <typename K, bool PAIRS, int NT, int S, int F>
+__global__ void __launch_bounds__(NT)
+k_transpose_pm(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const K* __restrict__ src,
+               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint32_t* __restrict__ pout,
+               uint16_t* __restrict__ ppre) {
+  using C = PmCfg<K, PAIRS, NT, S, F>;
+  static_assert(F <= 256 && F <= NT && S <= 65535 && S % NT == 0 && NT % 32 == 0, "shape");
+  extern __shared__ __align__(16) unsigned char sm[];
+  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
+  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
+  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);  // frag << 8 | bucket
+  K* outb = reinterpret_cast<K*>(sm + C::off_out);
+  uint32_t* vout = reinterpret_cast<uint32_t*>(sm + C::off_vout);
+  uint16_t* table = reinterpret_cast<uint16_t*>(sm + C::off_table);
+  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_fstart);
+  uint32_t* fsrc = reinterpret_cast<uint32_t*>(sm + C::off_fsrc);
+  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);  // [0..31] scans
+  uint32_t* ptot = misc + 64;
+  uint32_t* poff = ptot + kTB;     // kTB + 1 entries
+  uint32_t* bdupv = poff + kTB + 1;
+  K* bval = reinterpret_cast<K*>(sm + C::off_bval);
+
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const TileInfo ti = tiles[blockIdx.x];
+  const LevelSeg sg = segs[ti.seg];
+  const uint32_t bt = ti.bt;
+  const uint32_t b0 = bt * kTB;
+  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
+  const uint32_t nint = nb - 1;
+  const K* P = piv + sg.piv_base;
+  if (t < (int)nint) {
+    const uint32_t j = b0 + 1 + t;
+    bval[t] = P[j - 1];
+    bdupv[t] = (j >= 2 && P[j - 2] == P[j - 1]) ? 1u : 0u;
+  }
+  uint32_t oc = ti.out, npc = 0;
+  uint32_t c = 0, o = 0;  // next column and offset inside its run (uniform across the CTA)
+  const int i0 = t * C::VS;
+  const uint32_t* rows = segmat + sg.segmat_base;
+  const uint32_t rstride = sg.nbt + 1;
+
+  while (c < sg.ncols) {
+    // ---- window: the runs of columns c .. c+F-1, prefix-summed; take up to S keys
+    uint32_t len = 0, srcpos = 0;
+    if (t < F && c + t < sg.ncols) {
+      const uint32_t* row = rows + uint64_t(c + t) * rstride;
+      const uint32_t a = row[bt], e = row[bt + 1];
+      const uint32_t skip = t == 0 ? o : 0;
+      len = e - a - skip;
+      srcpos = sg.off + (c + t) * sg.rows + a + skip;
+    }
+    uint32_t wtot;
+    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
+    if (t < F) {
+      fstart[t] = ex;
+      fsrc[t] = srcpos;
+    }
+    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
+    // fragments overlapping [0, S): the runs of the window whose prefix is below S
+    const int inpiece = (t < (int)nwin && ex < (uint32_t)S) ? 1 : 0;
+    const uint32_t nf = __syncthreads_count(inpiece);
+    const uint32_t Pn = min((uint32_t)S, wtot);
+    if (t == 0) fstart[nf] = Pn;  // clips the last fragment at S
+    __syncthreads();
+    uint32_t nc, no;
+    if (wtot <= (uint32_t)S) {  // the whole window fits
+      nc = c + nwin;
+      no = 0;
+    } else {  // the piece ends inside run nf-1: continue there if it has keys left
+      const uint32_t last = nf - 1;
+      const uint32_t used = Pn - fstart[last];
+      const uint32_t* row = rows + uint64_t(c + last) * rstride;
+      const uint32_t base = last == 0 ? o : 0;
+      const uint32_t full = row[bt + 1] - row[bt] - base;
+      if (used < full) {
+        nc = c + last;
+        no = base + used;
+      } else {
+        nc = c + last + 1;
+        no = 0;
+      }
+    }
+    if (Pn > 0) {
+      for (uint32_t i = t; i < nf * kTB; i += NT) table[i] = 0;
+      // ---- load fragments (one warp per fragment, cp.async, coalesced)
+      for (uint32_t f = w; f < nf; f += C::NW) {
+        const uint32_t fs = fstart[f], fe = fstart[f + 1];
+        const K* gs = src + fsrc[f] - fs;
+        const uint32_t* gv = PAIRS ? vsrc + fsrc[f] - fs : nullptr;
+        for (uint32_t q = fs + lane; q < fe; q += 32) {
+          cp_async_elem(&stage[C::pk(q)], &gs[q]);
+          if (PAIRS) cp_async_elem(&vstage[C::pw(q)], &gv[q]);
+          code[C::pw(q)] = f << 8;
+        }
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      // ---- bucket of every key (binary search over the tile's boundaries), striped
+      for (int i = t; i < (int)Pn; i += NT) {
+        const K xk = stage[C::pk(i)];
+        uint32_t lo = 0, hi = nint;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (before_boundary(xk, bval[mid], bdupv[mid] != 0)) hi = mid; else lo = mid + 1;
+        }
+        code[C::pw(i)] |= lo;
+      }
+      __syncthreads();
+      // ---- group heads (fragment or bucket changes); carry = last head before this thread
+      uint32_t last_head = 0;
+      {
+        uint32_t prev = (i0 > 0 && i0 <= (int)Pn) ? code[C::pw(i0 - 1)] : 0xffffffffu;
+        for (int q = 0; q < C::VS; q++) {
+          const int i = i0 + q;
+          if (i < (int)Pn) {
+            const uint32_t cd = code[C::pw(i)];
+            if (i == 0 || cd != prev) last_head = i;
+            prev = cd;
+          }
+        }
+      }
+      const uint32_t carry = block_excl_max<C::NW>(last_head, misc);
+      // ---- group sizes into the (fragment, bucket) table: the last key of a group writes
+      {
+        uint32_t head = carry;
+        uint32_t cur = (i0 > 0 && i0 <= (int)Pn) ? code[C::pw(i0 - 1)] : 0xffffffffu;
+        for (int q = 0; q < C::VS; q++) {
+          const int i = i0 + q;
+          if (i < (int)Pn) {
+            const uint32_t cd = code[C::pw(i)];
+            if (i == 0 || cd != cur) head = i;
+            cur = cd;
+            const bool lastg = (i == (int)Pn - 1) || code[C::pw(i + 1)] != cd;
+            if (lastg) table[(cd >> 8) * kTB + (cd & 0xff)] = (uint16_t)(i - head + 1);
+          }
+        }
+      }
+      __syncthreads();
+      // ---- exclusive scan of the table down the fragments, per bucket (lane = bucket)
+      const uint32_t per = (nf + C::NW - 1) / C::NW;
+      const uint32_t f0 = min(nf, w * per), f1 = min(nf, f0 + per);
+      {
+        uint32_t sum = 0;
+        for (uint32_t f = f0; f < f1; f++) sum += table[f * kTB + lane];
+        wsum[w * 32 + lane] = sum;
+      }
+      __syncthreads();
+      {
+        uint32_t run = 0, total = 0;
+        for (int ww = 0; ww < C::NW; ww++) {
+          const uint32_t v = wsum[ww * 32 + lane];
+          if (ww < w) run += v;
+          total += v;
+        }
+        for (uint32_t f = f0; f < f1; f++) {
+          const uint32_t v = table[f * kTB + lane];
+          table[f * kTB + lane] = (uint16_t)run;
+          run += v;
+        }
+        if (w == 0) {
+          ptot[lane] = total;
+          uint32_t v = lane < (int)nb ? total : 0, xs = v;
+          for (int q = 1; q < 32; q <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
+            if (lane >= q) xs += y;
+          }
+          poff[lane] = xs - v;
+          if (lane == 31) poff[kTB] = xs;
+        }
+      }
+      __syncthreads();
+      // ---- scatter into the piece's bucket-major image
+      {
+        uint32_t head = carry;
+        uint32_t cur = (i0 > 0 && i0 <= (int)Pn) ? code[C::pw(i0 - 1)] : 0xffffffffu;
+        for (int q = 0; q < C::VS; q++) {
+          const int i = i0 + q;
+          if (i < (int)Pn) {
+            const uint32_t cd = code[C::pw(i)];
+            if (i == 0 || cd != cur) head = i;
+            cur = cd;
+            const uint32_t b = cd & 0xff;
+            const uint32_t dpos = poff[b] + table[(cd >> 8) * kTB + b] + (i - head);
+            outb[dpos] = stage[C::pk(i)];
+            if (PAIRS) vout[dpos] = vstage[C::pw(i)];
+          }
+        }
+      }
+      __syncthreads();
+      for (uint32_t q = t; q < Pn; q += NT) {
+        dst[oc + q] = outb[q];
+        if (PAIRS) vdst[oc + q] = vout[q];
+      }
+      const uint32_t pe = ti.piece_base + npc;
+      if (t == 0) pout[pe] = oc;
+      if (t <= kTB) ppre[uint64_t(pe) * kPP + t] = (uint16_t)poff[t];
+      oc += Pn;
+      npc++;
+    }
+    c = nc;
+    o = no;
+    __syncthreads();
+  }
+  if (t == 0) tiles[blockIdx.x].npieces = npc;
+}
+
+// ------------------------------------------------------------------------------
+// Bucket planning, per segment (one CTA): bucket sizes from the piece tables,
+// final offsets (exclusive scan, P:283 / P:461), RNG node keys, and the work
+// lists: single-value buckets (copy), on-chip classes, oversize.
+struct PlanOut {
+  uint32_t* list;       // [ncls + 2][cap_per_list] bucket indices
+  uint32_t* count;      // [ncls + 2] atomic counters; ncls = copy list, ncls+1 = oversize
+  uint32_t cap_per_list;
+  uint32_t ncls;
+  uint32_t cls_tile[12];  // class tile sizes (ascending)
+  uint32_t max_tile;
+};
+
+// Bucket sizes from the piece tables: CTA per tile, warp w sums pieces w, w+NW, ...
+__global__ void k_bucket_sizes(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
+                               const uint16_t* __restrict__ ppre, uint32_t* __restrict__ bsize) {
+  const TileInfo ti = tiles[blockIdx.x];
+  const LevelSeg sg = segs[ti.seg];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t sum = 0;
+  for (uint32_t q = w; q < ti.npieces; q += nw) {
+    const uint16_t* pr = ppre + uint64_t(ti.piece_base + q) * kPP;
+    sum += pr[lane + 1] - pr[lane];
+  }
+  __shared__ uint32_t red[32][33];
+  red[w][lane] = sum;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t tot = 0;
+    for (int i = 0; i < nw; i++) tot += red[i][lane];
+    const uint32_t b = ti.bt * kTB + lane;
+    if (b < sg.k) bsize[sg.buck_base + b] = tot;
+  }
+}
+
+template <typename K>
+__global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
+                              const uint32_t* __restrict__ bsize, const K* __restrict__ piv,
+                              BucketRec* __restrict__ recs, PlanOut po) {
+  const LevelSeg sg = segs[blockIdx.x];
+  const uint32_t t0 = tile_base[blockIdx.x];
+  __shared__ uint32_t carry;
+  __shared__ uint32_t ws[32];
+  if (threadIdx.x == 0) carry = sg.off;
+  __syncthreads();
+  const K* P = piv + sg.piv_base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (uint32_t c0 = 0; c0 < sg.k; c0 += blockDim.x) {
+    const uint32_t b = c0 + threadIdx.x;
+    const uint32_t size = b < sg.k ? bsize[sg.buck_base + b] : 0;
+    uint32_t x = size;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t a = lane < nw ? ws[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, a, o);
+        if (lane >= o) a += y;
+      }
+      if (lane < nw) ws[lane] = a;
+    }
+    __syncthreads();
+    const uint32_t excl = carry + x - size + (w ? ws[w - 1] : 0);
+    if (b < sg.k) {
+      const uint64_t gi = uint64_t(sg.buck_base) + b;
+      BucketRec rc;
+      rc.tile = t0 + b / kTB;
+      rc.lane = b % kTB;
+      rc.out = excl;
+      rc.size = size;
+      rc.node = child_key(sg.node, 1, b);
+      recs[gi] = rc;
+      if (size) {
+        int cls;
+        const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
+        if (single) cls = po.ncls;
+        else if (size > po.max_tile) cls = po.ncls + 1;
+        else {
+          cls = 0;
+          while (po.cls_tile[cls] < size) cls++;
+        }
+        const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+        po.list[uint64_t(cls) * po.cap_per_list + slot] = (uint32_t)gi;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + size;
+    __syncthreads();
+  }
+}
+
+// Gather a bucket's sub-chunks (piece order) into shared memory:
+// store(i, key, val) is called for i = 0..size-1 via cp.async-free plain copies.
+template <int NT, typename F>
+__device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_j, const uint32_t* __restrict__ pout,
+                                              const uint16_t* __restrict__ ppre, uint32_t* s_off, uint32_t* s_len,
+                                              uint32_t* s_dst, uint32_t* misc, F&& copy_chunk) {
+  constexpr int NW = NT / 32;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint32_t base = 0;
+  for (uint32_t c0 = 0; c0 < ti.npieces; c0 += NT) {
+    const uint32_t q = c0 + t;
+    uint32_t o = 0, l = 0;
+    if (q < ti.npieces) {
+      const uint16_t* pr = ppre + uint64_t(ti.piece_base + q) * kPP;
+      const uint32_t a = pr[lane_j], e = pr[lane_j + 1];
+      o = pout[ti.piece_base + q] + a;
+      l = e - a;
+    }
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<NW>(l, misc, &tot);
+    if (q < ti.npieces) {
+      s_off[t] = o;
+      s_len[t] = l;
+      s_dst[t] = base + ex;
+    }
+    __syncthreads();
+    const uint32_t nq = min((uint32_t)NT, ti.npieces - c0);
+    for (uint32_t c = w; c < nq; c += NW) copy_chunk(s_off[c], s_len[c], s_dst[c], lane);
+    base += tot;
+    __syncthreads();
+  }
+}
+
+// Bucket sort with gather: CTA loops over its class list.
+template <typename K, int NT, int V, bool PAIRS>
+__global__ void __launch_bounds__(NT)
+k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
+             const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
+             const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst, const uint32_t* __restrict__ pout,
+             const uint16_t* __restrict__ ppre) {
+  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using BS = BlockSort<SK, NT, V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SK* s = reinterpret_cast<SK*>(smem_raw);
+  uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES + (PAIRS ? BS::TILE * 4 : 0));
+  uint32_t* s_len = s_off + NT;
+  uint32_t* s_dst = s_len + NT;
+  uint32_t* misc = s_dst + NT;
+  const uint32_t total = *count;
+  for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const BucketRec rc = recs[list[it]];
+    const TileInfo ti = tiles[rc.tile];
+    for (int i = threadIdx.x + rc.size; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc,
+                      [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        for (uint32_t q = ln; q < l; q += 32) {
+                          if constexpr (PAIRS) {
+                            s[BS::pad(d + q)] = (uint64_t(src[o + q]) << 32) | (d + q);
+                            vs[d + q] = vsrc[o + q];
+                          } else {
+                            cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
+                          }
+                        }
+                      });
+    cp_async_wait_all();
+    __syncthreads();
+    BS::sort_smem(s);
+    for (int i = threadIdx.x; i < (int)rc.size; i += NT) {
+      const SK x = s[BS::pad(i)];
+      if constexpr (PAIRS) {
+        dst[rc.out + i] = uint32_t(x >> 32);
+        vdst[rc.out + i] = vs[uint32_t(x)];
+      } else {
+        dst[rc.out + i] = x;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Gather-copy (single-value buckets, oversize buckets, debug): the bucket's
+// keys in the paper's order, contiguous at rc.out in dst.  CTA loops over a list.
+template <typename K, int NT>
+__global__ void __launch_bounds__(NT)
+k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
+                const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint32_t all_k,
+                const K* __restrict__ src, K* __restrict__ dst, const uint32_t* __restrict__ vsrc,
+                uint32_t* __restrict__ vdst, const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
+  __shared__ uint32_t s_off[NT], s_len[NT], s_dst[NT], misc[64];
+  const uint32_t total = list ? *count : all_k;
+  for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const BucketRec rc = recs[list ? list[it] : it];
+    const TileInfo ti = tiles[rc.tile];
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc,
+                      [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        for (uint32_t q = ln; q < l; q += 32) {
+                          dst[rc.out + d + q] = src[o + q];
+                          if (vsrc) vdst[rc.out + d + q] = vsrc[o + q];
+                        }
+                      });
+  }
+}
+
+}  // namespace sq

@@ -218,11 +218,11 @@ def test_host_entry_points():
                                     (1 << 16, 1000), (50000, 7)])
 def test_level_intermediate_parity(n, card):
     """Pivots, accepted round, bucket ends and the post-SkewTranspose array of
-    one level equal the oracle's (paper-literal sampling from D)."""
+    one level equal the oracle's, sampling from the level input (L9)."""
     rng = np.random.default_rng(n ^ card)
     keys = rng.integers(0, card, n, dtype=np.uint64).astype(np.uint32)
     seed = 77
-    post, _, P, be, r, deg = O.level(keys, seed=seed, sample_from_input=False)
+    post, _, P, be, r, deg = O.level(keys, seed=seed, sample_from_input=True)
     m = O.ceil_sqrt(n)
     src = to_dev(keys)
     dst = torch.empty_like(src)
