@@ -146,6 +146,11 @@ void sq_get_stats(sq_stats *out);
  * other values. */
 int sq_set_max_tile(uint32_t max_tile);
 
+/* Tuning/test knob: buckets larger than one CTA's tile are sorted by a
+ * thread-block cluster of 4, 8 or 16 CTAs (default, enable = 1); with 0 they
+ * recurse into another SquareSort level instead.  Process-wide. */
+int sq_set_cluster_sort(int enable);
+
 /* Per-kernel device timing: when enabled, every kernel the library launches is
  * bracketed by CUDA events on its stream and the elapsed times accumulate per
  * kernel role (colsort, bucketsort, smallsort, sample, count, transpose, ...).

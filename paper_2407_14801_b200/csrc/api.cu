@@ -108,6 +108,7 @@ static void prof_collect() {  // after a stream sync
 
 // ------------------------------------------------------------------ options
 static uint32_t g_max_tile = 0;  // 0 = default
+static int g_cluster = 1;        // cluster sorts for buckets beyond one CTA
 
 // ------------------------------------------------------------------ device check
 static void check_device() {
@@ -283,6 +284,11 @@ template <> struct PmTr<uint32_t, false> { static constexpr int NT = 512, S = 81
 template <> struct PmTr<uint32_t, true> { static constexpr int NT = 512, S = 4096, F = 256; };
 template <> struct PmTr<uint64_t, false> { static constexpr int NT = 512, S = 4096, F = 256; };
 
+// cluster bucket sort: per-CTA tile (threads x keys) for 32-bit / 64-bit sort keys
+template <typename SK> struct ClusterCfg;
+template <> struct ClusterCfg<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
+template <> struct ClusterCfg<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
+
 // ------------------------------------------------------------------ the engine
 struct Seg {
   uint32_t off, len;
@@ -370,6 +376,49 @@ struct Engine {
       copy_ranges(bigr, src, dst);  // a level sorts a segment where it will end up
       run_level(big, dst, depth, nullptr);
     }
+  }
+
+  template <int CL>
+  void launch_cluster_t(const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs, const TileInfo* tiles,
+                        int T, int X, const uint32_t* pout, const uint16_t* ppre, uint32_t nbuck) {
+    using CC = ClusterCfg<SK>;
+    using BS = BlockSort<SK, CC::NT, CC::V>;
+    const size_t smem = 2 * BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * CC::NT + 64) * 4;
+    auto f = k_clustersort<K, CC::NT, CC::V, CL, PAIRS>;
+    static int max_clusters = -1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(CC::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (max_clusters < 0) {
+      set_smem(f, smem);
+      if (CL > 8) SQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cfg.gridDim = dim3(CL * num_sms());
+      int mc = 0;
+      SQ_CUDA(cudaOccupancyMaxActiveClusters(&mc, f, &cfg));
+      max_clusters = mc;
+    }
+    if (max_clusters <= 0) throw Error(SQ_ERR_CUDA, "cluster of " + std::to_string(CL) + " CTAs cannot be scheduled");
+    cfg.gridDim = dim3(CL * std::min<uint32_t>(max_clusters, nbuck));
+    ProfScope ps("clustersort", st);
+    SQ_CUDA(cudaLaunchKernelEx(&cfg, f, recs, tiles, lst, cnt, (const K*)kb[T], kb[X],
+                               (const uint32_t*)(PAIRS ? vb[T] : nullptr), PAIRS ? vb[X] : nullptr, pout, ppre));
+    check_launch("k_clustersort");
+  }
+
+  void launch_cluster(uint32_t cl, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
+                      const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
+                      uint32_t nbuck) {
+    if (cl == 4) launch_cluster_t<4>(lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    else if (cl == 8) launch_cluster_t<8>(lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    else launch_cluster_t<16>(lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
   }
 
   // One SquareSort level (Alg 1) for a batch of segments that live in buffer X,
@@ -524,9 +573,19 @@ struct Engine {
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};
     po.ncls = 0;
+    uint32_t cls_cl[12] = {0};  // 0 = one CTA, else cluster size
     for (uint32_t t : kTiles)
       if (t <= cap && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
     po.max_tile = cap;
+    if (g_cluster) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
+      const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
+      for (uint32_t cl : {4u, 8u, 16u}) {
+        if (cl * ct <= po.max_tile) continue;
+        cls_cl[po.ncls] = cl;
+        po.cls_tile[po.ncls++] = cl * ct;
+        po.max_tile = cl * ct;
+      }
+    }
     po.cap_per_list = (uint32_t)buck_tot;
     po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 2) * buck_tot * 4);
     po.count = (uint32_t*)ar.alloc((po.ncls + 2) * 4);
@@ -560,6 +619,10 @@ struct Engine {
     // 6. bucket sorts: gather from T, sort on chip, write to X
     for (uint32_t c = 0; c < po.ncls; c++) {
       const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
+      if (cls_cl[c]) {
+        launch_cluster(cls_cl[c], lst, po.count + c, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
+        continue;
+      }
       with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
         constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
         using BS = BlockSort<SK, NT, V>;
@@ -855,6 +918,11 @@ int sq_profile_read(char* buf, size_t cap) {
   if (!buf || cap == 0) return SQ_ERR_INVALID_ARGUMENT;
   snprintf(buf, cap, "%s", out.c_str());
   return out.size() < cap ? SQ_OK : SQ_ERR_INVALID_ARGUMENT;
+}
+
+int sq_set_cluster_sort(int enable) {
+  g_cluster = enable ? 1 : 0;
+  return SQ_OK;
 }
 
 int sq_set_max_tile(uint32_t t) {

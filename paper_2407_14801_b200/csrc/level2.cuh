@@ -17,6 +17,7 @@
 //    sort gathers the sub-chunks on chip and writes the sorted bucket to its
 //    final position, so no bucket sizes are needed before the transpose.
 #pragma once
+#include <cooperative_groups.h>
 #include <type_traits>
 #include "level.cuh"
 
@@ -651,16 +652,18 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t*
   }
 }
 
-// Gather a bucket's sub-chunks (piece order) into shared memory:
-// store(i, key, val) is called for i = 0..size-1 via cp.async-free plain copies.
+// Gather the bucket positions [lo, hi) (piece order = the paper's order) of a
+// bucket: copy_chunk(global_offset, length, position - lo, lane) is called for
+// every intersecting sub-chunk, one warp per sub-chunk.
 template <int NT, typename F>
 __device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_j, const uint32_t* __restrict__ pout,
                                               const uint16_t* __restrict__ ppre, uint32_t* s_off, uint32_t* s_len,
-                                              uint32_t* s_dst, uint32_t* misc, F&& copy_chunk) {
+                                              uint32_t* s_dst, uint32_t* misc, uint32_t lo, uint32_t hi,
+                                              F&& copy_chunk) {
   constexpr int NW = NT / 32;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   uint32_t base = 0;
-  for (uint32_t c0 = 0; c0 < ti.npieces; c0 += NT) {
+  for (uint32_t c0 = 0; c0 < ti.npieces && base < hi; c0 += NT) {
     const uint32_t q = c0 + t;
     uint32_t o = 0, l = 0;
     if (q < ti.npieces) {
@@ -672,13 +675,17 @@ __device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_
     uint32_t tot;
     const uint32_t ex = block_excl_sum<NW>(l, misc, &tot);
     if (q < ti.npieces) {
-      s_off[t] = o;
-      s_len[t] = l;
-      s_dst[t] = base + ex;
+      // clip [base+ex, base+ex+l) to [lo, hi)
+      const uint32_t p0 = base + ex, p1 = p0 + l;
+      const uint32_t c0c = max(p0, lo), c1c = min(p1, hi);
+      s_off[t] = o + (c0c - p0);
+      s_len[t] = c1c > c0c ? c1c - c0c : 0;
+      s_dst[t] = c0c - lo;
     }
     __syncthreads();
     const uint32_t nq = min((uint32_t)NT, ti.npieces - c0);
-    for (uint32_t c = w; c < nq; c += NW) copy_chunk(s_off[c], s_len[c], s_dst[c], lane);
+    for (uint32_t c = w; c < nq; c += NW)
+      if (s_len[c]) copy_chunk(s_off[c], s_len[c], s_dst[c], lane);
     base += tot;
     __syncthreads();
   }
@@ -705,7 +712,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     const BucketRec rc = recs[list[it]];
     const TileInfo ti = tiles[rc.tile];
     for (int i = threadIdx.x + rc.size; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
-    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc,
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, 0u, rc.size,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
@@ -745,13 +752,187 @@ k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__
   for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
     const BucketRec rc = recs[list ? list[it] : it];
     const TileInfo ti = tiles[rc.tile];
-    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc,
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, 0u, rc.size,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         for (uint32_t q = ln; q < l; q += 32) {
                           dst[rc.out + d + q] = src[o + q];
                           if (vsrc) vdst[rc.out + d + q] = vsrc[o + q];
                         }
                       });
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Cluster bucket sort (the GPU's simple_sort for buckets larger than one CTA
+// holds, P:259-261 / P:852): a cluster of CL CTAs (CL = 4, 8, 16) sorts one
+// bucket of up to CL*TILE keys.  CTA r gathers bucket positions
+// [r*chunk, (r+1)*chunk) and sorts them on chip; then log2(CL) rounds of
+// pairwise merge-path merges read the partner runs through distributed shared
+// memory (each CTA produces its `chunk` positions of the merged group), the
+// last round writing the sorted bucket straight to HBM.  No extra HBM pass.
+template <typename SK>
+struct DistSeq {  // a sorted sequence spread over consecutive CTAs, `chunk` keys each
+  SK* const* parts;  // shared-memory pointers of the cluster's CTAs (mapped)
+  uint32_t first;    // first CTA
+  uint32_t chunk;
+  uint32_t len;
+  template <int PER>
+  __device__ __forceinline__ SK at(uint32_t i) const {
+    const uint32_t c = i / chunk, off = i - c * chunk;
+    return parts[first + c][off + off / PER];
+  }
+};
+
+// Merge-path split of diagonal d between two distributed sorted sequences,
+// found by one warp with 32-ary search: smallest a in [max(0,d-|B|), min(d,|A|)]
+// with A[a] > B[d-1-a] (ties taken from A first).  Result broadcast to the warp.
+template <typename SK, int PER>
+__device__ __forceinline__ uint32_t warp_merge_split(const DistSeq<SK>& A, const DistSeq<SK>& B, uint32_t d) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = d > B.len ? d - B.len : 0, hi = min(d, A.len);
+  // invariant: the answer lies in [lo, hi]; pred(a) = A[a] > B[d-1-a] is monotone
+  while (hi > lo) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t p = lo + lane * step;
+    bool gt = true;  // probes at or beyond hi count as true
+    if (p < hi) gt = A.template at<PER>(p) > B.template at<PER>(d - 1 - p);
+    const uint32_t m = __ballot_sync(0xffffffffu, gt);
+    const uint32_t first = m ? (uint32_t)(__ffs(m) - 1) : 32u;  // first probe with pred true
+    if (first == 0) {
+      hi = lo;
+    } else {
+      const uint32_t lo_old = lo;
+      lo = lo_old + (first - 1) * step + 1;                       // pred(probe first-1) is false
+      hi = (uint32_t)min((uint64_t)hi, (uint64_t)lo_old + (uint64_t)first * step);  // pred(probe first) true
+    }
+  }
+  return lo;
+}
+
+template <typename K, int NT, int V, int CL, bool PAIRS>
+__global__ void __launch_bounds__(NT)
+k_clustersort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
+              const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, const K* __restrict__ src,
+              K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+              const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
+  namespace cg = cooperative_groups;
+  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using BS = BlockSort<SK, NT, V>;
+  constexpr int PER = BS::PER;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SK* bufA = reinterpret_cast<SK*>(smem_raw);                     // my part of the current sequence
+  SK* bufB = reinterpret_cast<SK*>(smem_raw + BS::SMEM_BYTES);   // staged merge inputs
+  uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + 2 * BS::SMEM_BYTES);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + 2 * BS::SMEM_BYTES + (PAIRS ? BS::TILE * 4 : 0));
+  uint32_t* s_len = s_off + NT;
+  uint32_t* s_dst = s_len + NT;
+  uint32_t* misc = s_dst + NT;
+  __shared__ SK* partsA[CL];
+  __shared__ uint32_t* partsV[CL];
+  __shared__ uint32_t split[2];
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t rank = cluster.block_rank();
+  if (threadIdx.x < CL) {
+    partsA[threadIdx.x] = cluster.map_shared_rank(bufA, threadIdx.x);
+    partsV[threadIdx.x] = cluster.map_shared_rank(vs, threadIdx.x);
+  }
+  __syncthreads();
+  const uint32_t total = *count;
+  const uint32_t ncl = gridDim.x / CL, cid = blockIdx.x / CL;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t it = cid; it < total; it += ncl) {
+    const BucketRec rc = recs[list[it]];
+    const TileInfo ti = tiles[rc.tile];
+    const uint32_t L = rc.size;
+    const uint32_t chunk = (L + CL - 1) / CL;
+    const uint32_t lo = min(L, rank * chunk), hi = min(L, lo + chunk);
+    const uint32_t mylen = hi - lo;
+    // ---- gather this CTA's chunk and sort it on chip
+    for (int i = threadIdx.x + mylen; i < BS::TILE; i += NT) bufA[BS::pad(i)] = KeyTraits<SK>::kMax;
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
+                      [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        for (uint32_t q = ln; q < l; q += 32) {
+                          if constexpr (PAIRS) {
+                            bufA[BS::pad(d + q)] = (uint64_t(src[o + q]) << 32) | (lo + d + q);
+                            vs[d + q] = vsrc[o + q];
+                          } else {
+                            cp_async_elem(&bufA[BS::pad(d + q)], &src[o + q]);
+                          }
+                        }
+                      });
+    cp_async_wait_all();
+    __syncthreads();
+    BS::sort_smem(bufA);
+    // ---- merge rounds: groups of 2h CTAs merge the sequences held by [g, g+h) and [g+h, g+2h)
+    for (uint32_t h = 1; h < CL; h *= 2) {
+      const bool last = 2 * h == CL;
+      const uint32_t g = rank & ~(2 * h - 1);
+      const uint32_t la = (uint32_t)min((uint64_t)h * chunk, (uint64_t)(L > g * chunk ? L - g * chunk : 0));
+      const uint32_t lb = (uint32_t)min((uint64_t)h * chunk, (uint64_t)(L > (g + h) * chunk ? L - (g + h) * chunk : 0));
+      DistSeq<SK> A{partsA, g, chunk, la};
+      DistSeq<SK> B{partsA, g + h, chunk, lb};
+      const uint32_t mbeg = min((rank - g) * chunk, la + lb);
+      const uint32_t mend = min(mbeg + chunk, la + lb);
+      cluster.sync();  // previous round's parts are complete everywhere
+      if (w < 2) {
+        const uint32_t sp = warp_merge_split<SK, PER>(A, B, w == 0 ? mbeg : mend);
+        if (lane == 0) split[w] = sp;
+      }
+      __syncthreads();
+      const uint32_t a0 = split[0], a1 = split[1];
+      const uint32_t b0 = mbeg - a0, b1 = mend - a1;
+      const uint32_t na = a1 - a0, nbk = b1 - b0;
+      // stage A[a0,a1) then B[b0,b1) into bufB (bulk DSMEM reads, coalesced)
+      for (uint32_t i = threadIdx.x; i < na; i += NT) bufB[BS::pad(i)] = A.template at<PER>(a0 + i);
+      for (uint32_t i = threadIdx.x; i < nbk; i += NT) bufB[BS::pad(na + i)] = B.template at<PER>(b0 + i);
+      cluster.sync();  // all partners finished reading my bufA
+      // local merge of bufB[0,na) and bufB[na,na+nbk): thread t produces outputs [t*V, t*V+V)
+      const uint32_t mlen = na + nbk;
+      const uint32_t d0 = threadIdx.x * V;
+      SK r[V];
+      if (d0 < mlen) {
+        uint32_t lo2 = d0 > nbk ? d0 - nbk : 0, hi2 = min(d0, na);
+        while (lo2 < hi2) {
+          const uint32_t mid = (lo2 + hi2) >> 1;
+          if (bufB[BS::pad(mid)] <= bufB[BS::pad(na + d0 - 1 - mid)]) lo2 = mid + 1; else hi2 = mid;
+        }
+        uint32_t ia = lo2, ib = d0 - lo2;
+        SK a = ia < na ? bufB[BS::pad(ia)] : KeyTraits<SK>::kMax;
+        SK b = ib < nbk ? bufB[BS::pad(na + ib)] : KeyTraits<SK>::kMax;
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+          const bool takeA = ib >= nbk || (ia < na && a <= b);
+          r[k] = takeA ? a : b;
+          if (takeA) {
+            ia++;
+            a = ia < na ? bufB[BS::pad(ia)] : KeyTraits<SK>::kMax;
+          } else {
+            ib++;
+            b = ib < nbk ? bufB[BS::pad(na + ib)] : KeyTraits<SK>::kMax;
+          }
+        }
+      }
+      if (!last) {
+#pragma unroll
+        for (int k = 0; k < V; k++)
+          if (d0 + k < mlen) bufA[BS::pad(d0 + k)] = r[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+          const uint32_t pos = mbeg + d0 + k;
+          if (d0 + k < mlen) {
+            if constexpr (PAIRS) {
+              const uint32_t src_pos = uint32_t(r[k]);  // position in the bucket's gathered order
+              dst[rc.out + pos] = uint32_t(r[k] >> 32);
+              vdst[rc.out + pos] = partsV[src_pos / chunk][src_pos % chunk];
+            } else {
+              dst[rc.out + pos] = r[k];
+            }
+          }
+        }
+      }
+    }
+    cluster.sync();  // the next bucket may not overwrite shared memory others still read
   }
 }
 

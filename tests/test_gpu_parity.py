@@ -17,8 +17,10 @@ import paper_2407_14801_b200 as sq  # noqa: E402
 @pytest.fixture(autouse=True)
 def _reset_tile():
     sq.set_max_tile(0)
+    sq.set_cluster_sort(True)
     yield
     sq.set_max_tile(0)
+    sq.set_cluster_sort(True)
 
 
 def to_dev(a):
@@ -139,24 +141,29 @@ def test_sizes_u64(n):
     assert np.array_equal(gpu_sort(keys, 7), np.sort(keys))
 
 
+@pytest.mark.parametrize("cluster", [False, True])
 @pytest.mark.parametrize("tile", [64, 256, 1024])
 @pytest.mark.parametrize("n", [5000, 70001, 300000])
-def test_forced_multilevel_vs_oracle(tile, n):
-    # a small on-chip tile forces SquareSort levels inside columns and buckets
+def test_forced_multilevel_vs_oracle(tile, n, cluster):
+    # a small on-chip tile forces cluster sorts (buckets up to 16 tiles) and, past
+    # them or with clusters off, SquareSort levels inside columns and buckets
     sq.set_max_tile(tile)
+    sq.set_cluster_sort(cluster)
     rng = np.random.default_rng(tile * 7 + n)
     for card in (2**32, 1000, 3):
         keys = rng.integers(0, card, n, dtype=np.uint64).astype(np.uint32)
         want, _ = oracle_sort(keys, 11)
         got = gpu_sort(keys, 11)
         assert np.array_equal(got, want), card
-        if card == 2**32 and n >= 16 * tile:
+        if card == 2**32 and n >= 16 * tile and not cluster:
             assert sq.get_stats()["levels"] >= 2
 
 
+@pytest.mark.parametrize("cluster", [False, True])
 @pytest.mark.parametrize("tile", [64, 512])
-def test_forced_multilevel_pairs_and_u64(tile):
+def test_forced_multilevel_pairs_and_u64(tile, cluster):
     sq.set_max_tile(tile)
+    sq.set_cluster_sort(cluster)
     rng = np.random.default_rng(tile)
     n = 50000
     k = rng.integers(0, 50, n, dtype=np.uint64).astype(np.uint32)
