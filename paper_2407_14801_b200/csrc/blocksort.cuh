@@ -69,55 +69,61 @@ struct BlockSort {
   static constexpr int V = V_;
   static constexpr int TILE = NT * V;
   static constexpr int PER = 128 / sizeof(K);  // elements per 128-byte pad period
+  static constexpr int PSH = sizeof(K) == 4 ? 5 : 4;
   static constexpr int SMEM_ELEMS = TILE + TILE / PER + 1;
   static constexpr size_t SMEM_BYTES = size_t(SMEM_ELEMS) * sizeof(K);
 
-  __device__ __forceinline__ static int pad(int i) { return i + i / PER; }
+  // one pad element per 128 bytes keeps the blocked per-thread accesses conflict-free
+  __device__ __forceinline__ static uint32_t pad(uint32_t i) { return i + (i >> PSH); }
 
   // Sort the TILE keys held in s[pad(0..TILE-1)] (padding slots hold KeyTraits::kMax).
   // On return s holds the sorted tile (padded layout); a __syncthreads() has
   // been executed so all threads may read it.
   __device__ static void sort_smem(K* s) {
-    const int t = threadIdx.x;
+    const uint32_t t = threadIdx.x;
     K r[V];
 #pragma unroll
     for (int j = 0; j < V; j++) r[j] = s[pad(t * V + j)];
     thread_sort<K, V>(r);
 #pragma unroll 1
-    for (int w = V; w < TILE; w *= 2) {
+    for (uint32_t w = V; w < (uint32_t)TILE; w *= 2) {
       __syncthreads();  // previous readers of s are done
 #pragma unroll
       for (int j = 0; j < V; j++) s[pad(t * V + j)] = r[j];
       __syncthreads();
-      const int g = (t * V) & ~(2 * w - 1);  // first index of the run pair
-      const int diag = t * V - g;
-      const K* A = s;  // indices g .. g+w-1   (through pad())
-      const int a0 = g, b0 = g + w;
+      const uint32_t a0 = (t * V) & ~(2 * w - 1);  // run A = [a0, b0), run B = [b0, b0 + w)
+      const uint32_t b0 = a0 + w, bend = b0 + w;
+      const uint32_t diag = t * V - a0;
       // merge path: smallest i with A[i] > B[diag-1-i] (ties taken from A first)
-      int lo = diag > w ? diag - w : 0;
-      int hi = diag < w ? diag : w;
+      uint32_t lo = diag > w ? diag - w : 0;
+      uint32_t hi = diag < w ? diag : w;
       while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        K a = A[pad(a0 + mid)];
-        K b = A[pad(b0 + diag - 1 - mid)];
-        if (a <= b) lo = mid + 1; else hi = mid;
+        const uint32_t mid = (lo + hi) >> 1;
+        const K x = s[pad(a0 + mid)];
+        const K y = s[pad(b0 + diag - 1 - mid)];
+        const bool le = x <= y;
+        lo = le ? mid + 1 : lo;
+        hi = le ? hi : mid;
       }
-      int i = lo, jj = diag - lo;
-      K a = i < w ? A[pad(a0 + i)] : KeyTraits<K>::kMax;
-      K b = jj < w ? A[pad(b0 + jj)] : KeyTraits<K>::kMax;
-      // Serial merge.  Exhausted runs read as kMax: a real kMax key and the
-      // sentinel are equal values, so which one is emitted never matters.
+      uint32_t ja = a0 + lo, jb = b0 + diag - lo;
+      K a = ja < b0 ? s[pad(ja)] : KeyTraits<K>::kMax;
+      K b = jb < bend ? s[pad(jb)] : KeyTraits<K>::kMax;
+      // Branch-free serial merge.  An exhausted run reads as kMax: a real kMax
+      // key and the sentinel are equal values (pair composites never equal
+      // kMax), so which one is emitted never changes the output.  Reads one
+      // past a run stay inside the buffer (index <= TILE).
 #pragma unroll
       for (int k = 0; k < V; k++) {
-        bool takeA = a <= b;
+        const bool takeA = a <= b;
         r[k] = takeA ? a : b;
-        if (takeA) {
-          i++;
-          a = i < w ? A[pad(a0 + i)] : KeyTraits<K>::kMax;
-        } else {
-          jj++;
-          b = jj < w ? A[pad(b0 + jj)] : KeyTraits<K>::kMax;
-        }
+        const uint32_t jn = (takeA ? ja : jb) + 1;
+        const uint32_t end = takeA ? b0 : bend;
+        K v = s[pad(jn)];
+        v = jn < end ? v : KeyTraits<K>::kMax;
+        a = takeA ? v : a;
+        b = takeA ? b : v;
+        ja = takeA ? jn : ja;
+        jb = takeA ? jb : jn;
       }
     }
     __syncthreads();
