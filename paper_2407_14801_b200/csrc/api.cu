@@ -280,7 +280,7 @@ template <> struct TrCfg<uint32_t, true> { static constexpr int NT = 256, S = 40
 template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
 // piece-major transpose (sort path): threads, piece size, fragments per piece
 template <typename K, bool PAIRS> struct PmTr;
-template <> struct PmTr<uint32_t, false> { static constexpr int NT = 512, S = 8192, F = 256; };
+template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128; };
 template <> struct PmTr<uint32_t, true> { static constexpr int NT = 512, S = 4096, F = 256; };
 template <> struct PmTr<uint64_t, false> { static constexpr int NT = 512, S = 4096, F = 256; };
 
@@ -426,7 +426,7 @@ struct Engine {
   // bucket sorts gather from T and write the sorted buckets back into X.
   void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
     using TC = PmTr<K, PAIRS>;
-    using CF = PmCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
+    using CF = TmaCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
     ensure_scratch();
     g_stats.levels++;
     const int T = 1 - X;
@@ -562,13 +562,13 @@ struct Engine {
       check_launch("k_tile_scan");
     }
     {
-      auto f = k_transpose_pm<K, PAIRS, TC::NT, TC::S, TC::F>;
+      auto f = k_transpose_tma<K, PAIRS, TC::NT, TC::S, TC::F>;
       static bool init = false;
       if (!init) { set_smem(f, CF::SMEM); init = true; }
       ProfScope ps("transpose", st);
       f<<<ntiles, TC::NT, CF::SMEM, st>>>(dL, dTiles, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr,
                                           piv, segmat, pout, ppre);
-      check_launch("k_transpose_pm");
+      check_launch("k_transpose_tma");
     }
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};

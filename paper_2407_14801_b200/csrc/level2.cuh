@@ -558,6 +558,334 @@ k_transpose_pm(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, 
 }
 
 // ------------------------------------------------------------------------------
+// TMA helpers (cp.async.bulk: SASS UBLKCP) and an mbarrier.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// global -> shared bulk copy, completion counted on `bar` (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+// shared -> global bulk copy (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_addr(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
+// ------------------------------------------------------------------------------
+// SkewTranspose, piece-major, TMA-staged.  Same contract as k_transpose_pm.
+// Per piece (up to S keys from up to F runs of the tile's column-major stream):
+//  * every run fragment is fetched with ONE bulk copy (its 16-byte-aligned
+//    envelope, placed so the keys keep their alignment), completion on an
+//    mbarrier;
+//  * warp w owns a contiguous range of fragments: lane b binary-searches the
+//    end of bucket b inside the fragment (a sorted run: each bucket is one
+//    contiguous group), giving the (fragment, bucket) counts and a per-warp
+//    running prefix per bucket;
+//  * a block scan over warps and buckets gives every group's offset in the
+//    piece's bucket-major image; each key finds its bucket by a 5-step shuffle
+//    search over the lanes' bucket ends and is stored at its offset;
+//  * the image is written back with one bulk store (unaligned head and tail
+//    by threads); the bucket prefix goes to the piece tables.
+template <typename K, bool PAIRS, int NT, int S, int F>
+struct TmaCfg {
+  static constexpr int NW = NT / 32;
+  static constexpr int SLK = 48 / (int)sizeof(K);  // slack elements per fragment slot
+  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t STG = al((S + SLK * F + 16) * sizeof(K));
+  static constexpr size_t VSTG = PAIRS ? al((S + 12 * F + 16) * 4) : 0;
+  static constexpr size_t OUT = al((S + 16 / sizeof(K) + 4) * sizeof(K));
+  static constexpr size_t VOUT = PAIRS ? al((S + 8) * 4) : 0;
+  static constexpr size_t CODE = al((S + SLK * F + 16) * 4);
+  static constexpr size_t off_stage = 0;
+  static constexpr size_t off_vstage = off_stage + STG;
+  static constexpr size_t off_code = off_vstage + VSTG;  // per stage slot: bucket | rank << 5
+  static constexpr size_t off_out = off_code + CODE;
+  static constexpr size_t off_vout = off_out + OUT;
+  static constexpr size_t off_frag = al(off_vout + VOUT);  // fstart[F+1], fsrc[F], fe[F], fve[F]
+  static constexpr size_t off_wsum = al(off_frag + (4 * F + 1) * 4);  // NW x 32 u32
+  static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);
+  static constexpr size_t off_bval = al(off_misc + (64 + 2 * 33) * 4);
+  static constexpr size_t off_bar = al(off_bval + kTB * (sizeof(K) + 4));
+  static constexpr size_t SMEM = off_bar + 16;
+};
+
+template <typename K, bool PAIRS, int NT, int S, int F>
+__global__ void __launch_bounds__(NT)
+k_transpose_tma(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const K* __restrict__ src,
+                K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+                const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint32_t* __restrict__ pout,
+                uint16_t* __restrict__ ppre) {
+  using C = TmaCfg<K, PAIRS, NT, S, F>;
+  static_assert(F <= NT && F % 32 == 0 && S <= 65535 && NT % 32 == 0, "shape");
+  constexpr int EB = sizeof(K);
+  extern __shared__ __align__(128) unsigned char sm[];
+  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
+  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
+  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);
+  unsigned char* outraw = sm + C::off_out;
+  unsigned char* voutraw = sm + C::off_vout;
+  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
+  uint32_t* fsrc = fstart + F + 1;
+  uint32_t* fe = fsrc + F;   // stage element index of the fragment's first key
+  uint32_t* fve = fe + F;    // vstage element index (pairs)
+  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
+  uint32_t* poff = misc + 64;  // 33 entries: bucket offsets in the piece image
+  K* bval = reinterpret_cast<K*>(sm + C::off_bval);
+  uint32_t* bdupv = reinterpret_cast<uint32_t*>(sm + C::off_bval + kTB * sizeof(K));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::off_bar);
+
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const TileInfo ti = tiles[blockIdx.x];
+  const LevelSeg sg = segs[ti.seg];
+  const uint32_t bt = ti.bt;
+  const uint32_t b0 = bt * kTB;
+  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
+  const K* P = piv + sg.piv_base;
+  if (t < (int)nb - 1) {  // internal boundary b0+1+t ends bucket t of the tile
+    const uint32_t j = b0 + 1 + t;
+    bval[t] = P[j - 1];
+    bdupv[t] = (j >= 2 && P[j - 2] == P[j - 1]) ? 1u : 0u;
+  }
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  uint32_t oc = ti.out, npc = 0;
+  uint32_t c = 0, o = 0;
+  const uint32_t* rows = segmat + sg.segmat_base;
+  const uint32_t rstride = sg.nbt + 1;
+
+  while (c < sg.ncols) {
+    // ---- window of F runs, prefix sums; the piece takes up to S keys
+    uint32_t len = 0, srcpos = 0;
+    if (t < F && c + t < sg.ncols) {
+      const uint32_t* row = rows + uint64_t(c + t) * rstride;
+      const uint32_t a = row[bt], e = row[bt + 1];
+      const uint32_t skip = t == 0 ? o : 0;
+      len = e - a - skip;
+      srcpos = sg.off + (c + t) * sg.rows + a + skip;
+    }
+    uint32_t wtot;
+    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
+    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
+    const int inpiece = (t < (int)nwin && ex < (uint32_t)S) ? 1 : 0;
+    const uint32_t nf = __syncthreads_count(inpiece);
+    const uint32_t Pn = min((uint32_t)S, wtot);
+    // ---- issue the bulk copies (thread f owns fragment f)
+    if (t < (int)nf) {
+      const uint32_t flen = min(ex + len, Pn) - ex;
+      fstart[t] = ex;
+      fsrc[t] = srcpos;
+      const uintptr_t ga = reinterpret_cast<uintptr_t>(src + srcpos);
+      const uint32_t mis = (uint32_t)(ga & 15);
+      const uint32_t slot = (uint32_t)C::al((ex + C::SLK * t) * EB);  // byte offset, 16-aligned
+      fe[t] = (slot + mis) / EB;
+      if (flen) {
+        const uint32_t bytes = (mis + flen * EB + 15) & ~15u;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(reinterpret_cast<unsigned char*>(stage) + slot, reinterpret_cast<const void*>(ga - mis), bytes,
+                 bar);
+      }
+      if (PAIRS) {
+        const uintptr_t va = reinterpret_cast<uintptr_t>(vsrc + srcpos);
+        const uint32_t vmis = (uint32_t)(va & 15);
+        const uint32_t vslot = (uint32_t)C::al((ex + 12 * t) * 4);
+        fve[t] = (vslot + vmis) / 4;
+        if (flen) {
+          const uint32_t vbytes = (vmis + flen * 4 + 15) & ~15u;
+          mbar_expect_tx(bar, vbytes);
+          bulk_g2s(reinterpret_cast<unsigned char*>(vstage) + vslot, reinterpret_cast<const void*>(va - vmis), vbytes,
+                   bar);
+        }
+      }
+    }
+    if (t == 0) fstart[nf] = Pn;
+    // next window position (same rule as k_transpose_pm)
+    uint32_t nc, no;
+    if (wtot <= (uint32_t)S) {
+      nc = c + nwin;
+      no = 0;
+    } else {
+      __syncthreads();
+      const uint32_t last = nf - 1;
+      const uint32_t used = Pn - fstart[last];
+      const uint32_t* row = rows + uint64_t(c + last) * rstride;
+      const uint32_t base = last == 0 ? o : 0;
+      const uint32_t full = row[bt + 1] - row[bt] - base;
+      if (used < full) {
+        nc = c + last;
+        no = base + used;
+      } else {
+        nc = c + last + 1;
+        no = 0;
+      }
+    }
+    __syncthreads();  // all expect_tx posted before the single arrival
+    if (Pn > 0) {
+      if (t == 0) mbar_arrive(bar);
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      // ---- pass 1: warp w walks its fragments in 32-key chunks (sorted keys, one per
+      // lane).  Lane j finds where boundary j falls among the chunk's keys (5 shuffle
+      // steps) -- the end of bucket j in the chunk; each key then finds its bucket
+      // among those ends (5 steps).  Its rank among the warp's keys of that bucket
+      // (stream order) is the bucket's running count plus its offset in the group.
+      const uint32_t per = (nf + C::NW - 1) / C::NW;
+      const uint32_t f0 = min(nf, w * per), f1 = min(nf, f0 + per);
+      const bool has_thr = lane < (int)nb - 1;
+      const K thr_v = has_thr ? bval[lane] : K(0);
+      const bool thr_d = has_thr && bdupv[lane] != 0;
+      uint32_t run = 0;  // lane b: keys of bucket b in this warp's earlier chunks
+      for (uint32_t f = f0; f < f1; f++) {
+        const uint32_t flen = fstart[f + 1] - fstart[f];
+        const K* fk = stage + fe[f];
+        uint32_t* fc = code + fe[f];
+        for (uint32_t c0 = 0; c0 < flen; c0 += 32) {
+          const uint32_t cl = min(32u, flen - c0);
+          const K x = lane < (int)cl ? fk[c0 + lane] : KeyTraits<K>::kMax;
+          uint32_t p = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const K y = __shfl_sync(0xffffffffu, x, p + st - 1);
+            if (has_thr && before_boundary(y, thr_v, thr_d)) p += st;
+          }
+          {  // the 5 steps reach at most 31: all 32 keys may lie before the boundary
+            const K yl = __shfl_sync(0xffffffffu, x, 31);
+            if (p == 31 && has_thr && before_boundary(yl, thr_v, thr_d)) p = 32;
+          }
+          const uint32_t endb = has_thr ? min(p, cl) : cl;
+          uint32_t startb = __shfl_up_sync(0xffffffffu, endb, 1);
+          if (lane == 0) startb = 0;
+          uint32_t bk = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, endb, bk + st - 1);
+            if (e <= (uint32_t)lane) bk += st;
+          }
+          const uint32_t rk = __shfl_sync(0xffffffffu, run - startb, bk) + lane;
+          if (lane < (int)cl) fc[c0 + lane] = bk | (rk << 5);
+          run += endb - startb;
+        }
+      }
+      wsum[w * 32 + lane] = run;
+      __syncthreads();
+      // ---- block scan: per bucket, warp bases (exclusive over warps) + bucket offsets in the piece
+      if (w == 0) {
+        uint32_t tot = 0;
+        for (int ww = 0; ww < C::NW; ww++) {
+          const uint32_t v = wsum[ww * 32 + lane];
+          wsum[ww * 32 + lane] = tot;
+          tot += v;
+        }
+        const uint32_t v = lane < (int)nb ? tot : 0;
+        uint32_t xs = v;
+        for (int q = 1; q < 32; q <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
+          if (lane >= q) xs += y;
+        }
+        poff[lane] = xs - v;
+        if (lane == 31) poff[kTB] = xs;
+        for (int ww = 0; ww < C::NW; ww++) wsum[ww * 32 + lane] += xs - v;
+      }
+      __syncthreads();
+      // ---- pass 2: every key to its place in the piece's bucket-major image (shifted for the bulk store)
+      const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
+      K* outb = reinterpret_cast<K*>(outraw) + oshift;
+      const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
+      uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
+      const uint32_t* wbase = wsum + w * 32;
+      for (uint32_t f = f0; f < f1; f++) {
+        const uint32_t flen = fstart[f + 1] - fstart[f];
+        const K* fk = stage + fe[f];
+        const uint32_t* fc = code + fe[f];
+        const uint32_t* fv = PAIRS ? vstage + fve[f] : nullptr;
+        for (uint32_t i = lane; i < flen; i += 32) {
+          const uint32_t cd = fc[i];
+          const uint32_t dpos = wbase[cd & 31] + (cd >> 5);
+          outb[dpos] = fk[i];
+          if (PAIRS) vout[dpos] = fv[i];
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+      // ---- write the image: bulk store of the aligned body, threads do head and tail
+      {
+        const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
+        const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
+        const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
+        if (a1 > a0) {
+          if (t == 0) {
+            bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
+                     (uint32_t)(a1 - a0));
+          }
+          const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
+          if (t < (int)nh) dst[oc + t] = outb[t];
+          if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
+        } else {
+          for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
+        }
+        if (PAIRS) {
+          const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
+          const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
+          const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
+          if (c1 > c0) {
+            if (t == 0)
+              bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
+                       (uint32_t)(c1 - c0));
+            const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
+            if (t < (int)nh) vdst[oc + t] = vout[t];
+            if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
+          } else {
+            for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
+          }
+        }
+        if (t == 0) bulk_commit();
+      }
+      const uint32_t pe = ti.piece_base + npc;
+      if (t == 0) pout[pe] = oc;
+      if (t <= kTB) ppre[uint64_t(pe) * kPP + t] = (uint16_t)poff[t];
+      oc += Pn;
+      npc++;
+      if (t == 0) bulk_wait_read0();  // the image buffer may be rewritten next piece
+    }
+    c = nc;
+    o = no;
+    __syncthreads();
+  }
+  if (t == 0) {
+    tiles[blockIdx.x].npieces = npc;
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------
 // Bucket planning, per segment (one CTA): bucket sizes from the piece tables,
 // final offsets (exclusive scan, P:283 / P:461), RNG node keys, and the work
 // lists: single-value buckets (copy), on-chip classes, oversize.
