@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -109,6 +110,7 @@ static void prof_collect() {  // after a stream sync
 // ------------------------------------------------------------------ options
 static uint32_t g_max_tile = 0;  // 0 = default
 static int g_cluster = 1;        // cluster sorts for buckets beyond one CTA
+static int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv("SQ_CONCURRENT_CLASSES")) : 0;
 
 // ------------------------------------------------------------------ device check
 static void check_device() {
@@ -285,9 +287,33 @@ template <> struct PmTr<uint32_t, true> { static constexpr int NT = 512, S = 409
 template <> struct PmTr<uint64_t, false> { static constexpr int NT = 512, S = 4096, F = 256; };
 
 // cluster bucket sort: per-CTA tile (threads x keys) for 32-bit / 64-bit sort keys
+// (small per-CTA tiles keep 3 CTAs per SM resident; the big one serves the
+// rare buckets beyond 16 small tiles)
 template <typename SK> struct ClusterCfg;
-template <> struct ClusterCfg<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
-template <> struct ClusterCfg<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
+template <> struct ClusterCfg<uint32_t> { static constexpr int NT = 256, V = 32, TILE = 8192; };
+template <> struct ClusterCfg<uint64_t> { static constexpr int NT = 256, V = 16, TILE = 4096; };
+template <typename SK> struct ClusterBig;
+template <> struct ClusterBig<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
+template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
+// largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
+template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
+
+// Side streams for running the bucket-class kernels concurrently.
+struct SideStreams {
+  static constexpr int N = 4;
+  cudaStream_t s[N] = {};
+  int dev = -1;
+};
+static SideStreams& side_streams() {
+  static thread_local SideStreams ss;
+  int dev = 0;
+  SQ_CUDA(cudaGetDevice(&dev));
+  if (ss.dev != dev) {
+    for (auto& x : ss.s) SQ_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    ss.dev = dev;
+  }
+  return ss;
+}
 
 // ------------------------------------------------------------------ the engine
 struct Seg {
@@ -378,10 +404,10 @@ struct Engine {
     }
   }
 
-  template <int CL>
-  void launch_cluster_t(const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs, const TileInfo* tiles,
-                        int T, int X, const uint32_t* pout, const uint16_t* ppre, uint32_t nbuck) {
-    using CC = ClusterCfg<SK>;
+  template <int CL, typename CC>
+  void launch_cluster_t(cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
+                        const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
+                        uint32_t nbuck) {
     using BS = BlockSort<SK, CC::NT, CC::V>;
     const size_t smem = 2 * BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * CC::NT + 64) * 4;
     auto f = k_clustersort<K, CC::NT, CC::V, CL, PAIRS>;
@@ -394,7 +420,7 @@ struct Engine {
     attr[0].val.clusterDim.z = 1;
     cfg.blockDim = dim3(CC::NT);
     cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
+    cfg.stream = cs;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (max_clusters < 0) {
@@ -407,18 +433,22 @@ struct Engine {
     }
     if (max_clusters <= 0) throw Error(SQ_ERR_CUDA, "cluster of " + std::to_string(CL) + " CTAs cannot be scheduled");
     cfg.gridDim = dim3(CL * std::min<uint32_t>(max_clusters, nbuck));
-    ProfScope ps("clustersort", st);
+    ProfScope ps("clustersort", cs);
     SQ_CUDA(cudaLaunchKernelEx(&cfg, f, recs, tiles, lst, cnt, (const K*)kb[T], kb[X],
                                (const uint32_t*)(PAIRS ? vb[T] : nullptr), PAIRS ? vb[X] : nullptr, pout, ppre));
     check_launch("k_clustersort");
   }
 
-  void launch_cluster(uint32_t cl, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
+  // cl > 0: clusters of `cl` small tiles; cl < 0: clusters of -cl big tiles
+  void launch_cluster(int cl, cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
                       const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
                       uint32_t nbuck) {
-    if (cl == 4) launch_cluster_t<4>(lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
-    else if (cl == 8) launch_cluster_t<8>(lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
-    else launch_cluster_t<16>(lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    using CS = ClusterCfg<SK>;
+    using CB = ClusterBig<SK>;
+    if (cl == 4) launch_cluster_t<4, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    else if (cl == 8) launch_cluster_t<8, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    else if (cl == 16) launch_cluster_t<16, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    else launch_cluster_t<16, CB>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
   }
 
   // One SquareSort level (Alg 1) for a batch of segments that live in buffer X,
@@ -573,17 +603,25 @@ struct Engine {
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};
     po.ncls = 0;
-    uint32_t cls_cl[12] = {0};  // 0 = one CTA, else cluster size
-    for (uint32_t t : kTiles)
-      if (t <= cap && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
-    po.max_tile = cap;
-    if (g_cluster) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
-      const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
-      for (uint32_t cl : {4u, 8u, 16u}) {
-        if (cl * ct <= po.max_tile) continue;
-        cls_cl[po.ncls] = cl;
-        po.cls_tile[po.ncls++] = cl * ct;
-        po.max_tile = cl * ct;
+    int cls_cl[12] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
+    {
+      const uint32_t one = g_cluster && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
+      for (uint32_t t : kTiles)
+        if (t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
+      po.max_tile = one;
+      if (g_cluster) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
+        const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
+        for (int cl : {4, 8, 16}) {
+          if (cl * ct <= po.max_tile) continue;
+          cls_cl[po.ncls] = cl;
+          po.cls_tile[po.ncls++] = cl * ct;
+          po.max_tile = cl * ct;
+        }
+        if (!g_max_tile && 16u * ClusterBig<SK>::TILE > po.max_tile) {
+          cls_cl[po.ncls] = -16;
+          po.cls_tile[po.ncls++] = 16u * ClusterBig<SK>::TILE;
+          po.max_tile = 16u * ClusterBig<SK>::TILE;
+        }
       }
     }
     po.cap_per_list = (uint32_t)buck_tot;
@@ -616,11 +654,18 @@ struct Engine {
       SQ_CUDA(cudaMemcpyAsync(dbg->info, dinf, 8, cudaMemcpyDeviceToDevice, st));
       return;
     }
-    // 6. bucket sorts: gather from T, sort on chip, write to X
-    for (uint32_t c = 0; c < po.ncls; c++) {
+    // 6. bucket sorts: gather from T, sort on chip, write to X.  The
+    // size classes are independent: their kernels run concurrently on side streams.
+    SideStreams& ss = side_streams();
+    cudaEvent_t fork = pool_event();
+    SQ_CUDA(cudaEventRecord(fork, st));
+    for (int i = 0; i < SideStreams::N; i++) SQ_CUDA(cudaStreamWaitEvent(ss.s[i], fork, 0));
+    int rr = 0;
+    for (int c = (int)po.ncls - 1; c >= 0; c--) {  // biggest classes first
       const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
+      cudaStream_t cs = g_concurrent_classes ? ss.s[rr++ % SideStreams::N] : st;
       if (cls_cl[c]) {
-        launch_cluster(cls_cl[c], lst, po.count + c, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
+        launch_cluster(cls_cl[c], cs, lst, po.count + c, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
         continue;
       }
       with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
@@ -633,13 +678,20 @@ struct Engine {
           set_smem(f, smem);
           grid = wave_grid(f, NT, smem);
         }
-        ProfScope ps("bucketsort", st);
-        f<<<(uint32_t)std::min<uint64_t>(grid, buck_tot), NT, smem, st>>>(recs, dTiles, lst, po.count + c, kb[T],
+        ProfScope ps("bucketsort", cs);
+        f<<<(uint32_t)std::min<uint64_t>(grid, buck_tot), NT, smem, cs>>>(recs, dTiles, lst, po.count + c, kb[T],
                                                                          kb[X], PAIRS ? vb[T] : nullptr,
                                                                          PAIRS ? vb[X] : nullptr, pout, ppre);
         check_launch("k_bucketsort");
       });
     }
+    for (int i = 0; i < SideStreams::N; i++) {
+      cudaEvent_t j = pool_event();
+      SQ_CUDA(cudaEventRecord(j, ss.s[i]));
+      SQ_CUDA(cudaStreamWaitEvent(st, j, 0));
+      g_event_pool.push_back(j);
+    }
+    g_event_pool.push_back(fork);
     {  // single-value buckets (copied) and oversize buckets (made contiguous)
       ProfScope ps("gather", st);
       const uint32_t g = (uint32_t)std::min<uint64_t>(buck_tot, 4 * num_sms());
