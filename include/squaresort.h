@@ -146,10 +146,13 @@ void sq_get_stats(sq_stats *out);
  * other values. */
 int sq_set_max_tile(uint32_t max_tile);
 
-/* Tuning/test knob: buckets larger than one CTA's tile are sorted by a
- * thread-block cluster of 4, 8 or 16 CTAs (default, enable = 1); with 0 they
- * recurse into another SquareSort level instead.  Process-wide. */
-int sq_set_cluster_sort(int enable);
+/* Tuning/test knob: how buckets larger than one CTA's tile (16384 32-bit or
+ * 8192 64-bit keys by default) are sorted.  0: another SquareSort level
+ * (P:291-293); 1 (default): the multi-CTA base case -- chunks sorted on chip,
+ * then merge passes through HBM, up to 16 chunks (larger buckets recurse);
+ * 2: thread-block clusters of 4/8/16 CTAs merging through distributed shared
+ * memory.  Process-wide; SQ_ERR_INVALID_ARGUMENT for other values. */
+int sq_set_big_bucket_mode(int mode);
 
 /* Per-kernel device timing: when enabled, every kernel the library launches is
  * bracketed by CUDA events on its stream and the elapsed times accumulate per

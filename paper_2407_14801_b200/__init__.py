@@ -22,7 +22,7 @@ STATUS = {0: "SQ_OK", 1: "SQ_ERR_INVALID_ARGUMENT", 2: "SQ_ERR_OUT_OF_MEMORY", 3
 EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_host",
            "sq_sort_u64_host", "sq_sort_pairs_u32_u32_host", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
-           "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_cluster_sort"]
+           "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode"]
 
 
 class SqError(RuntimeError):
@@ -72,8 +72,8 @@ def lib():
         L.sq_get_stats.restype = None
         L.sq_set_max_tile.argtypes = [u32]
         L.sq_set_max_tile.restype = ctypes.c_int
-        L.sq_set_cluster_sort.argtypes = [ctypes.c_int]
-        L.sq_set_cluster_sort.restype = ctypes.c_int
+        L.sq_set_big_bucket_mode.argtypes = [ctypes.c_int]
+        L.sq_set_big_bucket_mode.restype = ctypes.c_int
         L.sq_profile.argtypes = [ctypes.c_int]
         L.sq_profile.restype = ctypes.c_int
         L.sq_profile_read.argtypes = [ctypes.c_char_p, sz]
@@ -193,8 +193,12 @@ def set_max_tile(t: int):
     _check(lib().sq_set_max_tile(t))
 
 
-def set_cluster_sort(enable: bool):
-    _check(lib().sq_set_cluster_sort(1 if enable else 0))
+BIG_LEVEL, BIG_MERGE, BIG_CLUSTER = 0, 1, 2
+
+
+def set_big_bucket_mode(mode: int):
+    """0: recurse into a SquareSort level, 1: multi-CTA merge sort (default), 2: clusters."""
+    _check(lib().sq_set_big_bucket_mode(mode))
 
 
 def profile(enable: bool = True):

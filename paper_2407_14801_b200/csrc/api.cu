@@ -109,7 +109,9 @@ static void prof_collect() {  // after a stream sync
 
 // ------------------------------------------------------------------ options
 static uint32_t g_max_tile = 0;  // 0 = default
-static int g_cluster = 1;        // cluster sorts for buckets beyond one CTA
+// buckets larger than one CTA's tile: 0 = another SquareSort level,
+// 1 = multi-CTA merge sort (default), 2 = thread-block cluster sort
+static int g_big_mode = 1;
 static int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv("SQ_CONCURRENT_CLASSES")) : 0;
 
 // ------------------------------------------------------------------ device check
@@ -298,6 +300,9 @@ template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16,
 // largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
 template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
 
+// merge passes: threads x outputs per thread (tile = NT * VM keys)
+template <typename K> struct MergeCfg { static constexpr int NT = 512, VM = 16; };
+
 // Side streams for running the bucket-class kernels concurrently.
 struct SideStreams {
   static constexpr int N = 4;
@@ -333,16 +338,16 @@ struct Engine {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;  // on-chip sort key
   cudaStream_t st;
   Arena& ar;
-  K* kb[2];
-  uint32_t* vb[2];
+  K* kb[3];        // [0] caller's buffer, [1] scratch, [2] merge-sort scratch
+  uint32_t* vb[3];
   size_t n;
   uint32_t cap;
 
   Engine(cudaStream_t s, Arena& a, K* keys, uint32_t* vals, size_t n_) : st(s), ar(a), n(n_) {
     kb[0] = keys;
-    kb[1] = nullptr;
+    kb[1] = kb[2] = nullptr;
     vb[0] = vals;
-    vb[1] = nullptr;
+    vb[1] = vb[2] = nullptr;
     cap = key_max_tile<SK>();
     if (g_max_tile && g_max_tile < cap) cap = g_max_tile;
   }
@@ -350,6 +355,10 @@ struct Engine {
   void ensure_scratch() {
     if (!kb[1]) kb[1] = (K*)ar.alloc(n * sizeof(K));
     if (PAIRS && !vb[1]) vb[1] = (uint32_t*)ar.alloc(n * sizeof(uint32_t));
+  }
+  void ensure_third() {
+    if (!kb[2]) kb[2] = (K*)ar.alloc(n * sizeof(K));
+    if (PAIRS && !vb[2]) vb[2] = (uint32_t*)ar.alloc(n * sizeof(uint32_t));
   }
 
   void copy_ranges(const std::vector<SegDesc>& r, int src, int dst) {
@@ -605,11 +614,11 @@ struct Engine {
     po.ncls = 0;
     int cls_cl[12] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
     {
-      const uint32_t one = g_cluster && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
+      const uint32_t one = g_big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
       for (uint32_t t : kTiles)
         if (t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
       po.max_tile = one;
-      if (g_cluster) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
+      if (g_big_mode == 2) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
         const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
         for (int cl : {4, 8, 16}) {
           if (cl * ct <= po.max_tile) continue;
@@ -624,8 +633,21 @@ struct Engine {
         }
       }
     }
-    po.cap_per_list = (uint32_t)buck_tot;
-    po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 2) * buck_tot * 4);
+    uint64_t level_keys = 0;
+    for (const Seg& g : segs) level_keys += g.len;
+    po.msort_max = po.max_tile;
+    po.mtile = MergeCfg<K>::NT * MergeCfg<K>::VM;
+    po.mcap = 1;
+    if (g_big_mode == 1) {  // multi-CTA merge sort for buckets of up to 16 chunks
+      po.msort_max = 16u * po.max_tile;
+      po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
+      ensure_third();
+    }
+    po.mlist = (MTile*)ar.alloc(uint64_t(kMaxPasses) * po.mcap * sizeof(MTile));
+    po.mcount = (uint32_t*)ar.alloc(kMaxPasses * 4);
+    SQ_CUDA(cudaMemsetAsync(po.mcount, 0, kMaxPasses * 4, st));
+    po.cap_per_list = (uint32_t)(buck_tot + level_keys / std::max<uint32_t>(po.max_tile, 1) + 16);
+    po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 2) * po.cap_per_list * 4);
     po.count = (uint32_t*)ar.alloc((po.ncls + 2) * 4);
     SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 2) * 4, st));
     {
@@ -679,19 +701,37 @@ struct Engine {
           grid = wave_grid(f, NT, smem);
         }
         ProfScope ps("bucketsort", cs);
-        f<<<(uint32_t)std::min<uint64_t>(grid, buck_tot), NT, smem, cs>>>(recs, dTiles, lst, po.count + c, kb[T],
-                                                                         kb[X], PAIRS ? vb[T] : nullptr,
-                                                                         PAIRS ? vb[X] : nullptr, pout, ppre);
+        f<<<(uint32_t)std::min<uint64_t>(grid, po.cap_per_list), NT, smem, cs>>>(
+            recs, dTiles, lst, po.count + c, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
+            ppre, kb[2], PAIRS ? vb[2] : nullptr);
         check_launch("k_bucketsort");
       });
     }
     for (int i = 0; i < SideStreams::N; i++) {
       cudaEvent_t j = pool_event();
+      if (!g_concurrent_classes) break;
       SQ_CUDA(cudaEventRecord(j, ss.s[i]));
       SQ_CUDA(cudaStreamWaitEvent(st, j, 0));
       g_event_pool.push_back(j);
     }
     g_event_pool.push_back(fork);
+    if (g_big_mode == 1) {  // merge passes of the multi-CTA base case (buffers X <-> U)
+      using MC = MergeCfg<K>;
+      using BS = BlockSort<K, MC::NT, MC::VM>;
+      const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
+      auto f = k_merge_pass<K, PAIRS, MC::NT, MC::VM>;
+      static int grid = 0;
+      if (!grid) {
+        set_smem(f, smem);
+        grid = wave_grid(f, MC::NT, smem);
+      }
+      for (uint32_t p = 0; p < (uint32_t)kMaxPasses; p++) {
+        ProfScope ps("merge", st);
+        f<<<grid, MC::NT, smem, st>>>(recs, po.mlist + uint64_t(p) * po.mcap, po.mcount + p, p, kb[X], kb[2],
+                                      PAIRS ? vb[X] : nullptr, PAIRS ? vb[2] : nullptr);
+        check_launch("k_merge_pass");
+      }
+    }
     {  // single-value buckets (copied) and oversize buckets (made contiguous)
       ProfScope ps("gather", st);
       const uint32_t g = (uint32_t)std::min<uint64_t>(buck_tot, 4 * num_sms());
@@ -724,12 +764,13 @@ struct Engine {
       SQ_CUDA(cudaMemcpyAsync(hr.data(), recs, buck_tot * sizeof(BucketRec), cudaMemcpyDeviceToHost, st));
       SQ_CUDA(cudaStreamSynchronize(st));
       g_stats.host_syncs++;
-      for (uint32_t i : hl) {
+      for (uint32_t e : hl) {
+        const uint32_t i = item_bucket(e);
         over.push_back({hr[i].out, hr[i].size, hr[i].node});
         g_stats.oversize_keys += hr[i].size;
       }
     }
-    for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)piv,
+    for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)po.mlist, (void*)piv,
                     (void*)flags, (void*)p0s, (void*)info, (void*)fix, (void*)segmin})
       ar.release(p);
     if (!over.empty()) sort_batch(over, X, X, depth + 1, "bucketsort");
@@ -972,8 +1013,9 @@ int sq_profile_read(char* buf, size_t cap) {
   return out.size() < cap ? SQ_OK : SQ_ERR_INVALID_ARGUMENT;
 }
 
-int sq_set_cluster_sort(int enable) {
-  g_cluster = enable ? 1 : 0;
+int sq_set_big_bucket_mode(int mode) {
+  if (mode < 0 || mode > 2) return SQ_ERR_INVALID_ARGUMENT;
+  g_big_mode = mode;
   return SQ_OK;
 }
 

@@ -46,12 +46,25 @@ struct TileInfo {
 
 // Per-bucket record for the bucket phase.
 struct BucketRec {
-  uint32_t tile;   // tile index (TileInfo)
-  uint32_t lane;   // bucket index within the tile (0..31)
-  uint32_t out;    // absolute final offset of the sorted bucket
+  uint32_t tile;    // tile index (TileInfo)
+  uint32_t lane;    // bucket index within the tile (0..31)
+  uint32_t out;     // absolute final offset of the sorted bucket
   uint32_t size;
-  uint64_t node;   // RNG node key of the bucket (child(node, 1, b)), for deeper levels
+  uint64_t node;    // RNG node key of the bucket (child(node, 1, b)), for deeper levels
+  uint32_t chunk;   // merge-sort base case: keys per sorted chunk (= size otherwise)
+  uint32_t passes;  // merge passes after the chunk sorts (0: sorted by one CTA)
 };
+
+// Bucket-sort work items: bucket index * 16 + chunk index.
+__host__ __device__ __forceinline__ uint32_t item_bucket(uint32_t e) { return e >> 4; }
+__host__ __device__ __forceinline__ uint32_t item_chunk(uint32_t e) { return e & 15u; }
+
+// Merge-pass work item: pair j of runs, output tile t of the merged pair.
+struct MTile {
+  uint32_t bucket;
+  uint16_t pair, tile;
+};
+constexpr int kMaxPasses = 4;  // 16 chunks
 
 constexpr int kPP = kTB + 1;  // prefix entries per piece
 
@@ -890,12 +903,19 @@ k_transpose_tma(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
 // final offsets (exclusive scan, P:283 / P:461), RNG node keys, and the work
 // lists: single-value buckets (copy), on-chip classes, oversize.
 struct PlanOut {
-  uint32_t* list;       // [ncls + 2][cap_per_list] bucket indices
+  uint32_t* list;       // [ncls + 2][cap_per_list] work items (bucket * 16 + chunk)
   uint32_t* count;      // [ncls + 2] atomic counters; ncls = copy list, ncls+1 = oversize
   uint32_t cap_per_list;
   uint32_t ncls;
   uint32_t cls_tile[12];  // class tile sizes (ascending)
-  uint32_t max_tile;
+  uint32_t max_tile;      // largest bucket sorted by one CTA
+  // merge-sort base case for max_tile < size <= msort_max: chunks of <= max_tile keys,
+  // sorted by one CTA each, then up to kMaxPasses merge passes with tiles of mtile keys
+  uint32_t msort_max;
+  uint32_t mtile;
+  MTile* mlist;           // [kMaxPasses][mcap]
+  uint32_t* mcount;       // [kMaxPasses]
+  uint32_t mcap;
 };
 
 // Bucket sizes from the piece tables: CTA per tile, warp w sums pieces w, w+NW, ...
@@ -960,18 +980,38 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t*
       rc.out = excl;
       rc.size = size;
       rc.node = child_key(sg.node, 1, b);
+      rc.chunk = size;
+      rc.passes = 0;
+      const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
+      uint32_t q = 1;  // chunks
+      if (size && !single && size > po.max_tile && size <= po.msort_max) {
+        q = (size + po.max_tile - 1) / po.max_tile;
+        rc.chunk = (size + q - 1) / q;
+        uint32_t np = 0;
+        while ((1u << np) < q) np++;
+        rc.passes = np;
+        for (uint32_t p = 0; p < np; p++) {  // merge tiles of every pass
+          const uint32_t R = rc.chunk << p;
+          for (uint32_t j = 0; 2 * j * R < size; j++) {
+            const uint32_t plen = min(size, (2 * j + 2) * R) - 2 * j * R;
+            for (uint32_t t = 0; t * po.mtile < plen; t++) {
+              const uint32_t slot = atomicAdd(&po.mcount[p], 1u);
+              po.mlist[uint64_t(p) * po.mcap + slot] = MTile{(uint32_t)gi, (uint16_t)j, (uint16_t)t};
+            }
+          }
+        }
+      }
       recs[gi] = rc;
       if (size) {
         int cls;
-        const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
         if (single) cls = po.ncls;
-        else if (size > po.max_tile) cls = po.ncls + 1;
+        else if (size > po.msort_max) cls = po.ncls + 1;
         else {
           cls = 0;
-          while (po.cls_tile[cls] < size) cls++;
+          while (po.cls_tile[cls] < rc.chunk) cls++;
         }
-        const uint32_t slot = atomicAdd(&po.count[cls], 1u);
-        po.list[uint64_t(cls) * po.cap_per_list + slot] = (uint32_t)gi;
+        const uint32_t slot = atomicAdd(&po.count[cls], q);
+        for (uint32_t k = 0; k < q; k++) po.list[uint64_t(cls) * po.cap_per_list + slot + k] = (uint32_t)gi * 16 + k;
       }
     }
     __syncthreads();
@@ -1019,13 +1059,15 @@ __device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_
   }
 }
 
-// Bucket sort with gather: CTA loops over its class list.
+// Bucket sort with gather: CTA loops over its class list.  An item is a
+// whole bucket or one chunk of a merge-sorted bucket; chunks of a bucket with an
+// odd number of merge passes go to `dst_odd`, so the last pass ends in `dst`.
 template <typename K, int NT, int V, bool PAIRS>
 __global__ void __launch_bounds__(NT)
 k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
              const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
              const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst, const uint32_t* __restrict__ pout,
-             const uint16_t* __restrict__ ppre) {
+             const uint16_t* __restrict__ ppre, K* __restrict__ dst_odd, uint32_t* __restrict__ vdst_odd) {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   using BS = BlockSort<SK, NT, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1037,10 +1079,15 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
   uint32_t* misc = s_dst + NT;
   const uint32_t total = *count;
   for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
-    const BucketRec rc = recs[list[it]];
+    const uint32_t e = list[it];
+    const BucketRec rc = recs[item_bucket(e)];
     const TileInfo ti = tiles[rc.tile];
-    for (int i = threadIdx.x + rc.size; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
-    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, 0u, rc.size,
+    const uint32_t lo = item_chunk(e) * rc.chunk, hi = min(rc.size, lo + rc.chunk);
+    const uint32_t len = hi - lo;
+    K* out = (rc.passes & 1) ? dst_odd : dst;
+    uint32_t* vout = (rc.passes & 1) ? vdst_odd : vdst;
+    for (int i = threadIdx.x + len; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
@@ -1054,14 +1101,144 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     cp_async_wait_all();
     __syncthreads();
     BS::sort_smem(s);
-    for (int i = threadIdx.x; i < (int)rc.size; i += NT) {
+    for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
       if constexpr (PAIRS) {
-        dst[rc.out + i] = uint32_t(x >> 32);
-        vdst[rc.out + i] = vs[uint32_t(x)];
+        out[rc.out + lo + i] = uint32_t(x >> 32);
+        vout[rc.out + lo + i] = vs[uint32_t(x)];
       } else {
-        dst[rc.out + i] = x;
+        out[rc.out + lo + i] = x;
       }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Merge pass of the multi-CTA base case: an item is output tile t of the merge of
+// runs 2j and 2j+1 (length R = chunk << pass) of one bucket.  The tile's input
+// ranges come from two merge-path splits in global memory (32-ary warp search);
+// they are staged in shared memory, merged (each thread VM outputs, ties from the
+// earlier run: stable) and written back coalesced.  Buffers alternate so that the
+// bucket's last pass writes its final place.
+template <typename K>
+struct GSeq {  // sorted run in global memory
+  const K* p;
+  uint32_t len;
+  template <int PER>
+  __device__ __forceinline__ K at(uint32_t i) const { return p[i]; }
+};
+
+template <typename SEQ, typename K>
+__device__ __forceinline__ uint32_t warp_split(const SEQ& A, const SEQ& B, uint32_t d) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = d > B.len ? d - B.len : 0, hi = min(d, A.len);
+  while (hi > lo) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t p = lo + lane * step;
+    bool gt = true;
+    if (p < hi) gt = A.template at<1>(p) > B.template at<1>(d - 1 - p);
+    const uint32_t m = __ballot_sync(0xffffffffu, gt);
+    const uint32_t first = m ? (uint32_t)(__ffs(m) - 1) : 32u;
+    if (first == 0) {
+      hi = lo;
+    } else {
+      const uint32_t lo_old = lo;
+      lo = lo_old + (first - 1) * step + 1;
+      hi = (uint32_t)min((uint64_t)hi, (uint64_t)lo_old + (uint64_t)first * step);
+    }
+  }
+  return lo;
+}
+
+template <typename K, bool PAIRS, int NT, int VM>
+__global__ void __launch_bounds__(NT)
+k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items, const uint32_t* __restrict__ count,
+             uint32_t pass, K* __restrict__ bufX, K* __restrict__ bufU, uint32_t* __restrict__ vX,
+             uint32_t* __restrict__ vU) {
+  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  constexpr int TM = NT * VM;
+  using BS = BlockSort<K, NT, VM>;  // padding helper only
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* sk = reinterpret_cast<K*>(smem_raw);                        // TM (+pad) keys: A part then B part
+  uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);  // TM vals (pairs)
+  __shared__ uint32_t split[2];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t total = *count;
+  for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const MTile mt = items[it];
+    const BucketRec rc = recs[mt.bucket];
+    const uint32_t R = rc.chunk << pass;
+    const bool src_is_U = ((rc.passes - pass) & 1) != 0;
+    const K* src = src_is_U ? bufU : bufX;
+    K* dst = src_is_U ? bufX : bufU;
+    const uint32_t* vsrc = src_is_U ? vU : vX;
+    uint32_t* vdst = src_is_U ? vX : vU;
+    const uint32_t a0 = 2 * mt.pair * R;
+    const uint32_t b0 = min(rc.size, a0 + R), b1 = min(rc.size, a0 + 2 * R);
+    GSeq<K> A{src + rc.out + a0, b0 - a0}, B{src + rc.out + b0, b1 - b0};
+    const uint32_t d0 = mt.tile * TM, d1 = min(d0 + TM, A.len + B.len);
+    if (w < 2) {
+      const uint32_t sp = warp_split<GSeq<K>, K>(A, B, w == 0 ? d0 : d1);
+      if (lane == 0) split[w] = sp;
+    }
+    __syncthreads();
+    const uint32_t sa0 = split[0], sa1 = split[1];
+    const uint32_t na = sa1 - sa0, nb = (d1 - sa1) - (d0 - sa0), sb0 = d0 - sa0;
+    for (uint32_t i = threadIdx.x; i < na + nb; i += NT) {
+      const bool fa = i < na;
+      const uint32_t gi = fa ? a0 + sa0 + i : b0 + sb0 + (i - na);
+      sk[BS::pad(i)] = src[rc.out + gi];
+      if (PAIRS) sv[i] = vsrc[rc.out + gi];
+    }
+    __syncthreads();
+    // merge stage[0,na) with stage[na,na+nb): thread t -> outputs [t*VM, t*VM+VM)
+    const uint32_t m = na + nb, dd = threadIdx.x * VM;
+    K r[VM];
+    uint32_t ri[VM];
+    if (dd < m) {
+      uint32_t lo = dd > nb ? dd - nb : 0, hi = min(dd, na);
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const bool le = sk[BS::pad(mid)] <= sk[BS::pad(na + dd - 1 - mid)];
+        lo = le ? mid + 1 : lo;
+        hi = le ? hi : mid;
+      }
+      uint32_t ja = lo, jb = na + dd - lo;
+      K a = ja < na ? sk[BS::pad(ja)] : KeyTraits<K>::kMax;
+      K b = jb < m ? sk[BS::pad(jb)] : KeyTraits<K>::kMax;
+#pragma unroll
+      for (int k = 0; k < VM; k++) {
+        // ties and exhausted runs: take A unless A is exhausted (stability for pairs)
+        const bool takeA = ja < na && (jb >= m || a <= b);
+        r[k] = takeA ? a : b;
+        ri[k] = takeA ? ja : jb;
+        const uint32_t jn = (takeA ? ja : jb) + 1;
+        const uint32_t end = takeA ? na : m;
+        K v = sk[BS::pad(jn)];
+        v = jn < end ? v : KeyTraits<K>::kMax;
+        a = takeA ? v : a;
+        b = takeA ? b : v;
+        ja = takeA ? jn : ja;
+        jb = takeA ? jb : jn;
+      }
+    }
+    uint32_t rv[VM];
+    if (PAIRS) {
+#pragma unroll
+      for (int k = 0; k < VM; k++) rv[k] = dd + k < m ? sv[ri[k]] : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < VM; k++)
+      if (dd + k < m) {
+        sk[BS::pad(dd + k)] = r[k];
+        if (PAIRS) sv[dd + k] = rv[k];
+      }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += NT) {
+      dst[rc.out + a0 + d0 + i] = sk[BS::pad(i)];
+      if (PAIRS) vdst[rc.out + a0 + d0 + i] = sv[i];
     }
     __syncthreads();
   }
@@ -1078,7 +1255,7 @@ k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__
   __shared__ uint32_t s_off[NT], s_len[NT], s_dst[NT], misc[64];
   const uint32_t total = list ? *count : all_k;
   for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
-    const BucketRec rc = recs[list ? list[it] : it];
+    const BucketRec rc = recs[list ? item_bucket(list[it]) : it];
     const TileInfo ti = tiles[rc.tile];
     gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, 0u, rc.size,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
@@ -1169,7 +1346,7 @@ k_clustersort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ t
   const uint32_t ncl = gridDim.x / CL, cid = blockIdx.x / CL;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (uint32_t it = cid; it < total; it += ncl) {
-    const BucketRec rc = recs[list[it]];
+    const BucketRec rc = recs[item_bucket(list[it])];
     const TileInfo ti = tiles[rc.tile];
     const uint32_t L = rc.size;
     const uint32_t chunk = (L + CL - 1) / CL;

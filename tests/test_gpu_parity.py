@@ -17,10 +17,10 @@ import paper_2407_14801_b200 as sq  # noqa: E402
 @pytest.fixture(autouse=True)
 def _reset_tile():
     sq.set_max_tile(0)
-    sq.set_cluster_sort(True)
+    sq.set_big_bucket_mode(sq.BIG_MERGE)
     yield
     sq.set_max_tile(0)
-    sq.set_cluster_sort(True)
+    sq.set_big_bucket_mode(sq.BIG_MERGE)
 
 
 def to_dev(a):
@@ -141,29 +141,29 @@ def test_sizes_u64(n):
     assert np.array_equal(gpu_sort(keys, 7), np.sort(keys))
 
 
-@pytest.mark.parametrize("cluster", [False, True])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("tile", [64, 256, 1024])
 @pytest.mark.parametrize("n", [5000, 70001, 300000])
-def test_forced_multilevel_vs_oracle(tile, n, cluster):
-    # a small on-chip tile forces cluster sorts (buckets up to 16 tiles) and, past
-    # them or with clusters off, SquareSort levels inside columns and buckets
+def test_forced_multilevel_vs_oracle(tile, n, mode):
+    # a small on-chip tile forces the big-bucket path (merge sort or clusters, up
+    # to 16 tiles) and, past it or in mode 0, SquareSort levels in columns and buckets
     sq.set_max_tile(tile)
-    sq.set_cluster_sort(cluster)
+    sq.set_big_bucket_mode(mode)
     rng = np.random.default_rng(tile * 7 + n)
     for card in (2**32, 1000, 3):
         keys = rng.integers(0, card, n, dtype=np.uint64).astype(np.uint32)
         want, _ = oracle_sort(keys, 11)
         got = gpu_sort(keys, 11)
         assert np.array_equal(got, want), card
-        if card == 2**32 and n >= 16 * tile and not cluster:
+        if card == 2**32 and n >= 16 * tile and mode == 0:
             assert sq.get_stats()["levels"] >= 2
 
 
-@pytest.mark.parametrize("cluster", [False, True])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("tile", [64, 512])
-def test_forced_multilevel_pairs_and_u64(tile, cluster):
+def test_forced_multilevel_pairs_and_u64(tile, mode):
     sq.set_max_tile(tile)
-    sq.set_cluster_sort(cluster)
+    sq.set_big_bucket_mode(mode)
     rng = np.random.default_rng(tile)
     n = 50000
     k = rng.integers(0, 50, n, dtype=np.uint64).astype(np.uint32)
@@ -195,6 +195,18 @@ def test_pairs_stability_with_duplicates():
         gk, gv = gpu_sort(k, 9, v)
         ek, ev = CF.stable_pairs_sort(k, v)
         assert np.array_equal(gk, ek) and np.array_equal(gv, ev)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_big_bucket_modes_full_tile(mode):
+    # default tiles, 2^24 keys: buckets of ~4K with a tail beyond 16K exercise each mode
+    sq.set_big_bucket_mode(mode)
+    keys, _ = S.config("cfg5", n=1 << 24)
+    assert np.array_equal(gpu_sort(keys, 5), np.sort(keys))
+    k, v = S.config("cfg5p", n=1 << 23)
+    gk, gv = gpu_sort(k, 5, v)
+    assert np.array_equal(gk, np.arange(len(k), dtype=np.uint32))
+    assert np.array_equal(gk[gv], np.arange(len(k), dtype=np.uint32)[gv]) and np.array_equal(k[gv], gk)
 
 
 def test_seed_invariance():
