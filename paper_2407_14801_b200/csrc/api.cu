@@ -205,7 +205,7 @@ struct Arena {
 // ------------------------------------------------------------------ size classes
 // On-chip tiles (threads x keys per thread) for 32-bit sort keys and for
 // 64-bit sort keys (u64 keys, pair composites).
-static const uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768};
+static const uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 12288, 16384, 32768};
 
 template <typename SK> constexpr uint32_t key_max_tile() { return sizeof(SK) == 4 ? 32768u : 16384u; }
 
@@ -233,8 +233,11 @@ static void with_tile(uint32_t tile, F&& f) {
       case 512: return f(IC<64>{}, IC<8>{});
       case 1024: return f(IC<128>{}, IC<8>{});
       case 2048: return f(IC<128>{}, IC<16>{});
+      case 3072: return f(IC<96>{}, IC<32>{});
       case 4096: return f(IC<256>{}, IC<16>{});
+      case 6144: return f(IC<192>{}, IC<32>{});
       case 8192: return f(IC<512>{}, IC<16>{});
+      case 12288: return f(IC<384>{}, IC<32>{});
       case 16384: return f(IC<512>{}, IC<32>{});
       case 32768: return f(IC<1024>{}, IC<32>{});
     }
@@ -246,8 +249,11 @@ static void with_tile(uint32_t tile, F&& f) {
       case 512: return f(IC<64>{}, IC<8>{});
       case 1024: return f(IC<128>{}, IC<8>{});
       case 2048: return f(IC<256>{}, IC<8>{});
+      case 3072: return f(IC<192>{}, IC<16>{});
       case 4096: return f(IC<256>{}, IC<16>{});
+      case 6144: return f(IC<384>{}, IC<16>{});
       case 8192: return f(IC<512>{}, IC<16>{});
+      case 12288: return f(IC<768>{}, IC<16>{});
       case 16384: return f(IC<1024>{}, IC<16>{});
     }
   }
@@ -612,7 +618,7 @@ struct Engine {
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};
     po.ncls = 0;
-    int cls_cl[12] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
+    int cls_cl[16] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
     {
       const uint32_t one = g_big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
       for (uint32_t t : kTiles)

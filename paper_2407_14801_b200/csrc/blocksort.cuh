@@ -91,12 +91,15 @@ struct BlockSort {
 #pragma unroll
       for (int j = 0; j < V; j++) s[pad(t * V + j)] = r[j];
       __syncthreads();
-      const uint32_t a0 = (t * V) & ~(2 * w - 1);  // run A = [a0, b0), run B = [b0, b0 + w)
-      const uint32_t b0 = a0 + w, bend = b0 + w;
+      // run A = [a0, b0), run B = [b0, bend) (TILE need not be a power of two: the
+      // last pair of a pass may be short or have no B run at all)
+      const uint32_t a0 = (t * V) & ~(2 * w - 1);
+      const uint32_t b0 = min(a0 + w, (uint32_t)TILE), bend = min(a0 + 2 * w, (uint32_t)TILE);
+      const uint32_t la = b0 - a0, lb = bend - b0;
       const uint32_t diag = t * V - a0;
       // merge path: smallest i with A[i] > B[diag-1-i] (ties taken from A first)
-      uint32_t lo = diag > w ? diag - w : 0;
-      uint32_t hi = diag < w ? diag : w;
+      uint32_t lo = diag > lb ? diag - lb : 0;
+      uint32_t hi = diag < la ? diag : la;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         const K x = s[pad(a0 + mid)];
@@ -118,7 +121,7 @@ struct BlockSort {
         r[k] = takeA ? a : b;
         const uint32_t jn = (takeA ? ja : jb) + 1;
         const uint32_t end = takeA ? b0 : bend;
-        K v = s[pad(jn)];
+        K v = s[pad(jn)];  // jn <= TILE: inside the buffer (SMEM_ELEMS > pad(TILE))
         v = jn < end ? v : KeyTraits<K>::kMax;
         a = takeA ? v : a;
         b = takeA ? b : v;

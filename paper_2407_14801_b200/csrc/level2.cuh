@@ -907,7 +907,7 @@ struct PlanOut {
   uint32_t* count;      // [ncls + 2] atomic counters; ncls = copy list, ncls+1 = oversize
   uint32_t cap_per_list;
   uint32_t ncls;
-  uint32_t cls_tile[12];  // class tile sizes (ascending)
+  uint32_t cls_tile[16];  // class tile sizes (ascending)
   uint32_t max_tile;      // largest bucket sorted by one CTA
   // merge-sort base case for max_tile < size <= msort_max: chunks of <= max_tile keys,
   // sorted by one CTA each, then up to kMaxPasses merge passes with tiles of mtile keys
@@ -986,7 +986,7 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t*
       uint32_t q = 1;  // chunks
       if (size && !single && size > po.max_tile && size <= po.msort_max) {
         q = (size + po.max_tile - 1) / po.max_tile;
-        rc.chunk = (size + q - 1) / q;
+        rc.chunk = po.max_tile;  // full chunks; the last one takes the remainder
         uint32_t np = 0;
         while ((1u << np) < q) np++;
         rc.passes = np;
@@ -1003,15 +1003,19 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t*
       }
       recs[gi] = rc;
       if (size) {
-        int cls;
-        if (single) cls = po.ncls;
-        else if (size > po.msort_max) cls = po.ncls + 1;
-        else {
-          cls = 0;
-          while (po.cls_tile[cls] < rc.chunk) cls++;
+        if (single || size > po.msort_max) {
+          const int cls = single ? po.ncls : po.ncls + 1;
+          const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+          po.list[uint64_t(cls) * po.cap_per_list + slot] = (uint32_t)gi * 16;
+        } else {
+          for (uint32_t k = 0; k < q; k++) {
+            const uint32_t len = min(rc.chunk, size - k * rc.chunk);
+            int cls = 0;
+            while (po.cls_tile[cls] < len) cls++;
+            const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+            po.list[uint64_t(cls) * po.cap_per_list + slot] = (uint32_t)gi * 16 + k;
+          }
         }
-        const uint32_t slot = atomicAdd(&po.count[cls], q);
-        for (uint32_t k = 0; k < q; k++) po.list[uint64_t(cls) * po.cap_per_list + slot + k] = (uint32_t)gi * 16 + k;
       }
     }
     __syncthreads();
