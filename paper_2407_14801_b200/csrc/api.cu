@@ -307,7 +307,7 @@ template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16,
 template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
-template <typename K> struct MergeCfg { static constexpr int NT = 512, VM = 16; };
+template <typename K> struct MergeCfg { static constexpr int NT = 256, VM = 16; };
 
 // Side streams for running the bucket-class kernels concurrently.
 struct SideStreams {
@@ -522,6 +522,10 @@ struct Engine {
     if (maxnp > key_max_tile<K>()) throw Error(SQ_ERR_INVALID_ARGUMENT, "pivot sample too large for one CTA");
     const uint32_t ntiles = (uint32_t)tiles.size();
 
+    std::vector<uint32_t> seg_of(buck_tot);
+    for (uint32_t s2 = 0; s2 < ns; s2++)
+      for (uint32_t b = 0; b < L[s2].k; b++) seg_of[L[s2].buck_base + b] = s2;
+    uint32_t* dSegOf = ar.upload(seg_of);
     LevelSeg* dL = ar.upload(L);
     TileInfo* dTiles = ar.upload(tiles);
     uint32_t* dTileBase = ar.upload(tile_base);
@@ -661,7 +665,11 @@ struct Engine {
       uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
       k_bucket_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, ppre, bsize);
       check_launch("k_bucket_sizes");
-      k_bucket_plan<K><<<ns, 1024, 0, st>>>(dL, dTileBase, bsize, piv, recs, po);
+      uint32_t* boff = (uint32_t*)ar.alloc(buck_tot * 4);
+      k_bucket_offsets<<<ns, 1024, 0, st>>>(dL, bsize, boff);
+      check_launch("k_bucket_offsets");
+      k_bucket_plan<K><<<(uint32_t)((buck_tot + 255) / 256), 256, 0, st>>>(dL, ns, dSegOf, dTileBase, bsize, boff, piv,
+                                                                         recs, (uint32_t)buck_tot, po);
       check_launch("k_bucket_plan");
     }
     if (dbg) {

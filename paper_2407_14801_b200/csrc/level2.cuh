@@ -940,17 +940,15 @@ __global__ void k_bucket_sizes(const LevelSeg* __restrict__ segs, const TileInfo
   }
 }
 
-template <typename K>
-__global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
-                              const uint32_t* __restrict__ bsize, const K* __restrict__ piv,
-                              BucketRec* __restrict__ recs, PlanOut po) {
+// Bucket final offsets: exclusive scan of the sizes per segment (one CTA per
+// segment, P:283 / P:461).
+__global__ void k_bucket_offsets(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ bsize,
+                                 uint32_t* __restrict__ boff) {
   const LevelSeg sg = segs[blockIdx.x];
-  const uint32_t t0 = tile_base[blockIdx.x];
   __shared__ uint32_t carry;
   __shared__ uint32_t ws[32];
   if (threadIdx.x == 0) carry = sg.off;
   __syncthreads();
-  const K* P = piv + sg.piv_base;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (uint32_t c0 = 0; c0 < sg.k; c0 += blockDim.x) {
     const uint32_t b = c0 + threadIdx.x;
@@ -972,55 +970,70 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, const uint32_t*
     }
     __syncthreads();
     const uint32_t excl = carry + x - size + (w ? ws[w - 1] : 0);
-    if (b < sg.k) {
-      const uint64_t gi = uint64_t(sg.buck_base) + b;
-      BucketRec rc;
-      rc.tile = t0 + b / kTB;
-      rc.lane = b % kTB;
-      rc.out = excl;
-      rc.size = size;
-      rc.node = child_key(sg.node, 1, b);
-      rc.chunk = size;
-      rc.passes = 0;
-      const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
-      uint32_t q = 1;  // chunks
-      if (size && !single && size > po.max_tile && size <= po.msort_max) {
-        q = (size + po.max_tile - 1) / po.max_tile;
-        rc.chunk = po.max_tile;  // full chunks; the last one takes the remainder
-        uint32_t np = 0;
-        while ((1u << np) < q) np++;
-        rc.passes = np;
-        for (uint32_t p = 0; p < np; p++) {  // merge tiles of every pass
-          const uint32_t R = rc.chunk << p;
-          for (uint32_t j = 0; 2 * j * R < size; j++) {
-            const uint32_t plen = min(size, (2 * j + 2) * R) - 2 * j * R;
-            for (uint32_t t = 0; t * po.mtile < plen; t++) {
-              const uint32_t slot = atomicAdd(&po.mcount[p], 1u);
-              po.mlist[uint64_t(p) * po.mcap + slot] = MTile{(uint32_t)gi, (uint16_t)j, (uint16_t)t};
-            }
-          }
-        }
-      }
-      recs[gi] = rc;
-      if (size) {
-        if (single || size > po.msort_max) {
-          const int cls = single ? po.ncls : po.ncls + 1;
-          const uint32_t slot = atomicAdd(&po.count[cls], 1u);
-          po.list[uint64_t(cls) * po.cap_per_list + slot] = (uint32_t)gi * 16;
-        } else {
-          for (uint32_t k = 0; k < q; k++) {
-            const uint32_t len = min(rc.chunk, size - k * rc.chunk);
-            int cls = 0;
-            while (po.cls_tile[cls] < len) cls++;
-            const uint32_t slot = atomicAdd(&po.count[cls], 1u);
-            po.list[uint64_t(cls) * po.cap_per_list + slot] = (uint32_t)gi * 16 + k;
-          }
-        }
-      }
-    }
+    if (b < sg.k) boff[sg.buck_base + b] = excl;
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = excl + size;
     __syncthreads();
+  }
+}
+
+// Bucket records and work lists (one thread per bucket, all segments in one
+// grid): single-value buckets (copy), on-chip classes, merge-sorted
+// chunks and their merge tiles, oversize (next level).
+template <typename K>
+__global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ seg_of,
+                              const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ bsize,
+                              const uint32_t* __restrict__ boff, const K* __restrict__ piv,
+                              BucketRec* __restrict__ recs, uint32_t nbuck, PlanOut po) {
+  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= nbuck) return;
+  const uint32_t sidx = seg_of[gi];
+  const LevelSeg sg = segs[sidx];
+  const uint32_t b = gi - sg.buck_base;
+  const uint32_t size = bsize[gi];
+  const K* P = piv + sg.piv_base;
+  BucketRec rc;
+  rc.tile = tile_base[sidx] + b / kTB;
+  rc.lane = b % kTB;
+  rc.out = boff[gi];
+  rc.size = size;
+  rc.node = child_key(sg.node, 1, b);
+  rc.chunk = size;
+  rc.passes = 0;
+  const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
+  uint32_t q = 1;  // chunks
+  if (size && !single && size > po.max_tile && size <= po.msort_max) {
+    q = (size + po.max_tile - 1) / po.max_tile;
+    rc.chunk = po.max_tile;  // full chunks; the last one takes the remainder
+    uint32_t np = 0;
+    while ((1u << np) < q) np++;
+    rc.passes = np;
+    for (uint32_t p = 0; p < np; p++) {  // merge tiles of every pass
+      const uint32_t R = rc.chunk << p;
+      uint32_t ntile = 0;
+      for (uint32_t j = 0; 2 * j * R < size; j++) ntile += (min(size, (2 * j + 2) * R) - 2 * j * R + po.mtile - 1) / po.mtile;
+      uint32_t slot = atomicAdd(&po.mcount[p], ntile);
+      for (uint32_t j = 0; 2 * j * R < size; j++) {
+        const uint32_t plen = min(size, (2 * j + 2) * R) - 2 * j * R;
+        for (uint32_t t = 0; t * po.mtile < plen; t++)
+          po.mlist[uint64_t(p) * po.mcap + slot++] = MTile{gi, (uint16_t)j, (uint16_t)t};
+      }
+    }
+  }
+  recs[gi] = rc;
+  if (!size) return;
+  if (single || size > po.msort_max) {
+    const int cls = single ? po.ncls : po.ncls + 1;
+    const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+    po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16;
+  } else {
+    for (uint32_t k = 0; k < q; k++) {
+      const uint32_t len = min(rc.chunk, size - k * rc.chunk);
+      int cls = 0;
+      while (po.cls_tile[cls] < len) cls++;
+      const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+      po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16 + k;
+    }
   }
 }
 
@@ -1095,8 +1108,9 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
-                            s[BS::pad(d + q)] = (uint64_t(src[o + q]) << 32) | (d + q);
-                            vs[d + q] = vsrc[o + q];
+                            // key into the low half of the composite slot, fixed up below
+                            cp_async_elem(reinterpret_cast<uint32_t*>(&s[BS::pad(d + q)]), &src[o + q]);
+                            cp_async_elem(&vs[d + q], &vsrc[o + q]);
                           } else {
                             cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
                           }
@@ -1104,6 +1118,13 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
                       });
     cp_async_wait_all();
     __syncthreads();
+    if constexpr (PAIRS) {  // composite = key << 32 | position (stable order)
+      for (int i = threadIdx.x; i < (int)len; i += NT) {
+        const uint32_t key = *reinterpret_cast<uint32_t*>(&s[BS::pad(i)]);
+        s[BS::pad(i)] = (uint64_t(key) << 32) | uint32_t(i);
+      }
+      __syncthreads();
+    }
     BS::sort_smem(s);
     for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
@@ -1189,12 +1210,13 @@ k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items
     __syncthreads();
     const uint32_t sa0 = split[0], sa1 = split[1];
     const uint32_t na = sa1 - sa0, nb = (d1 - sa1) - (d0 - sa0), sb0 = d0 - sa0;
-    for (uint32_t i = threadIdx.x; i < na + nb; i += NT) {
+    for (uint32_t i = threadIdx.x; i < na + nb; i += NT) {  // all loads in flight at once
       const bool fa = i < na;
       const uint32_t gi = fa ? a0 + sa0 + i : b0 + sb0 + (i - na);
-      sk[BS::pad(i)] = src[rc.out + gi];
-      if (PAIRS) sv[i] = vsrc[rc.out + gi];
+      cp_async_elem(&sk[BS::pad(i)], &src[rc.out + gi]);
+      if (PAIRS) cp_async_elem(&sv[i], &vsrc[rc.out + gi]);
     }
+    cp_async_wait_all();
     __syncthreads();
     // merge stage[0,na) with stage[na,na+nb): thread t -> outputs [t*VM, t*VM+VM)
     const uint32_t m = na + nb, dd = threadIdx.x * VM;
