@@ -471,7 +471,7 @@ struct Engine {
   // bucket sorts gather from T and write the sorted buckets back into X.
   void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
     using TC = PmTr<K, PAIRS>;
-    using CF = TmaCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
+    using CF = MsCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
     ensure_scratch();
     g_stats.levels++;
     const int T = 1 - X;
@@ -611,13 +611,13 @@ struct Engine {
       check_launch("k_tile_scan");
     }
     {
-      auto f = k_transpose_tma<K, PAIRS, TC::NT, TC::S, TC::F>;
+      auto f = k_transpose_ms<K, PAIRS, TC::NT, TC::S, TC::F>;
       static bool init = false;
       if (!init) { set_smem(f, CF::SMEM); init = true; }
       ProfScope ps("transpose", st);
       f<<<ntiles, TC::NT, CF::SMEM, st>>>(dL, dTiles, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr,
                                           piv, segmat, pout, ppre);
-      check_launch("k_transpose_tma");
+      check_launch("k_transpose_ms");
     }
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};

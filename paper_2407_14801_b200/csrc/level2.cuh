@@ -899,6 +899,290 @@ k_transpose_tma(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
 }
 
 // ------------------------------------------------------------------------------
+// SkewTranspose, piece-major, TMA-staged, multisplit ranking (the sort path's
+// transpose).  Same contract and piece/window logic as k_transpose_tma; per piece:
+//  * bulk copies of the run fragments into aligned slots, then a warp-per-fragment
+//    compaction into stream order (the tile's column-major order);
+//  * pass 1, warp w over a contiguous range of the stream, 32 keys at a time:
+//    bucket by a branch-free 5-step search over the tile's thresholds, and a
+//    stable rank among the warp's keys of that bucket from 5 ballots (lane j also
+//    gets the count of bucket j) -- no dependence on fragment boundaries;
+//  * a block scan over (warp, bucket) gives the image offsets; pass 2 places every
+//    key; the image is written with one bulk store.
+template <typename K, bool PAIRS, int NT, int S, int F>
+struct MsCfg {
+  static constexpr int NW = NT / 32;
+  static constexpr int SLK = 48 / (int)sizeof(K);
+  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t SLOT = al((S + SLK * F + 16) * sizeof(K));
+  static constexpr size_t VSLOT = PAIRS ? al((S + 12 * F + 16) * 4) : 0;
+  static constexpr size_t off_slot = 0;
+  static constexpr size_t off_vslot = off_slot + SLOT;
+  static constexpr size_t off_stage = off_vslot + VSLOT;                 // S keys, stream order
+  static constexpr size_t off_vstage = off_stage + al(S * sizeof(K));
+  static constexpr size_t off_code = off_vstage + (PAIRS ? al(S * 4) : 0);  // S u32
+  static constexpr size_t off_out = off_code + al(S * 4);
+  static constexpr size_t off_vout = off_out + al((S + 16 / sizeof(K) + 4) * sizeof(K));
+  static constexpr size_t off_frag = off_vout + (PAIRS ? al((S + 8) * 4) : 0);  // fstart[F+1], fsrc[F], fe[F], fve[F]
+  static constexpr size_t off_wsum = al(off_frag + (4 * F + 1) * 4);
+  static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);
+  static constexpr size_t off_thr = al(off_misc + (64 + 33) * 4);      // 32 thresholds (u64 / pairs of u64)
+  static constexpr size_t off_bar = al(off_thr + 32 * 16);
+  static constexpr size_t SMEM = off_bar + 16;
+};
+
+// "x lies in a bucket after boundary j" for the tile's thresholds, branch-free.
+// u32 keys: threshold t = p + dup as u64 (x >= t).  u64 keys: (p, dup) pair.
+template <typename K> struct Thr;
+template <> struct Thr<uint32_t> {
+  uint64_t t;
+  __device__ __forceinline__ static Thr make(uint32_t p, bool dup, bool inf) {
+    return Thr{inf ? ~0ull : uint64_t(p) + (dup ? 1u : 0u)};
+  }
+  __device__ __forceinline__ bool passed(uint32_t x) const { return uint64_t(x) >= t; }
+};
+template <> struct Thr<uint64_t> {
+  uint64_t p, dup;  // dup = 2: never passed (sentinel)
+  __device__ __forceinline__ static Thr make(uint64_t p, bool dup, bool inf) { return Thr{p, inf ? 2ull : (dup ? 1ull : 0ull)}; }
+  __device__ __forceinline__ bool passed(uint64_t x) const { return dup != 2 && (x > p || (x == p && dup == 0)); }
+};
+
+template <typename K, bool PAIRS, int NT, int S, int F>
+__global__ void __launch_bounds__(NT)
+k_transpose_ms(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const K* __restrict__ src,
+               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint32_t* __restrict__ pout,
+               uint16_t* __restrict__ ppre) {
+  using C = MsCfg<K, PAIRS, NT, S, F>;
+  static_assert(F <= NT && F % 32 == 0 && S <= 65535 && S % (32 * (NT / 32)) == 0, "shape");
+  constexpr int EB = sizeof(K);
+  extern __shared__ __align__(128) unsigned char sm[];
+  K* slot = reinterpret_cast<K*>(sm + C::off_slot);
+  uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot);
+  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
+  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
+  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);
+  unsigned char* outraw = sm + C::off_out;
+  unsigned char* voutraw = sm + C::off_vout;
+  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
+  uint32_t* fsrc = fstart + F + 1;
+  uint32_t* fe = fsrc + F;
+  uint32_t* fve = fe + F;
+  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
+  uint32_t* poff = misc + 64;
+  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::off_bar);
+
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const TileInfo ti = tiles[blockIdx.x];
+  const LevelSeg sg = segs[ti.seg];
+  const uint32_t bt = ti.bt;
+  const uint32_t b0 = bt * kTB;
+  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
+  const K* P = piv + sg.piv_base;
+  if (t < 32) {  // threshold j ends bucket j of the tile (j < nb-1); the rest never pass
+    const uint32_t j = b0 + 1 + t;
+    const bool real = t < (int)nb - 1;
+    const K pj = real ? P[j - 1] : K(0);
+    const bool dup = real && j >= 2 && P[j - 2] == pj;
+    thr[t] = Thr<K>::make(pj, dup, !real);
+  }
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  uint32_t oc = ti.out, npc = 0;
+  uint32_t c = 0, o = 0;
+  const uint32_t* rows = segmat + sg.segmat_base;
+  const uint32_t rstride = sg.nbt + 1;
+  constexpr uint32_t PER_W = S / (NT / 32);  // stream keys per warp
+
+  while (c < sg.ncols) {
+    // ---- window of F runs; the piece takes up to S keys (same rule as k_transpose_tma)
+    uint32_t len = 0, srcpos = 0;
+    if (t < F && c + t < sg.ncols) {
+      const uint32_t* row = rows + uint64_t(c + t) * rstride;
+      const uint32_t a = row[bt], e = row[bt + 1];
+      const uint32_t skip = t == 0 ? o : 0;
+      len = e - a - skip;
+      srcpos = sg.off + (c + t) * sg.rows + a + skip;
+    }
+    uint32_t wtot;
+    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
+    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
+    const int inpiece = (t < (int)nwin && ex < (uint32_t)S) ? 1 : 0;
+    const uint32_t nf = __syncthreads_count(inpiece);
+    const uint32_t Pn = min((uint32_t)S, wtot);
+    if (t < (int)nf) {
+      const uint32_t flen = min(ex + len, Pn) - ex;
+      fstart[t] = ex;
+      fsrc[t] = srcpos;
+      const uintptr_t ga = reinterpret_cast<uintptr_t>(src + srcpos);
+      const uint32_t mis = (uint32_t)(ga & 15);
+      const uint32_t so = (uint32_t)C::al((ex + C::SLK * t) * EB);
+      fe[t] = (so + mis) / EB;
+      if (flen) {
+        const uint32_t bytes = (mis + flen * EB + 15) & ~15u;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(reinterpret_cast<unsigned char*>(slot) + so, reinterpret_cast<const void*>(ga - mis), bytes, bar);
+      }
+      if (PAIRS) {
+        const uintptr_t va = reinterpret_cast<uintptr_t>(vsrc + srcpos);
+        const uint32_t vmis = (uint32_t)(va & 15);
+        const uint32_t vso = (uint32_t)C::al((ex + 12 * t) * 4);
+        fve[t] = (vso + vmis) / 4;
+        if (flen) {
+          const uint32_t vbytes = (vmis + flen * 4 + 15) & ~15u;
+          mbar_expect_tx(bar, vbytes);
+          bulk_g2s(reinterpret_cast<unsigned char*>(vslot) + vso, reinterpret_cast<const void*>(va - vmis), vbytes,
+                   bar);
+        }
+      }
+    }
+    if (t == 0) fstart[nf] = Pn;
+    uint32_t nc, no;
+    if (wtot <= (uint32_t)S) {
+      nc = c + nwin;
+      no = 0;
+    } else {
+      __syncthreads();
+      const uint32_t last = nf - 1;
+      const uint32_t used = Pn - fstart[last];
+      const uint32_t* row = rows + uint64_t(c + last) * rstride;
+      const uint32_t base = last == 0 ? o : 0;
+      const uint32_t full = row[bt + 1] - row[bt] - base;
+      if (used < full) {
+        nc = c + last;
+        no = base + used;
+      } else {
+        nc = c + last + 1;
+        no = 0;
+      }
+    }
+    __syncthreads();
+    if (Pn > 0) {
+      if (t == 0) mbar_arrive(bar);
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      // ---- compaction into stream order (one warp per fragment)
+      for (uint32_t f = w; f < nf; f += C::NW) {
+        const uint32_t fs = fstart[f], fl = fstart[f + 1] - fs;
+        const K* fk = slot + fe[f];
+        for (uint32_t i = lane; i < fl; i += 32) {
+          stage[fs + i] = fk[i];
+          if (PAIRS) vstage[fs + i] = vslot[fve[f] + i];
+        }
+      }
+      __syncthreads();
+      // ---- pass 1: stable multisplit ranks within each warp's contiguous range
+      uint32_t run = 0;  // lane j: keys of bucket j seen by this warp
+      const uint32_t q0 = w * PER_W, q1 = min(Pn, q0 + PER_W);
+      for (uint32_t qb = q0; qb < q1; qb += 32) {
+        const uint32_t q = qb + lane;
+        const bool valid = q < q1;
+        const K x = valid ? stage[q] : K(0);
+        uint32_t b = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+          if (thr[b + st - 1].passed(x)) b += st;
+        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+        uint32_t peers = vm, mine = vm;  // keys with my bucket / with bucket == lane
+#pragma unroll
+        for (int k = 0; k < 5; k++) {
+          const uint32_t bk = __ballot_sync(0xffffffffu, (b >> k) & 1);
+          peers &= ((b >> k) & 1) ? bk : ~bk;
+          mine &= ((lane >> k) & 1) ? bk : ~bk;
+        }
+        const uint32_t rk = __shfl_sync(0xffffffffu, run, b) + __popc(peers & ((1u << lane) - 1));
+        if (valid) code[q] = b | (rk << 5);
+        run += __popc(mine);
+      }
+      wsum[w * 32 + lane] = run;
+      __syncthreads();
+      if (w == 0) {
+        uint32_t tot = 0;
+        for (int ww = 0; ww < C::NW; ww++) {
+          const uint32_t v = wsum[ww * 32 + lane];
+          wsum[ww * 32 + lane] = tot;
+          tot += v;
+        }
+        const uint32_t v = lane < (int)nb ? tot : 0;
+        uint32_t xs = v;
+        for (int q = 1; q < 32; q <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
+          if (lane >= q) xs += y;
+        }
+        poff[lane] = xs - v;
+        if (lane == 31) poff[kTB] = xs;
+        for (int ww = 0; ww < C::NW; ww++) wsum[ww * 32 + lane] += xs - v;
+      }
+      __syncthreads();
+      // ---- pass 2: place every key in the piece image (shifted for the bulk store)
+      const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
+      K* outb = reinterpret_cast<K*>(outraw) + oshift;
+      const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
+      uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
+      const uint32_t* wbase = wsum + w * 32;
+      for (uint32_t q = q0 + lane; q < q1; q += 32) {
+        const uint32_t cd = code[q];
+        const uint32_t dpos = wbase[cd & 31] + (cd >> 5);
+        outb[dpos] = stage[q];
+        if (PAIRS) vout[dpos] = vstage[q];
+      }
+      fence_proxy_async();
+      __syncthreads();
+      {
+        const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
+        const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
+        const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
+        if (a1 > a0) {
+          if (t == 0)
+            bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
+                     (uint32_t)(a1 - a0));
+          const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
+          if (t < (int)nh) dst[oc + t] = outb[t];
+          if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
+        } else {
+          for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
+        }
+        if (PAIRS) {
+          const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
+          const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
+          const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
+          if (c1 > c0) {
+            if (t == 0)
+              bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
+                       (uint32_t)(c1 - c0));
+            const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
+            if (t < (int)nh) vdst[oc + t] = vout[t];
+            if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
+          } else {
+            for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
+          }
+        }
+        if (t == 0) bulk_commit();
+      }
+      const uint32_t pe = ti.piece_base + npc;
+      if (t == 0) pout[pe] = oc;
+      if (t <= kTB) ppre[uint64_t(pe) * kPP + t] = (uint16_t)poff[t];
+      oc += Pn;
+      npc++;
+      if (t == 0) bulk_wait_read0();
+    }
+    c = nc;
+    o = no;
+    __syncthreads();
+  }
+  if (t == 0) {
+    tiles[blockIdx.x].npieces = npc;
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------
 // Bucket planning, per segment (one CTA): bucket sizes from the piece tables,
 // final offsets (exclusive scan, P:283 / P:461), RNG node keys, and the work
 // lists: single-value buckets (copy), on-chip classes, oversize.
