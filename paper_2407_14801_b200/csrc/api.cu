@@ -611,13 +611,25 @@ struct Engine {
       check_launch("k_tile_scan");
     }
     {
-      auto f = k_transpose_ms<K, PAIRS, TC::NT, TC::S, TC::F>;
-      static bool init = false;
-      if (!init) { set_smem(f, CF::SMEM); init = true; }
+      PieceDesc* pieces = (PieceDesc*)ar.alloc(piece_tot * sizeof(PieceDesc));
+      SQ_CUDA(cudaMemsetAsync(pieces, 0, piece_tot * sizeof(PieceDesc), st));
+      {
+        ProfScope ps("tiles", st);
+        k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pout);
+        check_launch("k_piece_plan");
+      }
+      auto f = k_transpose_pc<K, PAIRS, TC::NT, TC::S, TC::F>;
+      static int grid = 0;
+      if (!grid) {
+        set_smem(f, CF::SMEM);
+        grid = wave_grid(f, TC::NT, CF::SMEM);
+      }
       ProfScope ps("transpose", st);
-      f<<<ntiles, TC::NT, CF::SMEM, st>>>(dL, dTiles, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr,
-                                          piv, segmat, pout, ppre);
-      check_launch("k_transpose_ms");
+      f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), TC::NT, CF::SMEM, st>>>(
+          dL, dTiles, pieces, (uint32_t)piece_tot, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv,
+          segmat, ppre);
+      check_launch("k_transpose_pc");
+      ar.release(pieces);
     }
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};

@@ -921,10 +921,11 @@ struct MsCfg {
   static constexpr size_t off_stage = off_vslot + VSLOT;                 // S keys, stream order
   static constexpr size_t off_vstage = off_stage + al(S * sizeof(K));
   static constexpr size_t off_code = off_vstage + (PAIRS ? al(S * 4) : 0);  // S u32
-  static constexpr size_t off_out = off_code + al(S * 4);
+  static constexpr size_t off_out = off_code + al(S * 4);  // the piece image (read by the bulk store)
   static constexpr size_t off_vout = off_out + al((S + 16 / sizeof(K) + 4) * sizeof(K));
   static constexpr size_t off_frag = off_vout + (PAIRS ? al((S + 8) * 4) : 0);  // fstart[F+1], fsrc[F], fe[F], fve[F]
-  static constexpr size_t off_wsum = al(off_frag + (4 * F + 1) * 4);
+  static constexpr size_t off_wcnt = al(off_frag + (4 * F + 1) * 4);  // NW x 32 u32 running bucket counts
+  static constexpr size_t off_wsum = al(off_wcnt + NW * 32 * 4);
   static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);
   static constexpr size_t off_thr = al(off_misc + (64 + 33) * 4);      // 32 thresholds (u64 / pairs of u64)
   static constexpr size_t off_bar = al(off_thr + 32 * 16);
@@ -968,6 +969,7 @@ k_transpose_ms(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, 
   uint32_t* fsrc = fstart + F + 1;
   uint32_t* fe = fsrc + F;
   uint32_t* fve = fe + F;
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(sm + C::off_wcnt);
   uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
   uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
   uint32_t* poff = misc + 64;
@@ -1078,8 +1080,11 @@ k_transpose_ms(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, 
       }
       __syncthreads();
       // ---- pass 1: stable multisplit ranks within each warp's contiguous range
-      uint32_t run = 0;  // lane j: keys of bucket j seen by this warp
+      uint32_t* wc = wcnt + w * 32;  // this warp's running count per bucket
+      wc[lane] = 0;
+      __syncwarp();
       const uint32_t q0 = w * PER_W, q1 = min(Pn, q0 + PER_W);
+      const uint32_t lt = (1u << lane) - 1;
       for (uint32_t qb = q0; qb < q1; qb += 32) {
         const uint32_t q = qb + lane;
         const bool valid = q < q1;
@@ -1088,19 +1093,17 @@ k_transpose_ms(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, 
 #pragma unroll
         for (int st = 16; st >= 1; st >>= 1)
           if (thr[b + st - 1].passed(x)) b += st;
-        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-        uint32_t peers = vm, mine = vm;  // keys with my bucket / with bucket == lane
-#pragma unroll
-        for (int k = 0; k < 5; k++) {
-          const uint32_t bk = __ballot_sync(0xffffffffu, (b >> k) & 1);
-          peers &= ((b >> k) & 1) ? bk : ~bk;
-          mine &= ((lane >> k) & 1) ? bk : ~bk;
-        }
-        const uint32_t rk = __shfl_sync(0xffffffffu, run, b) + __popc(peers & ((1u << lane) - 1));
+        b = valid ? b : 32u + lane;  // invalid lanes match nobody
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const uint32_t before = __popc(peers & lt);
+        uint32_t rk = 0;
+        if (valid) rk = wc[b] + before;
+        __syncwarp();
+        if (valid && before == 0) wc[b] += __popc(peers);  // one leader per bucket
+        __syncwarp();
         if (valid) code[q] = b | (rk << 5);
-        run += __popc(mine);
       }
-      wsum[w * 32 + lane] = run;
+      wsum[w * 32 + lane] = wc[lane];
       __syncthreads();
       if (w == 0) {
         uint32_t tot = 0;
@@ -1180,6 +1183,277 @@ k_transpose_ms(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, 
     tiles[blockIdx.x].npieces = npc;
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   }
+}
+
+// ------------------------------------------------------------------------------
+// Piece plan: the piece boundaries of every bucket tile depend only on the run
+// lengths (segmat), so a light pre-pass (one CTA per tile) computes them with the
+// same window rule as k_transpose_ms (up to S keys from up to F runs), and the
+// transpose then processes pieces as independent work items (no serial chain per
+// tile, no wave tail).
+struct PieceDesc {
+  uint32_t tile, col, off, nf, pn, out;  // pn == 0: unused slot
+};
+
+template <int NT, int S, int F>
+__global__ void __launch_bounds__(NT)
+k_piece_plan(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const uint32_t* __restrict__ segmat,
+             PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pout) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t misc[64];
+  __shared__ uint32_t fst[F + 1];
+  const int t = threadIdx.x;
+  const TileInfo ti = tiles[blockIdx.x];
+  const LevelSeg sg = segs[ti.seg];
+  const uint32_t bt = ti.bt;
+  const uint32_t* rows = segmat + sg.segmat_base;
+  const uint32_t rstride = sg.nbt + 1;
+  uint32_t c = 0, o = 0, oc = ti.out, npc = 0;
+  while (c < sg.ncols) {
+    uint32_t len = 0;
+    if (t < F && c + t < sg.ncols) {
+      const uint32_t* row = rows + uint64_t(c + t) * rstride;
+      len = row[bt + 1] - row[bt] - (t == 0 ? o : 0);
+    }
+    uint32_t wtot;
+    const uint32_t ex = block_excl_sum<NW>(len, misc, &wtot);
+    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
+    const uint32_t nf = __syncthreads_count(t < (int)nwin && ex < (uint32_t)S);
+    const uint32_t Pn = min((uint32_t)S, wtot);
+    if (t < F) fst[t] = ex;
+    __syncthreads();
+    uint32_t nc, no;
+    if (wtot <= (uint32_t)S) {
+      nc = c + nwin;
+      no = 0;
+    } else {
+      const uint32_t last = nf - 1;
+      const uint32_t used = Pn - fst[last];
+      const uint32_t* row = rows + uint64_t(c + last) * rstride;
+      const uint32_t base = last == 0 ? o : 0;
+      const uint32_t full = row[bt + 1] - row[bt] - base;
+      if (used < full) {
+        nc = c + last;
+        no = base + used;
+      } else {
+        nc = c + last + 1;
+        no = 0;
+      }
+    }
+    if (Pn > 0) {
+      if (t == 0) {
+        const uint32_t pe = ti.piece_base + npc;
+        pieces[pe] = PieceDesc{blockIdx.x, c, o, nf, Pn, oc};
+        pout[pe] = oc;
+      }
+      oc += Pn;
+      npc++;
+    }
+    c = nc;
+    o = no;
+    __syncthreads();
+  }
+  if (t == 0) tiles[blockIdx.x].npieces = npc;
+}
+
+// SkewTranspose of one piece per iteration (persistent grid over the piece slots);
+// per piece exactly the work of k_transpose_ms.
+template <typename K, bool PAIRS, int NT, int S, int F>
+__global__ void __launch_bounds__(NT)
+k_transpose_pc(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
+               const PieceDesc* __restrict__ pieces, uint32_t npslots, const K* __restrict__ src,
+               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
+  using C = MsCfg<K, PAIRS, NT, S, F>;
+  static_assert(F <= NT && F % 32 == 0 && S <= 65535 && S % (32 * (NT / 32)) == 0, "shape");
+  constexpr int EB = sizeof(K);
+  extern __shared__ __align__(128) unsigned char sm[];
+  K* slot = reinterpret_cast<K*>(sm + C::off_slot);
+  uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot);
+  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
+  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
+  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);
+  unsigned char* outraw = sm + C::off_out;
+  unsigned char* voutraw = sm + C::off_vout;
+  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
+  uint32_t* fsrc = fstart + F + 1;
+  uint32_t* fe = fsrc + F;
+  uint32_t* fve = fe + F;
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(sm + C::off_wcnt);
+  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
+  uint32_t* poff = misc + 64;
+  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::off_bar);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  constexpr uint32_t PER_W = S / (NT / 32);
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (uint32_t ps = blockIdx.x; ps < npslots; ps += gridDim.x) {
+    const PieceDesc pd = pieces[ps];
+    if (pd.pn == 0) continue;  // uniform across the CTA
+    const TileInfo ti = tiles[pd.tile];
+    const LevelSeg sg = segs[ti.seg];
+    const uint32_t bt = ti.bt;
+    const uint32_t b0 = bt * kTB;
+    const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
+    const uint32_t Pn = pd.pn, nf = pd.nf, oc = pd.out;
+    if (t < 32) {
+      const K* P = piv + sg.piv_base;
+      const uint32_t j = b0 + 1 + t;
+      const bool real = t < (int)nb - 1;
+      const K pj = real ? P[j - 1] : K(0);
+      const bool dup = real && j >= 2 && P[j - 2] == pj;
+      thr[t] = Thr<K>::make(pj, dup, !real);
+    }
+    // ---- fragments: runs of columns col .. col+nf-1 (the first starts at `off`)
+    uint32_t len = 0, srcpos = 0;
+    if (t < (int)nf) {
+      const uint32_t cc = pd.col + t;
+      const uint32_t* row = segmat + sg.segmat_base + uint64_t(cc) * (sg.nbt + 1);
+      const uint32_t a = row[bt] + (t == 0 ? pd.off : 0), e = row[bt + 1];
+      len = e - a;
+      srcpos = sg.off + cc * sg.rows + a;
+    }
+    uint32_t wtot;
+    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
+    if (t < (int)nf) {
+      const uint32_t flen = min(ex + len, Pn) - ex;
+      fstart[t] = ex;
+      const uintptr_t ga = reinterpret_cast<uintptr_t>(src + srcpos);
+      const uint32_t mis = (uint32_t)(ga & 15);
+      const uint32_t so = (uint32_t)C::al((ex + C::SLK * t) * EB);
+      fe[t] = (so + mis) / EB;
+      if (flen) {
+        const uint32_t bytes = (mis + flen * EB + 15) & ~15u;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(reinterpret_cast<unsigned char*>(slot) + so, reinterpret_cast<const void*>(ga - mis), bytes, bar);
+      }
+      if (PAIRS) {
+        const uintptr_t va = reinterpret_cast<uintptr_t>(vsrc + srcpos);
+        const uint32_t vmis = (uint32_t)(va & 15);
+        const uint32_t vso = (uint32_t)C::al((ex + 12 * t) * 4);
+        fve[t] = (vso + vmis) / 4;
+        if (flen) {
+          const uint32_t vbytes = (vmis + flen * 4 + 15) & ~15u;
+          mbar_expect_tx(bar, vbytes);
+          bulk_g2s(reinterpret_cast<unsigned char*>(vslot) + vso, reinterpret_cast<const void*>(va - vmis), vbytes,
+                   bar);
+        }
+      }
+    }
+    if (t == 0) fstart[nf] = Pn;
+    __syncthreads();
+    if (t == 0) mbar_arrive(bar);
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    // ---- compaction into stream order
+    for (uint32_t f = w; f < nf; f += C::NW) {
+      const uint32_t fs = fstart[f], fl = fstart[f + 1] - fs;
+      const K* fk = slot + fe[f];
+      for (uint32_t i = lane; i < fl; i += 32) {
+        stage[fs + i] = fk[i];
+        if (PAIRS) vstage[fs + i] = vslot[fve[f] + i];
+      }
+    }
+    __syncthreads();
+    // ---- pass 1: stable multisplit ranks (ballots) in each warp's contiguous range
+    uint32_t run = 0;
+    const uint32_t q0 = w * PER_W, q1 = min(Pn, q0 + PER_W);
+    for (uint32_t qb = q0; qb < q1; qb += 32) {
+      const uint32_t q = qb + lane;
+      const bool valid = q < q1;
+      const K x = valid ? stage[q] : K(0);
+      uint32_t b = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1)
+        if (thr[b + st - 1].passed(x)) b += st;
+      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+      uint32_t peers = vm, mine = vm;
+#pragma unroll
+      for (int k = 0; k < 5; k++) {
+        const uint32_t bk = __ballot_sync(0xffffffffu, (b >> k) & 1);
+        peers &= ((b >> k) & 1) ? bk : ~bk;
+        mine &= ((lane >> k) & 1) ? bk : ~bk;
+      }
+      const uint32_t rk = __shfl_sync(0xffffffffu, run, b) + __popc(peers & ((1u << lane) - 1));
+      if (valid) code[q] = b | (rk << 5);
+      run += __popc(mine);
+    }
+    wsum[w * 32 + lane] = run;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t tot = 0;
+      for (int ww = 0; ww < C::NW; ww++) {
+        const uint32_t v = wsum[ww * 32 + lane];
+        wsum[ww * 32 + lane] = tot;
+        tot += v;
+      }
+      const uint32_t v = lane < (int)nb ? tot : 0;
+      uint32_t xs = v;
+      for (int q = 1; q < 32; q <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
+        if (lane >= q) xs += y;
+      }
+      poff[lane] = xs - v;
+      if (lane == 31) poff[kTB] = xs;
+      for (int ww = 0; ww < C::NW; ww++) wsum[ww * 32 + lane] += xs - v;
+      if (lane == 0) bulk_wait_read0();  // the previous piece's image has been read out
+    }
+    __syncthreads();
+    // ---- pass 2: every key to its place in the piece image
+    const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
+    K* outb = reinterpret_cast<K*>(outraw) + oshift;
+    const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
+    uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
+    const uint32_t* wbase = wsum + w * 32;
+    for (uint32_t q = q0 + lane; q < q1; q += 32) {
+      const uint32_t cd = code[q];
+      const uint32_t dpos = wbase[cd & 31] + (cd >> 5);
+      outb[dpos] = stage[q];
+      if (PAIRS) vout[dpos] = vstage[q];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    {
+      const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
+      const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
+      const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
+      if (a1 > a0) {
+        if (t == 0)
+          bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
+                   (uint32_t)(a1 - a0));
+        const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
+        if (t < (int)nh) dst[oc + t] = outb[t];
+        if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
+      } else {
+        for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
+      }
+      if (PAIRS) {
+        const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
+        const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
+        const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
+        if (c1 > c0) {
+          if (t == 0)
+            bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
+                     (uint32_t)(c1 - c0));
+          const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
+          if (t < (int)nh) vdst[oc + t] = vout[t];
+          if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
+        } else {
+          for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
+        }
+      }
+      if (t == 0) bulk_commit();
+    }
+    if (t <= kTB) ppre[uint64_t(ps) * kPP + t] = (uint16_t)poff[t];
+    __syncthreads();
+  }
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------
