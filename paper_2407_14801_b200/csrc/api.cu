@@ -291,8 +291,8 @@ template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4
 // piece-major transpose (sort path): threads, piece size, fragments per piece
 template <typename K, bool PAIRS> struct PmTr;
 template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128; };
-template <> struct PmTr<uint32_t, true> { static constexpr int NT = 512, S = 4096, F = 256; };
-template <> struct PmTr<uint64_t, false> { static constexpr int NT = 512, S = 4096, F = 256; };
+template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128; };
+template <> struct PmTr<uint64_t, false> { static constexpr int NT = 256, S = 4096, F = 128; };
 
 // cluster bucket sort: per-CTA tile (threads x keys) for 32-bit / 64-bit sort keys
 // (small per-CTA tiles keep 3 CTAs per SM resident; the big one serves the
@@ -471,7 +471,7 @@ struct Engine {
   // bucket sorts gather from T and write the sorted buckets back into X.
   void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
     using TC = PmTr<K, PAIRS>;
-    using CF = MsCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
+    using CF = RkCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
     ensure_scratch();
     g_stats.levels++;
     const int T = 1 - X;
@@ -618,7 +618,7 @@ struct Engine {
         k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pout);
         check_launch("k_piece_plan");
       }
-      auto f = k_transpose_pc<K, PAIRS, TC::NT, TC::S, TC::F>;
+      auto f = k_transpose_rk<K, PAIRS, TC::NT, TC::S, TC::F>;
       static int grid = 0;
       if (!grid) {
         set_smem(f, CF::SMEM);
@@ -628,7 +628,7 @@ struct Engine {
       f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), TC::NT, CF::SMEM, st>>>(
           dL, dTiles, pieces, (uint32_t)piece_tot, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv,
           segmat, ppre);
-      check_launch("k_transpose_pc");
+      check_launch("k_transpose_rk");
       ar.release(pieces);
     }
     // 5. bucket plan: sizes, final offsets, work lists

@@ -1457,6 +1457,229 @@ k_transpose_pc(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
 }
 
 // ------------------------------------------------------------------------------
+// SkewTranspose of one piece per iteration with counter-based ranking (the sort
+// path's transpose).  Per piece:
+//  * every key is fetched with cp.async straight to its stream position (padded
+//    layout: one pad word per 32 keeps the blocked accesses conflict-free);
+//  * thread t owns K = S/NT consecutive stream keys: their buckets come from a
+//    walk over the tile's thresholds (keys of a run are sorted, so a key usually
+//    needs one or two comparisons; a new run restarts with a 5-step search), and
+//    a thread-private counter per bucket gives each key's rank among the
+//    thread's keys of its bucket;
+//  * an exclusive scan of the counters in bucket-major, thread-minor order is the
+//    stable bucket-major position of every key (column order, then row order);
+//  * the piece image goes out with one bulk store; its bucket prefix goes to the
+//    piece tables.
+template <typename K, bool PAIRS, int NT, int S, int F>
+struct RkCfg {
+  static constexpr int NW = NT / 32;
+  static constexpr int KT = S / NT;  // keys per thread
+  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr int PADK = 128 / (int)sizeof(K);
+  static constexpr size_t off_stage = 0;  // S keys + pads
+  static constexpr size_t off_vstage = al((S + S / PADK + 1) * sizeof(K));
+  static constexpr size_t off_cnt = off_vstage + (PAIRS ? al((S + S / 32 + 1) * 4) : 0);  // 32 x NT u16
+  static constexpr size_t off_out = off_cnt + al(32 * NT * 2);
+  static constexpr size_t off_vout = off_out + al((S + 16 / sizeof(K) + 4) * sizeof(K));
+  static constexpr size_t off_frag = off_vout + (PAIRS ? al((S + 8) * 4) : 0);  // fstart[F+1], fsrc[F]
+  static constexpr size_t off_misc = al(off_frag + (2 * F + 1) * 4);
+  static constexpr size_t off_thr = al(off_misc + (64 + 33) * 4);
+  static constexpr size_t SMEM = al(off_thr + 32 * 16 + 32 * 4);
+  __device__ __forceinline__ static uint32_t pk(uint32_t i) { return i + i / PADK; }
+  __device__ __forceinline__ static uint32_t pw(uint32_t i) { return i + (i >> 5); }
+};
+
+template <typename K, bool PAIRS, int NT, int S, int F>
+__global__ void __launch_bounds__(NT)
+k_transpose_rk(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
+               const PieceDesc* __restrict__ pieces, uint32_t npslots, const K* __restrict__ src,
+               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
+  using C = RkCfg<K, PAIRS, NT, S, F>;
+  constexpr int KT = C::KT;
+  static_assert(F <= NT && S % NT == 0 && KT <= 16 && S <= 65535, "shape");
+  constexpr int EB = sizeof(K);
+  extern __shared__ __align__(128) unsigned char sm[];
+  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
+  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(sm + C::off_cnt);  // [bucket][thread]
+  uint32_t* cnt32 = reinterpret_cast<uint32_t*>(sm + C::off_cnt);
+  unsigned char* outraw = sm + C::off_out;
+  unsigned char* voutraw = sm + C::off_vout;
+  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
+  uint32_t* fsrc = fstart + F + 1;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
+  uint32_t* poff = misc + 64;
+  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr);
+  uint32_t* thr32 = reinterpret_cast<uint32_t*>(sm + C::off_thr + 32 * 16);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+
+  for (uint32_t ps = blockIdx.x; ps < npslots; ps += gridDim.x) {
+    const PieceDesc pd = pieces[ps];
+    if (pd.pn == 0) continue;  // uniform across the CTA
+    const TileInfo ti = tiles[pd.tile];
+    const LevelSeg sg = segs[ti.seg];
+    const uint32_t bt = ti.bt;
+    const uint32_t b0 = bt * kTB;
+    const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
+    const uint32_t Pn = pd.pn, nf = pd.nf, oc = pd.out;
+    if (t < 32) {
+      const K* P = piv + sg.piv_base;
+      const uint32_t j = b0 + 1 + t;
+      const bool real = t < (int)nb - 1;
+      const K pj = real ? P[j - 1] : K(0);
+      const bool dup = real && j >= 2 && P[j - 2] == pj;
+      thr[t] = Thr<K>::make(pj, dup, !real);
+      if constexpr (sizeof(K) == 4) {
+        // 32-bit form: passed(x) == (x >= thr32) for every key except 0xffffffff,
+        // whose bucket is the number of real thresholds at most 0xffffffff
+        const uint64_t t64 = real ? uint64_t(pj) + (dup ? 1u : 0u) : (1ull << 32);
+        thr32[t] = t64 > 0xffffffffull ? 0xffffffffu : (uint32_t)t64;
+        const uint32_t cntmax = __popc(__ballot_sync(0xffffffffu, t64 <= 0xffffffffull));
+        if (t == 0) misc[60] = cntmax;
+      }
+    }
+    for (int i = t; i < 32 * NT / 2; i += NT) cnt32[i] = 0;
+    // ---- fragments of the piece, prefix-summed
+    uint32_t len = 0, srcpos = 0;
+    if (t < (int)nf) {
+      const uint32_t cc = pd.col + t;
+      const uint32_t* row = segmat + sg.segmat_base + uint64_t(cc) * (sg.nbt + 1);
+      const uint32_t a = row[bt] + (t == 0 ? pd.off : 0), e = row[bt + 1];
+      len = e - a;
+      srcpos = sg.off + cc * sg.rows + a;
+    }
+    uint32_t wtot;
+    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
+    if (t < (int)nf) {
+      fstart[t] = ex;
+      fsrc[t] = srcpos - ex;  // global index of stream position 0 of this fragment's frame
+    }
+    if (t == 0) fstart[nf] = Pn;
+    __syncthreads();
+    // ---- load: one warp per fragment, cp.async to the padded stream positions
+    for (uint32_t f = w; f < nf; f += C::NW) {
+      const uint32_t fs = fstart[f], fe2 = fstart[f + 1];
+      const K* g = src + fsrc[f];
+      const uint32_t* gv = PAIRS ? vsrc + fsrc[f] : nullptr;
+      for (uint32_t q = fs + lane; q < fe2; q += 32) {
+        cp_async_elem(&stage[C::pk(q)], &g[q]);
+        if (PAIRS) cp_async_elem(&vstage[C::pw(q)], &gv[q]);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- pass 1: buckets (threshold walk) and thread-private counters
+    const uint32_t q0 = t * KT;
+    K xs[KT];
+    uint32_t code[KT];  // bucket | local rank << 8
+    {
+      const uint32_t bmax = sizeof(K) == 4 ? misc[60] : 0u;
+#pragma unroll
+      for (int j = 0; j < KT; j++) {
+        const uint32_t q = q0 + j;
+        const bool valid = q < Pn;
+        const K x = valid ? stage[C::pk(q)] : K(0);
+        xs[j] = x;
+        uint32_t b = 0;  // branch-free 5-step search: number of thresholds passed
+        if constexpr (sizeof(K) == 4) {
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) b += (uint32_t(x) >= thr32[b + st - 1]) ? st : 0;
+          b = uint32_t(x) == 0xffffffffu ? bmax : b;
+        } else {
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) b += thr[b + st - 1].passed(x) ? st : 0;
+        }
+        if (valid) {
+          uint16_t* cp = &cnt[b * NT + t];
+          const uint32_t lr = *cp;
+          *cp = (uint16_t)(lr + 1);
+          code[j] = b | (lr << 8);
+        } else {
+          code[j] = 0xffffffffu;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- exclusive scan of the counters, bucket-major (u16 pairs: entries 2i, 2i+1)
+    {
+      constexpr int PER = 32 * NT / 2 / NT;  // u32 words per thread = 16
+      uint32_t v[PER];
+      uint32_t sum = 0;
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        v[i] = cnt32[t * PER + i];
+        sum += (v[i] & 0xffffu) + (v[i] >> 16);
+      }
+      uint32_t tot;
+      uint32_t run = block_excl_sum<C::NW>(sum, misc, &tot);
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        const uint32_t lo = v[i] & 0xffffu, hi = v[i] >> 16;
+        cnt32[t * PER + i] = run | ((run + lo) << 16);
+        run += lo + hi;
+      }
+    }
+    __syncthreads();
+    if (t < 32) poff[t] = t < (int)nb ? cnt[t * NT] : Pn;
+    if (t == 32) poff[kTB] = Pn;
+    // ---- pass 2: scatter into the piece image (shifted for the bulk store)
+    if (t == 0) bulk_wait_read0();  // previous piece's image has been read out
+    __syncthreads();
+    const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
+    K* outb = reinterpret_cast<K*>(outraw) + oshift;
+    const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
+    uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
+#pragma unroll
+    for (int j = 0; j < KT; j++) {
+      const uint32_t cd = code[j];
+      if (cd != 0xffffffffu) {
+        const uint32_t b = cd & 0xff;
+        const uint32_t dpos = cnt[b * NT + t] + (cd >> 8);
+        outb[dpos] = xs[j];
+        if (PAIRS) vout[dpos] = vstage[C::pw(q0 + j)];
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    {
+      const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
+      const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
+      const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
+      if (a1 > a0) {
+        if (t == 0)
+          bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
+                   (uint32_t)(a1 - a0));
+        const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
+        if (t < (int)nh) dst[oc + t] = outb[t];
+        if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
+      } else {
+        for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
+      }
+      if (PAIRS) {
+        const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
+        const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
+        const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
+        if (c1 > c0) {
+          if (t == 0)
+            bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
+                     (uint32_t)(c1 - c0));
+          const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
+          if (t < (int)nh) vdst[oc + t] = vout[t];
+          if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
+        } else {
+          for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
+        }
+      }
+      if (t == 0) bulk_commit();
+    }
+    if (t <= kTB) ppre[uint64_t(ps) * kPP + t] = (uint16_t)poff[t];
+    __syncthreads();
+  }
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------
 // Bucket planning, per segment (one CTA): bucket sizes from the piece tables,
 // final offsets (exclusive scan, P:283 / P:461), RNG node keys, and the work
 // lists: single-value buckets (copy), on-chip classes, oversize.
