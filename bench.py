@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -56,7 +57,7 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -64,7 +65,7 @@ class Clocks:
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.p.terminate()
         self.p.wait()
         self.f.seek(0)
@@ -223,28 +224,48 @@ def main():
         int(w64.sum().item()) == int(pristine.to(torch.int64).sum().item())
     del w64
 
-    hbm, hbm_src, _ = peaks()
+    hbm, hbm_src, sm_mhz_max = peaks()
     b_alg = 6 * W * n  # column pass + SkewTranspose + bucket pass, read + write
-    # dominant kernel role and its HBM roofline (algorithmic bytes per launch / mean duration)
-    role_bytes = {"colsort": 2 * W * n, "bucketsort": 2 * W * n, "transpose": 2 * W * n,
-                  "count": W * n, "smallsort": 2 * W * n}
+    # Dominant kernel role and its roofline.  HBM-bound roles: algorithmic bytes per
+    # launch / mean launch duration.  Sort roles are bound by integer ALU issue: their
+    # work is key comparisons (n*log2(m) per level pass: m-key columns, and the
+    # bucket sizes' sum n_i log n_i <= n log sqrt(n) + 4e n), each a
+    # compare + select on the ALU pipe: peak = SMs * 64 ALU lanes/clk * clock / 2.
+    m = int(math.isqrt(n - 1)) + 1
+    comps = n * math.log2(m)
+    alu_peak = 148 * 64 * sm_mhz_max * 1e6 / 2 / 1e12  # T comparisons/s
+    hbm_roles = {"transpose": 2 * W * n, "count": W * n}
+    alu_roles = {"colsort": comps, "bucketsort": comps, "smallsort": n * math.log2(max(n, 2)),
+                 "clustersort": comps}
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
     dname, (dlaunch, dms) = dom
     per_step_launch = dlaunch / args.steps
-    bytes_per_launch = role_bytes.get(dname, 0) / max(per_step_launch, 1)
-    achieved = bytes_per_launch / (dms / dlaunch / 1e3) / 1e9 if dms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dname)
+            traffic = json.load(open(tp))["bytes_per_launch"].get(dname)
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-                "algorithmic_bytes_per_launch": bytes_per_launch,
-                "launches_per_step": per_step_launch,
-                "share_of_step": dms / total_ms if total_ms > 0 else None}
+    mean_launch_s = dms / dlaunch / 1e3 if dlaunch else 0.0
+    if dname in alu_roles:
+        work = alu_roles[dname] / max(per_step_launch, 1)
+        achieved = work / mean_launch_s / 1e12 if mean_launch_s else 0.0
+        hbm_view = 2 * W * n / max(per_step_launch, 1) / mean_launch_s / 1e9 if mean_launch_s else 0.0
+        roofline = {"bound": "alu", "kernel": dname, "achieved": achieved, "peak": alu_peak,
+                    "unit": "T comparisons/s", "frac": achieved / alu_peak, "traffic": traffic,
+                    "peak_source": f"derived: 148 SMs x 64 ALU lanes/clk x {sm_mhz_max:.0f} MHz / 2 ops "
+                                   "per comparison (DESIGN.md 8)",
+                    "algorithmic_work_per_launch": work, "launches_per_step": per_step_launch,
+                    "share_of_step": dms / total_ms if total_ms > 0 else None,
+                    "hbm_view": {"achieved_gbs": hbm_view, "frac_of_measured": hbm_view / hbm}}
+    else:
+        bytes_per_launch = hbm_roles.get(dname, 0) / max(per_step_launch, 1)
+        achieved = bytes_per_launch / mean_launch_s / 1e9 if mean_launch_s else 0.0
+        roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "launches_per_step": per_step_launch,
+                    "share_of_step": dms / total_ms if total_ms > 0 else None}
     step_gbs = b_alg / (ms / 1e3) / 1e9
 
     out = {
