@@ -87,46 +87,52 @@ struct BlockSort {
     thread_sort<K, V>(r);
 #pragma unroll 1
     for (uint32_t w = V; w < (uint32_t)TILE; w *= 2) {
-      __syncthreads();  // previous readers of s are done
-#pragma unroll
-      for (int j = 0; j < V; j++) s[pad(t * V + j)] = r[j];
-      __syncthreads();
-      // run A = [a0, b0), run B = [b0, bend) (TILE need not be a power of two: the
-      // last pair of a pass may be short or have no B run at all)
+      // Runs of width w: run A = [a0, b0) ascending, run B = [b0, bend) stored
+      // DESCENDING, so that each pair is a bitonic sequence.  Reading one past the
+      // end of A lands on B's largest key and one past the end of B on A's largest:
+      // neither is ever taken too early, so the merge needs no bounds checks.
       const uint32_t a0 = (t * V) & ~(2 * w - 1);
       const uint32_t b0 = min(a0 + w, (uint32_t)TILE), bend = min(a0 + 2 * w, (uint32_t)TILE);
       const uint32_t la = b0 - a0, lb = bend - b0;
+      {
+        __syncthreads();  // previous readers of s are done
+        // this thread's V keys belong to run ((t*V) / w); odd runs are stored reversed
+        const uint32_t r0 = (t * V) & ~(w - 1);
+        const bool rev = ((t * V) / w) & 1;
+        const uint32_t rlen = min(w, (uint32_t)TILE - r0);
+        const uint32_t off = t * V - r0;
+#pragma unroll
+        for (int j = 0; j < V; j++) {
+          const uint32_t pos = rev ? r0 + rlen - 1 - (off + j) : t * V + j;
+          s[pad(pos)] = r[j];
+        }
+        __syncthreads();
+      }
       const uint32_t diag = t * V - a0;
-      // merge path: smallest i with A[i] > B[diag-1-i] (ties taken from A first)
+      // merge path: smallest i with A[i] > B[diag-1-i]; B[k] lives at bend-1-k
       uint32_t lo = diag > lb ? diag - lb : 0;
       uint32_t hi = diag < la ? diag : la;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         const K x = s[pad(a0 + mid)];
-        const K y = s[pad(b0 + diag - 1 - mid)];
+        const K y = s[pad(bend - diag + mid)];
         const bool le = x <= y;
         lo = le ? mid + 1 : lo;
         hi = le ? hi : mid;
       }
-      uint32_t ja = a0 + lo, jb = b0 + diag - lo;
-      K a = ja < b0 ? s[pad(ja)] : KeyTraits<K>::kMax;
-      K b = jb < bend ? s[pad(jb)] : KeyTraits<K>::kMax;
-      // Branch-free serial merge.  An exhausted run reads as kMax: a real kMax
-      // key and the sentinel are equal values (pair composites never equal
-      // kMax), so which one is emitted never changes the output.  Reads one
-      // past a run stay inside the buffer (index <= TILE).
+      uint32_t pa = a0 + lo;                 // physical index of the next A key
+      uint32_t pb = bend - 1 - (diag - lo);  // physical index of the next B key (descending)
+      K a = s[pad(pa)];
+      K b = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
 #pragma unroll
       for (int k = 0; k < V; k++) {
         const bool takeA = a <= b;
         r[k] = takeA ? a : b;
-        const uint32_t jn = (takeA ? ja : jb) + 1;
-        const uint32_t end = takeA ? b0 : bend;
-        K v = s[pad(jn)];  // jn <= TILE: inside the buffer (SMEM_ELEMS > pad(TILE))
-        v = jn < end ? v : KeyTraits<K>::kMax;
+        pa = takeA ? pa + 1 : pa;
+        pb = takeA ? pb : pb - 1;
+        const K v = s[pad(takeA ? pa : pb)];
         a = takeA ? v : a;
         b = takeA ? b : v;
-        ja = takeA ? jn : ja;
-        jb = takeA ? jb : jn;
       }
     }
     __syncthreads();
