@@ -205,7 +205,7 @@ struct Arena {
 // ------------------------------------------------------------------ size classes
 // On-chip tiles (threads x keys per thread) for 32-bit sort keys and for
 // 64-bit sort keys (u64 keys, pair composites).
-static const uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 12288, 16384, 32768};
+static const uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 12288, 16384, 24576, 32768};
 
 template <typename SK> constexpr uint32_t key_max_tile() { return sizeof(SK) == 4 ? 32768u : 16384u; }
 
@@ -239,6 +239,7 @@ static void with_tile(uint32_t tile, F&& f) {
       case 8192: return f(IC<512>{}, IC<16>{});
       case 12288: return f(IC<384>{}, IC<32>{});
       case 16384: return f(IC<512>{}, IC<32>{});
+      case 24576: return f(IC<768>{}, IC<32>{});
       case 32768: return f(IC<1024>{}, IC<32>{});
     }
   } else {
@@ -304,7 +305,7 @@ template <typename SK> struct ClusterBig;
 template <> struct ClusterBig<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
 template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
 // largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
-template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
+template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 32768u : 8192u; }
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
 template <typename K> struct MergeCfg { static constexpr int NT = 256, VM = 16; };
@@ -634,7 +635,7 @@ struct Engine {
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};
     po.ncls = 0;
-    int cls_cl[16] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
+    int cls_cl[20] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
     {
       const uint32_t one = g_big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
       for (uint32_t t : kTiles)

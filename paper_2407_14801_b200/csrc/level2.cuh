@@ -1688,7 +1688,7 @@ struct PlanOut {
   uint32_t* count;      // [ncls + 2] atomic counters; ncls = copy list, ncls+1 = oversize
   uint32_t cap_per_list;
   uint32_t ncls;
-  uint32_t cls_tile[16];  // class tile sizes (ascending)
+  uint32_t cls_tile[20];  // class tile sizes (ascending)
   uint32_t max_tile;      // largest bucket sorted by one CTA
   // merge-sort base case for max_tile < size <= msort_max: chunks of <= max_tile keys,
   // sorted by one CTA each, then up to kMaxPasses merge passes with tiles of mtile keys
