@@ -63,6 +63,40 @@ __device__ __forceinline__ void thread_sort(K (&r)[V]) {
   if constexpr (V > 1) apply_net<K, V>(r, std::make_integer_sequence<int, OddEvenNet<V>::N>{});
 }
 
+// Warp-shuffle bitonic merge of sorted runs held by G/2-lane groups (each lane V
+// ascending keys, lanes in run order) into runs held by G-lane groups.  The
+// first half-cleaner compares element x of run A with element x of run B read
+// backwards (partner lane = lane ^ (G-1), register V-1-i), leaving the lower
+// half in A's lanes and the upper half in B's lanes, each a bitonic sequence in
+// storage order; the cross-lane half-cleaners (lane ^ d/V) and the in-register
+// ones then sort each half ascending.  No shared memory is touched.
+template <typename K, int V, int G>
+__device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
+  const int lane = threadIdx.x & 31;
+  const bool upper = (lane & (G / 2)) != 0;
+  {
+    K p[V];
+#pragma unroll
+    for (int i = 0; i < V; i++) p[i] = __shfl_xor_sync(0xffffffffu, r[V - 1 - i], G - 1);
+#pragma unroll
+    for (int i = 0; i < V; i++) r[i] = upper ? (r[i] < p[i] ? p[i] : r[i]) : (r[i] < p[i] ? r[i] : p[i]);
+  }
+#pragma unroll
+  for (int d = G / 4; d >= 1; d >>= 1) {  // cross-lane half-cleaners (distance d*V keys)
+    const bool hi = (lane & d) != 0;
+#pragma unroll
+    for (int i = 0; i < V; i++) {
+      const K q = __shfl_xor_sync(0xffffffffu, r[i], d);
+      r[i] = hi ? (r[i] < q ? q : r[i]) : (r[i] < q ? r[i] : q);
+    }
+  }
+#pragma unroll
+  for (int d = V / 2; d >= 1; d >>= 1)  // in-register half-cleaners
+#pragma unroll
+    for (int i = 0; i < V; i++)
+      if ((i & d) == 0) cas(r[i], r[i + d]);
+}
+
 template <typename K, int NT_, int V_>
 struct BlockSort {
   static constexpr int NT = NT_;
@@ -85,8 +119,12 @@ struct BlockSort {
 #pragma unroll
     for (int j = 0; j < V; j++) r[j] = s[pad(t * V + j)];
     thread_sort<K, V>(r);
+    // the first two merge levels (runs of V -> 2V -> 4V keys) stay in registers
+    constexpr uint32_t WL = (TILE >= 4 * V && NT >= 4) ? 4 * V : ((TILE >= 2 * V && NT >= 2) ? 2 * V : V);
+    if constexpr (WL >= 2 * V) warp_bitonic_merge<K, V, 2>(r);
+    if constexpr (WL >= 4 * V) warp_bitonic_merge<K, V, 4>(r);
 #pragma unroll 1
-    for (uint32_t w = V; w < (uint32_t)TILE; w *= 2) {
+    for (uint32_t w = WL; w < (uint32_t)TILE; w *= 2) {
       // Runs of width w: run A = [a0, b0) ascending, run B = [b0, bend) stored
       // DESCENDING, so that each pair is a bitonic sequence.  Reading one past the
       // end of A lands on B's largest key and one past the end of B on A's largest:
