@@ -113,37 +113,45 @@ struct BlockSort {
   // Sort the TILE keys held in s[pad(0..TILE-1)] (padding slots hold KeyTraits::kMax).
   // On return s holds the sorted tile (padded layout); a __syncthreads() has
   // been executed so all threads may read it.
+  // pad(q + j) for q a multiple of V and 0 <= j < V: the V keys of a thread block
+  // never straddle a pad period unevenly, so the offsets are compile-time constants.
+  __device__ __forceinline__ static constexpr uint32_t poff(int j) { return uint32_t(j + j / PER); }
+
   __device__ static void sort_smem(K* s) {
     const uint32_t t = threadIdx.x;
     K r[V];
+    {
+      const K* sb = s + pad(t * V);
 #pragma unroll
-    for (int j = 0; j < V; j++) r[j] = s[pad(t * V + j)];
+      for (int j = 0; j < V; j++) r[j] = sb[poff(j)];
+    }
     thread_sort<K, V>(r);
     // the first two merge levels (runs of V -> 2V -> 4V keys) stay in registers
     constexpr uint32_t WL = (TILE >= 4 * V && NT >= 4) ? 4 * V : ((TILE >= 2 * V && NT >= 2) ? 2 * V : V);
     if constexpr (WL >= 2 * V) warp_bitonic_merge<K, V, 2>(r);
     if constexpr (WL >= 4 * V) warp_bitonic_merge<K, V, 4>(r);
 #pragma unroll 1
-    for (uint32_t w = WL; w < (uint32_t)TILE; w *= 2) {
+    for (uint32_t w = WL; w < (uint32_t)TILE; w *= 2) {  // w is a power of two
       // Runs of width w: run A = [a0, b0) ascending, run B = [b0, bend) stored
       // DESCENDING, so that each pair is a bitonic sequence.  Reading one past the
       // end of A lands on B's largest key and one past the end of B on A's largest:
       // neither is ever taken too early, so the merge needs no bounds checks.
-      const uint32_t a0 = (t * V) & ~(2 * w - 1);
+      const uint32_t tv = t * V;
+      const uint32_t a0 = tv & ~(2 * w - 1);
       const uint32_t b0 = min(a0 + w, (uint32_t)TILE), bend = min(a0 + 2 * w, (uint32_t)TILE);
       const uint32_t la = b0 - a0, lb = bend - b0;
       {
-        __syncthreads();  // previous readers of s are done
-        // this thread's V keys belong to run ((t*V) / w); odd runs are stored reversed
-        const uint32_t r0 = (t * V) & ~(w - 1);
-        const bool rev = ((t * V) / w) & 1;
+        // this thread's V keys belong to run tv / w; odd runs are stored reversed: the
+        // thread's block [tv, tv+V) of run [r0, r0+rlen) lands, reversed, on the block
+        // starting at r0 + rlen - V - (tv - r0) (a multiple of V, as rlen is)
+        const bool rev = (tv & w) != 0;
+        const uint32_t r0 = tv & ~(w - 1);
         const uint32_t rlen = min(w, (uint32_t)TILE - r0);
-        const uint32_t off = t * V - r0;
+        const uint32_t q = rev ? 2 * r0 + rlen - V - tv : tv;
+        K* sb = s + pad(q);
+        __syncthreads();  // previous readers of s are done
 #pragma unroll
-        for (int j = 0; j < V; j++) {
-          const uint32_t pos = rev ? r0 + rlen - 1 - (off + j) : t * V + j;
-          s[pad(pos)] = r[j];
-        }
+        for (int j = 0; j < V; j++) sb[poff(j)] = rev ? r[V - 1 - j] : r[j];
         __syncthreads();
       }
       const uint32_t diag = t * V - a0;
@@ -174,8 +182,11 @@ struct BlockSort {
       }
     }
     __syncthreads();
+    {
+      K* sb = s + pad(t * V);
 #pragma unroll
-    for (int j = 0; j < V; j++) s[pad(t * V + j)] = r[j];
+      for (int j = 0; j < V; j++) sb[poff(j)] = r[j];
+    }
     __syncthreads();
   }
 };
