@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsquaresort.so")
 SOURCES = ["api.cu"]
-DEPS = ["api.cu", "common.cuh", "blocksort.cuh", "level.cuh", "level2.cuh"]
+DEPS = ["api.cu", "common.cuh", "blocksort.cuh", "level.cuh", "level2.cuh", "skew.cuh"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared"]
 

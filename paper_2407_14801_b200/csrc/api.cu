@@ -20,7 +20,7 @@
 #include <vector>
 
 #include "../../include/squaresort.h"
-#include "level2.cuh"
+#include "skew.cuh"
 
 namespace sq {
 
@@ -291,9 +291,9 @@ template <> struct TrCfg<uint32_t, true> { static constexpr int NT = 256, S = 40
 template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
 // piece-major transpose (sort path): threads, piece size, fragments per piece
 template <typename K, bool PAIRS> struct PmTr;
-template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128; };
-template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128; };
-template <> struct PmTr<uint64_t, false> { static constexpr int NT = 256, S = 4096, F = 128; };
+template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
+template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
+template <> struct PmTr<uint64_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
 
 // cluster bucket sort: per-CTA tile (threads x keys) for 32-bit / 64-bit sort keys
 // (small per-CTA tiles keep 3 CTAs per SM resident; the big one serves the
@@ -619,17 +619,18 @@ struct Engine {
         k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pout);
         check_launch("k_piece_plan");
       }
-      auto f = k_transpose_rk<K, PAIRS, TC::NT, TC::S, TC::F>;
+      using XC = CtCfg<K, PAIRS, TC::XNT, TC::S, TC::F>;
+      auto f = k_transpose_ct<K, PAIRS, TC::XNT, TC::S, TC::F>;
       static int grid = 0;
       if (!grid) {
-        set_smem(f, CF::SMEM);
-        grid = wave_grid(f, TC::NT, CF::SMEM);
+        set_smem(f, XC::SMEM);
+        grid = wave_grid(f, TC::XNT, XC::SMEM);
       }
       ProfScope ps("transpose", st);
-      f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), TC::NT, CF::SMEM, st>>>(
+      f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), TC::XNT, XC::SMEM, st>>>(
           dL, dTiles, pieces, (uint32_t)piece_tot, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv,
           segmat, ppre);
-      check_launch("k_transpose_rk");
+      check_launch("k_transpose_ct");
       ar.release(pieces);
     }
     // 5. bucket plan: sizes, final offsets, work lists
