@@ -342,10 +342,15 @@ struct CtCfg {
   static constexpr size_t off_thr = off_bits + 2 * BITS_B;
   static constexpr size_t off_out = off_thr + 2 * THR_B;  // S keys + shift
   static constexpr size_t off_vout = off_out + al((S + 16 / EB) * EB);
-  static constexpr size_t off_cnt = off_vout + (PAIRS ? al((S + 4) * 4) : 0);  // 32 x NT u16
-  static constexpr size_t off_misc = off_cnt + al(33 * NT * 2);
+  static constexpr size_t off_cnt = off_vout + (PAIRS ? al((S + 4) * 4) : 0);  // 33 x NT u32
+  static constexpr size_t off_misc = off_cnt + al(33 * NT * 4);
   static constexpr size_t SMEM = off_misc + al(128 * 4);
 };
+
+// counter entry e = bucket * NT + thread -> word: 16-byte chunks XOR-swizzled by
+// (e / 32) % 8, so both the per-thread scan reads (32 consecutive entries) and the
+// per-warp atomics (32 consecutive entries of one bucket) are conflict-free
+__device__ __forceinline__ uint32_t cswz(uint32_t e) { return e ^ (((e >> 5) & 7) << 2); }
 
 template <typename K, bool PAIRS, int NT, int S, int F>
 __device__ __forceinline__ uint32_t ct_stage(uint32_t ps, uint32_t npslots, int b, unsigned char* sm,
@@ -452,8 +457,7 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
   extern __shared__ __align__(128) unsigned char sm[];
   unsigned char* outraw = sm + C::off_out;
   unsigned char* voutraw = sm + C::off_vout;
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(sm + C::off_cnt);  // [bucket][thread]
-  uint32_t* cnt32 = reinterpret_cast<uint32_t*>(sm + C::off_cnt);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + C::off_cnt);  // [bucket][thread], + a dummy row
   uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
   uint32_t* poff = misc + 64;
   const int t = threadIdx.x, lane = t & 31;
@@ -464,7 +468,7 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
     // stage the next piece into the other buffer while this one is processed
     const uint32_t nps = ct_stage<K, PAIRS, NT, S, F>(ps + gridDim.x, npslots, b ^ 1, sm, segs, tiles, pieces, src,
                                                       vsrc, piv, segmat);
-    for (int i = t; i < 33 * NT / 2; i += NT) cnt32[i] = 0;  // 32 bucket rows + the dummy row
+    for (int i = t; i < 33 * NT; i += NT) cnt[i] = 0;  // 32 bucket rows + the dummy row
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncthreads();
     const K* slot = reinterpret_cast<const K*>(sm + C::off_slot + b * C::SLOT_B);
@@ -525,33 +529,37 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
         for (int st = 16; st >= 1; st >>= 1) bk += thr[bk + st - 1].passed(x) ? st : 0;
       }
       bk = ((vb >> j) & 1) ? bk : 32u;  // invalid words count in a dummy row
-      uint16_t* cp = &cnt[bk * NT + t];
-      const uint32_t r = *cp;
-      *cp = (uint16_t)(r + 1);
+      // shared atomics: the counter updates of one thread are independent (a
+      // load/store pair would serialise them through possible aliasing)
+      const uint32_t r = atomicAdd(&cnt[cswz(bk * NT + t)], 1u);
       cd[j] = bk | (r << 8);
     }
     __syncthreads();
-    // ---- exclusive scan of the counters, bucket-major (u16 pairs: entries 2i, 2i+1)
+    // ---- exclusive scan of the counters, bucket-major (thread u: entries 32u .. 32u+31,
+    // read as eight 16-byte chunks; the swizzle makes them conflict-free)
     {
-      constexpr int PER = 32 * NT / 2 / NT;  // u32 words per thread = 16
-      uint32_t v[PER];
       uint32_t sum = 0;
 #pragma unroll
-      for (int i = 0; i < PER; i++) {
-        v[i] = cnt32[t * PER + i];
-        sum += (v[i] & 0xffffu) + (v[i] >> 16);
+      for (int i = 0; i < 8; i++) {
+        const uint4 q = *reinterpret_cast<const uint4*>(&cnt[cswz(32 * t + 4 * i)]);
+        sum += q.x + q.y + q.z + q.w;
       }
       uint32_t tot;
       uint32_t run = block_excl_sum<NW>(sum, misc, &tot);
 #pragma unroll
-      for (int i = 0; i < PER; i++) {
-        const uint32_t lo = v[i] & 0xffffu, hi = v[i] >> 16;
-        cnt32[t * PER + i] = run | ((run + lo) << 16);
-        run += lo + hi;
+      for (int i = 0; i < 8; i++) {
+        uint4* p4 = reinterpret_cast<uint4*>(&cnt[cswz(32 * t + 4 * i)]);
+        const uint4 q = *p4;
+        uint4 o;
+        o.x = run; run += q.x;
+        o.y = run; run += q.y;
+        o.z = run; run += q.z;
+        o.w = run; run += q.w;
+        *p4 = o;
       }
     }
     __syncthreads();
-    if (t < 32) poff[t] = t < (int)nb ? cnt[t * NT] : Pn;
+    if (t < 32) poff[t] = t < (int)nb ? cnt[cswz(t * NT)] : Pn;
     if (t == 32) poff[kTB] = Pn;
     if (t == 0) bulk_wait_read0();  // previous piece's image has been read out
     __syncthreads();
@@ -564,7 +572,7 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
     for (int j = 0; j < KT; j++) {
       const uint32_t bk = cd[j] & 0xff;
       if (bk < 32) {
-        const uint32_t dpos = cnt[bk * NT + t] + (cd[j] >> 8);
+        const uint32_t dpos = cnt[cswz(bk * NT + t)] + (cd[j] >> 8);
         outb[dpos] = xs[j];
         if (PAIRS) vout[dpos] = vslot[w0 + j];
       }
