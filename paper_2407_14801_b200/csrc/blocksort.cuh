@@ -117,19 +117,28 @@ struct BlockSort {
   // never straddle a pad period unevenly, so the offsets are compile-time constants.
   __device__ __forceinline__ static constexpr uint32_t poff(int j) { return uint32_t(j + j / PER); }
 
-  __device__ static void sort_smem(K* s) {
+  // Keys at positions >= len are padding (kMax).  Sorted, every position >= len holds
+  // kMax after every merge pass, so threads whose whole block lies there skip the
+  // work (and warps entirely in the padding skip the register stages).
+  __device__ static void sort_smem(K* s, uint32_t len = TILE) {
     const uint32_t t = threadIdx.x;
     K r[V];
-    {
-      const K* sb = s + pad(t * V);
+    if ((t & ~31u) * V < len) {  // warp-uniform
+      {
+        const K* sb = s + pad(t * V);
 #pragma unroll
-      for (int j = 0; j < V; j++) r[j] = sb[poff(j)];
+        for (int j = 0; j < V; j++) r[j] = sb[poff(j)];
+      }
+      thread_sort<K, V>(r);
+      // the first two merge levels (runs of V -> 2V -> 4V keys) stay in registers
+      constexpr uint32_t WL0 = (TILE >= 4 * V && NT >= 4) ? 4 * V : ((TILE >= 2 * V && NT >= 2) ? 2 * V : V);
+      if constexpr (WL0 >= 2 * V) warp_bitonic_merge<K, V, 2>(r);
+      if constexpr (WL0 >= 4 * V) warp_bitonic_merge<K, V, 4>(r);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; j++) r[j] = KeyTraits<K>::kMax;
     }
-    thread_sort<K, V>(r);
-    // the first two merge levels (runs of V -> 2V -> 4V keys) stay in registers
     constexpr uint32_t WL = (TILE >= 4 * V && NT >= 4) ? 4 * V : ((TILE >= 2 * V && NT >= 2) ? 2 * V : V);
-    if constexpr (WL >= 2 * V) warp_bitonic_merge<K, V, 2>(r);
-    if constexpr (WL >= 4 * V) warp_bitonic_merge<K, V, 4>(r);
 #pragma unroll 1
     for (uint32_t w = WL; w < (uint32_t)TILE; w *= 2) {  // w is a power of two
       // Runs of width w: run A = [a0, b0) ascending, run B = [b0, bend) stored
@@ -154,6 +163,7 @@ struct BlockSort {
         for (int j = 0; j < V; j++) sb[poff(j)] = rev ? r[V - 1 - j] : r[j];
         __syncthreads();
       }
+      if (tv >= len) continue;  // r[] stays all kMax
       const uint32_t diag = t * V - a0;
       // merge path: smallest i with A[i] > B[diag-1-i]; B[k] lives at bend-1-k
       uint32_t lo = diag > lb ? diag - lb : 0;
@@ -210,7 +220,7 @@ k_blocksort(const SegDesc* __restrict__ segs, const K* __restrict__ src, K* __re
   const K* in = src + d.off;
   for (int i = threadIdx.x; i < BS::TILE; i += NT) s[BS::pad(i)] = i < (int)d.len ? in[i] : KeyTraits<K>::kMax;
   __syncthreads();
-  BS::sort_smem(s);
+  BS::sort_smem(s, d.len);
   K* out = dst + d.off;
   for (int i = threadIdx.x; i < (int)d.len; i += NT) out[i] = s[BS::pad(i)];
 }
@@ -235,7 +245,7 @@ k_blocksort_pairs(const SegDesc* __restrict__ segs, const uint32_t* __restrict__
     s[BS::pad(i)] = c;
   }
   __syncthreads();
-  BS::sort_smem(s);
+  BS::sort_smem(s, d.len);
   for (int i = threadIdx.x; i < (int)d.len; i += NT) {
     uint64_t c = s[BS::pad(i)];
     kdst[d.off + i] = uint32_t(c >> 32);

@@ -89,7 +89,7 @@ k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* _
     s[BS::pad(i)] = x;
   }
   __syncthreads();
-  BS::sort_smem(s);
+  BS::sort_smem(s, np);
   int viol = 0;
   for (int i = threadIdx.x + 1; i < (int)np; i += NT)
     if (!(s[BS::pad(i - 1)] < s[BS::pad(i)])) viol = 1;
@@ -173,7 +173,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
     s[BS::pad(i)] = x;
   }
   __syncthreads();
-  BS::sort_smem(s);
+  BS::sort_smem(s, d.len);
   auto key_at = [&](int i) -> K {
     if constexpr (PAIRS) return K(s[BS::pad(i)] >> 32);
     else return s[BS::pad(i)];
@@ -1906,7 +1906,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
       }
       __syncthreads();
     }
-    BS::sort_smem(s);
+    BS::sort_smem(s, len);
     for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
       if constexpr (PAIRS) {
