@@ -52,10 +52,37 @@ struct OddEvenNet {
   }
 };
 
+// Compare-exchange that puts half of its work on the FMA pipe: min on the ALU pipe,
+// max = a + b - min (exact modulo 2^32) as two integer multiply-adds.  The sorts are
+// ALU-pipe bound (min/max/select/compare all issue there at half rate), the FMA pipe
+// is nearly idle; alternating the two forms balances the pipes.
+// The multiplier is read from constant memory so that ptxas cannot fold the
+// multiply-adds into ALU adds.
+__constant__ int32_t c_one = 1, c_mone = -1, c_mtwo = -2;
+__device__ __forceinline__ void cas_fma(uint32_t& a, uint32_t& b, uint32_t one, uint32_t mone) {
+  const uint32_t lo = min(a, b);
+  uint32_t sum, hi;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(sum) : "r"(a), "r"(one), "r"(b));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"(lo), "r"(mone), "r"(sum));
+  a = lo;
+  b = hi;
+}
+template <typename K>
+__device__ __forceinline__ void cas_fma_k(K& a, K& b, uint32_t one, uint32_t mone) {
+  if constexpr (sizeof(K) == 4) cas_fma(a, b, one, mone);
+  else cas(a, b);
+}
+template <typename K, int C>
+__device__ __forceinline__ void cas_bal(K& a, K& b, uint32_t one, uint32_t mone) {
+  if constexpr (sizeof(K) == 4 && (C & 1)) cas_fma(a, b, one, mone);
+  else cas(a, b);
+}
+
 template <typename K, int V, int... I>
 __device__ __forceinline__ void apply_net(K (&r)[V], std::integer_sequence<int, I...>) {
   constexpr OddEvenNet<V> net{};
-  (cas(r[net.a[I]], r[net.b[I]]), ...);
+  const uint32_t one = (uint32_t)c_one, mone = (uint32_t)c_mone;
+  (cas_bal<K, I>(r[net.a[I]], r[net.b[I]], one, mone), ...);
 }
 
 template <typename K, int V>
@@ -70,24 +97,42 @@ __device__ __forceinline__ void thread_sort(K (&r)[V]) {
 // half in A's lanes and the upper half in B's lanes, each a bitonic sequence in
 // storage order; the cross-lane half-cleaners (lane ^ d/V) and the in-register
 // ones then sort each half ascending.  No shared memory is touched.
+// upper ? max(x, y) : min(x, y).  For 32-bit keys with F set, one min on the ALU
+// pipe and three multiply-adds on the FMA pipe: m + u*(x + y - 2m), u = upper.
+template <typename K>
+__device__ __forceinline__ K dir_minmax(bool F, K x, K y, bool upper, uint32_t u, uint32_t one, uint32_t mtwo) {
+  if (sizeof(K) == 4 && F) {
+    const uint32_t m = min(uint32_t(x), uint32_t(y));
+    uint32_t sum, d, o;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(sum) : "r"(uint32_t(x)), "r"(one), "r"(uint32_t(y)));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(m), "r"(mtwo), "r"(sum));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(o) : "r"(u), "r"(d), "r"(m));
+    return K(o);
+  } else {
+    return upper ? (x < y ? y : x) : (x < y ? x : y);
+  }
+}
+
 template <typename K, int V, int G>
 __device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
   const int lane = threadIdx.x & 31;
   const bool upper = (lane & (G / 2)) != 0;
+  const uint32_t one = (uint32_t)c_one, mone = (uint32_t)c_mone, mtwo = (uint32_t)c_mtwo;
   {
     K p[V];
 #pragma unroll
     for (int i = 0; i < V; i++) p[i] = __shfl_xor_sync(0xffffffffu, r[V - 1 - i], G - 1);
 #pragma unroll
-    for (int i = 0; i < V; i++) r[i] = upper ? (r[i] < p[i] ? p[i] : r[i]) : (r[i] < p[i] ? r[i] : p[i]);
+    for (int i = 0; i < V; i++) r[i] = dir_minmax<K>(false, r[i], p[i], upper, upper ? 1u : 0u, one, mtwo);
   }
 #pragma unroll
   for (int d = G / 4; d >= 1; d >>= 1) {  // cross-lane half-cleaners (distance d*V keys)
     const bool hi = (lane & d) != 0;
+    const uint32_t u = hi ? 1u : 0u;
 #pragma unroll
     for (int i = 0; i < V; i++) {
       const K q = __shfl_xor_sync(0xffffffffu, r[i], d);
-      r[i] = hi ? (r[i] < q ? q : r[i]) : (r[i] < q ? r[i] : q);
+      r[i] = dir_minmax<K>(false, r[i], q, hi, u, one, mtwo);
     }
   }
 #pragma unroll
@@ -176,17 +221,19 @@ struct BlockSort {
         lo = le ? mid + 1 : lo;
         hi = le ? hi : mid;
       }
-      uint32_t pa = a0 + lo;                 // physical index of the next A key
-      uint32_t pb = bend - 1 - (diag - lo);  // physical index of the next B key (descending)
+      const uint32_t pa = a0 + lo;                 // physical index of the next A key
+      const uint32_t pb = bend - 1 - (diag - lo);  // physical index of the next B key (descending)
       K a = s[pad(pa)];
       K b = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
+      uint32_t na = pa + 1, nb = pb - 1;  // the index each run reads next
 #pragma unroll
       for (int k = 0; k < V; k++) {
         const bool takeA = a <= b;
         r[k] = takeA ? a : b;
-        pa = takeA ? pa + 1 : pa;
-        pb = takeA ? pb : pb - 1;
-        const K v = s[pad(takeA ? pa : pb)];
+        const uint32_t idx = takeA ? na : nb;
+        na += takeA ? 1u : 0u;
+        nb -= takeA ? 0u : 1u;
+        const K v = s[pad(idx)];
         a = takeA ? v : a;
         b = takeA ? b : v;
       }
