@@ -305,10 +305,12 @@ template <typename SK> struct ClusterBig;
 template <> struct ClusterBig<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
 template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
 // largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
-template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 32768u : 8192u; }
+template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
-template <typename K> struct MergeCfg { static constexpr int NT = 256, VM = 16; };
+template <typename K, bool PAIRS> struct MergeCfg {
+  static constexpr int NT = 256, VM = PAIRS ? 16 : 32;
+};
 
 // Side streams for running the bucket-class kernels concurrently.
 struct SideStreams {
@@ -660,7 +662,7 @@ struct Engine {
     uint64_t level_keys = 0;
     for (const Seg& g : segs) level_keys += g.len;
     po.msort_max = po.max_tile;
-    po.mtile = MergeCfg<K>::NT * MergeCfg<K>::VM;
+    po.mtile = MergeCfg<K, PAIRS>::NT * MergeCfg<K, PAIRS>::VM;
     po.mcap = 1;
     if (g_big_mode == 1) {  // multi-CTA merge sort for buckets of up to 16 chunks
       po.msort_max = 16u * po.max_tile;
@@ -744,7 +746,7 @@ struct Engine {
     }
     g_event_pool.push_back(fork);
     if (g_big_mode == 1) {  // merge passes of the multi-CTA base case (buffers X <-> U)
-      using MC = MergeCfg<K>;
+      using MC = MergeCfg<K, PAIRS>;
       using BS = BlockSort<K, MC::NT, MC::VM>;
       const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
       auto f = k_merge_pass<K, PAIRS, MC::NT, MC::VM>;
@@ -753,12 +755,17 @@ struct Engine {
         set_smem(f, smem);
         grid = wave_grid(f, MC::NT, smem);
       }
+      uint32_t* splits = (uint32_t*)ar.alloc(uint64_t(po.mcap) * 4);
       for (uint32_t p = 0; p < (uint32_t)kMaxPasses; p++) {
         ProfScope ps("merge", st);
-        f<<<grid, MC::NT, smem, st>>>(recs, po.mlist + uint64_t(p) * po.mcap, po.mcount + p, p, kb[X], kb[2],
-                                      PAIRS ? vb[X] : nullptr, PAIRS ? vb[2] : nullptr);
+        const MTile* items = po.mlist + uint64_t(p) * po.mcap;
+        k_merge_split<K><<<2 * num_sms(), 256, 0, st>>>(recs, items, po.mcount + p, p, po.mtile, kb[X], kb[2], splits);
+        check_launch("k_merge_split");
+        f<<<grid, MC::NT, smem, st>>>(recs, items, po.mcount + p, p, kb[X], kb[2], PAIRS ? vb[X] : nullptr,
+                                      PAIRS ? vb[2] : nullptr, splits);
         check_launch("k_merge_pass");
       }
+      ar.release(splits);
     }
     {  // single-value buckets (copied) and oversize buckets (made contiguous)
       ProfScope ps("gather", st);

@@ -1957,11 +1957,40 @@ __device__ __forceinline__ uint32_t warp_split(const SEQ& A, const SEQ& B, uint3
   return lo;
 }
 
+// Merge-path split of every merge item of a pass, one thread per item (a binary
+// search in global memory; all items in flight at once instead of one latency-bound
+// search per CTA inside the merge kernel).  splits[it] = A keys before output tile it.
+template <typename K>
+__global__ void k_merge_split(const BucketRec* __restrict__ recs, const MTile* __restrict__ items,
+                              const uint32_t* __restrict__ count, uint32_t pass, uint32_t TM,
+                              const K* __restrict__ bufX, const K* __restrict__ bufU, uint32_t* __restrict__ splits) {
+  const uint32_t total = *count;
+  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < total; it += gridDim.x * blockDim.x) {
+    const MTile mt = items[it];
+    const BucketRec rc = recs[mt.bucket];
+    const uint32_t R = rc.chunk << pass;
+    const bool src_is_U = ((rc.passes - pass) & 1) != 0;
+    const K* src = src_is_U ? bufU : bufX;
+    const uint32_t a0 = 2 * mt.pair * R;
+    const uint32_t b0 = min(rc.size, a0 + R), b1 = min(rc.size, a0 + 2 * R);
+    const K* A = src + rc.out + a0;
+    const K* B = src + rc.out + b0;
+    const uint32_t la = b0 - a0, lb = b1 - b0;
+    const uint32_t d = mt.tile * TM;
+    uint32_t lo = d > lb ? d - lb : 0, hi = min(d, la);
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    splits[it] = lo;
+  }
+}
+
 template <typename K, bool PAIRS, int NT, int VM>
 __global__ void __launch_bounds__(NT)
 k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items, const uint32_t* __restrict__ count,
              uint32_t pass, K* __restrict__ bufX, K* __restrict__ bufU, uint32_t* __restrict__ vX,
-             uint32_t* __restrict__ vU) {
+             uint32_t* __restrict__ vU, const uint32_t* __restrict__ splits) {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   constexpr int TM = NT * VM;
   using BS = BlockSort<K, NT, VM>;  // padding helper only
@@ -1984,50 +2013,92 @@ k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items
     const uint32_t b0 = min(rc.size, a0 + R), b1 = min(rc.size, a0 + 2 * R);
     GSeq<K> A{src + rc.out + a0, b0 - a0}, B{src + rc.out + b0, b1 - b0};
     const uint32_t d0 = mt.tile * TM, d1 = min(d0 + TM, A.len + B.len);
-    if (w < 2) {
-      const uint32_t sp = warp_split<GSeq<K>, K>(A, B, w == 0 ? d0 : d1);
-      if (lane == 0) split[w] = sp;
+    // the next item is the next output tile of the same pair, unless this is the last
+    bool last = it + 1 >= total;
+    if (!last) {
+      const MTile nx = items[it + 1];
+      last = nx.bucket != mt.bucket || nx.pair != mt.pair;
     }
-    __syncthreads();
-    const uint32_t sa0 = split[0], sa1 = split[1];
+    const uint32_t sa0 = splits[it], sa1 = last ? A.len : splits[it + 1];
+    (void)split;
+    (void)w;
+    (void)lane;
     const uint32_t na = sa1 - sa0, nb = (d1 - sa1) - (d0 - sa0), sb0 = d0 - sa0;
-    for (uint32_t i = threadIdx.x; i < na + nb; i += NT) {  // all loads in flight at once
-      const bool fa = i < na;
-      const uint32_t gi = fa ? a0 + sa0 + i : b0 + sb0 + (i - na);
-      cp_async_elem(&sk[BS::pad(i)], &src[rc.out + gi]);
-      if (PAIRS) cp_async_elem(&sv[i], &vsrc[rc.out + gi]);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    // merge stage[0,na) with stage[na,na+nb): thread t -> outputs [t*VM, t*VM+VM)
     const uint32_t m = na + nb, dd = threadIdx.x * VM;
     K r[VM];
     uint32_t ri[VM];
-    if (dd < m) {
-      uint32_t lo = dd > nb ? dd - nb : 0, hi = min(dd, na);
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        const bool le = sk[BS::pad(mid)] <= sk[BS::pad(na + dd - 1 - mid)];
-        lo = le ? mid + 1 : lo;
-        hi = le ? hi : mid;
+    if (!PAIRS && m == (uint32_t)TM) {  // uniform across the CTA
+      // keys only, full tile: A ascending at [0, na), B DESCENDING at [na, m)
+      // (bitonic), so the merge needs no bounds checks (as in BlockSort; ties between
+      // a phantom and a real key carry equal values, so keys-only output is
+      // unaffected).  Partial tiles (the last of a pair) take the checked merge.
+      for (uint32_t i = threadIdx.x; i < m; i += NT) {  // all loads in flight at once
+        const bool fa = i < na;
+        const uint32_t gi = fa ? a0 + sa0 + i : b0 + sb0 + (i - na);
+        cp_async_elem(&sk[BS::pad(fa ? i : na + m - 1 - i)], &src[rc.out + gi]);
       }
-      uint32_t ja = lo, jb = na + dd - lo;
-      K a = ja < na ? sk[BS::pad(ja)] : KeyTraits<K>::kMax;
-      K b = jb < m ? sk[BS::pad(jb)] : KeyTraits<K>::kMax;
+      cp_async_wait_all();
+      __syncthreads();
+      if (dd < m) {
+        uint32_t lo = dd > nb ? dd - nb : 0, hi = min(dd, na);
+        while (lo < hi) {  // smallest i with A[i] > B[dd-1-i]; B[k] lives at m-1-k
+          const uint32_t mid = (lo + hi) >> 1;
+          const bool le = sk[BS::pad(mid)] <= sk[BS::pad(m - dd + mid)];
+          lo = le ? mid + 1 : lo;
+          hi = le ? hi : mid;
+        }
+        const uint32_t pa = lo, pb = m - 1 - (dd - lo);
+        K a = sk[BS::pad(pa)];
+        K b = nb ? sk[BS::pad(pb)] : KeyTraits<K>::kMax;
+        uint32_t na_ = pa + 1, nb_ = pb - 1;
 #pragma unroll
-      for (int k = 0; k < VM; k++) {
-        // ties and exhausted runs: take A unless A is exhausted (stability for pairs)
-        const bool takeA = ja < na && (jb >= m || a <= b);
-        r[k] = takeA ? a : b;
-        ri[k] = takeA ? ja : jb;
-        const uint32_t jn = (takeA ? ja : jb) + 1;
-        const uint32_t end = takeA ? na : m;
-        K v = sk[BS::pad(jn)];
-        v = jn < end ? v : KeyTraits<K>::kMax;
-        a = takeA ? v : a;
-        b = takeA ? b : v;
-        ja = takeA ? jn : ja;
-        jb = takeA ? jb : jn;
+        for (int k = 0; k < VM; k++) {
+          const bool takeA = a <= b;
+          r[k] = takeA ? a : b;
+          const uint32_t idx = takeA ? na_ : nb_;
+          na_ += takeA ? 1u : 0u;
+          nb_ -= takeA ? 0u : 1u;
+          const K v = sk[BS::pad(idx)];
+          a = takeA ? v : a;
+          b = takeA ? b : v;
+        }
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < m; i += NT) {  // all loads in flight at once
+        const bool fa = i < na;
+        const uint32_t gi = fa ? a0 + sa0 + i : b0 + sb0 + (i - na);
+        cp_async_elem(&sk[BS::pad(i)], &src[rc.out + gi]);
+        if (PAIRS) cp_async_elem(&sv[i], &vsrc[rc.out + gi]);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      // merge stage[0,na) with stage[na,na+nb): thread t -> outputs [t*VM, t*VM+VM)
+      if (dd < m) {
+        uint32_t lo = dd > nb ? dd - nb : 0, hi = min(dd, na);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          const bool le = sk[BS::pad(mid)] <= sk[BS::pad(na + dd - 1 - mid)];
+          lo = le ? mid + 1 : lo;
+          hi = le ? hi : mid;
+        }
+        uint32_t ja = lo, jb = na + dd - lo;
+        K a = ja < na ? sk[BS::pad(ja)] : KeyTraits<K>::kMax;
+        K b = jb < m ? sk[BS::pad(jb)] : KeyTraits<K>::kMax;
+#pragma unroll
+        for (int k = 0; k < VM; k++) {
+          // ties and exhausted runs: take A unless A is exhausted (stability for pairs)
+          const bool takeA = ja < na && (jb >= m || a <= b);
+          r[k] = takeA ? a : b;
+          ri[k] = takeA ? ja : jb;
+          const uint32_t jn = (takeA ? ja : jb) + 1;
+          const uint32_t end = takeA ? na : m;
+          K v = sk[BS::pad(jn)];
+          v = jn < end ? v : KeyTraits<K>::kMax;
+          a = takeA ? v : a;
+          b = takeA ? b : v;
+          ja = takeA ? jn : ja;
+          jb = takeA ? jb : jn;
+        }
       }
     }
     uint32_t rv[VM];
@@ -2035,13 +2106,23 @@ k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items
 #pragma unroll
       for (int k = 0; k < VM; k++) rv[k] = dd + k < m ? sv[ri[k]] : 0u;
     }
+    (void)ri;
     __syncthreads();
+    if (dd + VM <= m) {
+      K* sb = sk + BS::pad(dd);
 #pragma unroll
-    for (int k = 0; k < VM; k++)
-      if (dd + k < m) {
-        sk[BS::pad(dd + k)] = r[k];
+      for (int k = 0; k < VM; k++) {
+        sb[BS::poff(k)] = r[k];
         if (PAIRS) sv[dd + k] = rv[k];
       }
+    } else {
+#pragma unroll
+      for (int k = 0; k < VM; k++)
+        if (dd + k < m) {
+          sk[BS::pad(dd + k)] = r[k];
+          if (PAIRS) sv[dd + k] = rv[k];
+        }
+    }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < m; i += NT) {
       dst[rc.out + a0 + d0 + i] = sk[BS::pad(i)];
