@@ -474,7 +474,6 @@ struct Engine {
   // bucket sorts gather from T and write the sorted buckets back into X.
   void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
     using TC = PmTr<K, PAIRS>;
-    using CF = RkCfg<K, PAIRS, TC::NT, TC::S, TC::F>;
     ensure_scratch();
     g_stats.levels++;
     const int T = 1 - X;
@@ -615,10 +614,11 @@ struct Engine {
     }
     {
       PieceDesc* pieces = (PieceDesc*)ar.alloc(piece_tot * sizeof(PieceDesc));
-      SQ_CUDA(cudaMemsetAsync(pieces, 0, piece_tot * sizeof(PieceDesc), st));
+      uint32_t* pcount = (uint32_t*)ar.alloc(16);
+      SQ_CUDA(cudaMemsetAsync(pcount, 0, 4, st));
       {
         ProfScope ps("tiles", st);
-        k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pout);
+        k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout);
         check_launch("k_piece_plan");
       }
       using XC = CtCfg<K, PAIRS, TC::XNT, TC::S, TC::F>;
@@ -630,9 +630,9 @@ struct Engine {
       }
       ProfScope ps("transpose", st);
       f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), TC::XNT, XC::SMEM, st>>>(
-          dL, dTiles, pieces, (uint32_t)piece_tot, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv,
-          segmat, ppre);
+          pieces, pcount, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv, segmat, ppre);
       check_launch("k_transpose_ct");
+      ar.release(pcount);
       ar.release(pieces);
     }
     // 5. bucket plan: sizes, final offsets, work lists

@@ -328,249 +328,6 @@ __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* _
 }
 
 // ------------------------------------------------------------------------------
-// SkewTranspose, piece-major (see the header).  CTA per bucket tile; the tile's
-// stream is the concatenation over columns c = 0..ncols-1 of the column's run
-// of this tile (sorted, contiguous).  A piece = up to S keys from up to F runs
-// ("fragments"); per piece: cp.async the fragments into shared memory, find
-// each key's bucket among the tile's kTB boundaries, rank it stably within its
-// (fragment, bucket) group -- in a sorted fragment a bucket is one contiguous
-// group -- and scan group sizes down the fragments per bucket.  The piece's
-// bucket-major image is written contiguously; its bucket prefix goes to the
-// piece tables.  Shared arrays are padded (one word per 32) so the blocked
-// per-thread loops are bank-conflict free.
-template <typename K, bool PAIRS, int NT, int S, int F>
-struct PmCfg {
-  static constexpr int NW = NT / 32;
-  static constexpr int VS = S / NT;
-  static constexpr int PADK = 128 / sizeof(K);  // elements per pad period for K arrays
-  static constexpr int SK = S + S / PADK + 1;   // padded K-array length
-  static constexpr int SW = S + S / 32 + 1;     // padded u32-array length
-  static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t off_stage = 0;
-  static constexpr size_t off_vstage = al(off_stage + SK * sizeof(K));
-  static constexpr size_t off_code = al(off_vstage + (PAIRS ? SW * 4 : 0));
-  static constexpr size_t off_out = al(off_code + SW * 4);
-  static constexpr size_t off_vout = al(off_out + S * sizeof(K));
-  static constexpr size_t off_table = al(off_vout + (PAIRS ? S * 4 : 0));  // F x kTB u16
-  static constexpr size_t off_fstart = al(off_table + F * kTB * 2);          // F+1 u32
-  static constexpr size_t off_fsrc = al(off_fstart + (F + 1) * 4);           // F u32
-  static constexpr size_t off_wsum = al(off_fsrc + F * 4);                   // NW x 32 u32
-  static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);             // 64 + 3*32+1 u32
-  static constexpr size_t off_bval = al(off_misc + (64 + 3 * kTB + 8) * 4);
-  static constexpr size_t SMEM = al(off_bval + kTB * sizeof(K));
-  __device__ __forceinline__ static int pk(int i) { return i + i / PADK; }
-  __device__ __forceinline__ static int pw(int i) { return i + (i >> 5); }
-};
-
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_pm(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const K* __restrict__ src,
-               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint32_t* __restrict__ pout,
-               uint16_t* __restrict__ ppre) {
-  using C = PmCfg<K, PAIRS, NT, S, F>;
-  static_assert(F <= 256 && F <= NT && S <= 65535 && S % NT == 0 && NT % 32 == 0, "shape");
-  extern __shared__ __align__(16) unsigned char sm[];
-  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
-  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
-  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);  // frag << 8 | bucket
-  K* outb = reinterpret_cast<K*>(sm + C::off_out);
-  uint32_t* vout = reinterpret_cast<uint32_t*>(sm + C::off_vout);
-  uint16_t* table = reinterpret_cast<uint16_t*>(sm + C::off_table);
-  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_fstart);
-  uint32_t* fsrc = reinterpret_cast<uint32_t*>(sm + C::off_fsrc);
-  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);  // [0..31] scans
-  uint32_t* ptot = misc + 64;
-  uint32_t* poff = ptot + kTB;     // kTB + 1 entries
-  uint32_t* bdupv = poff + kTB + 1;
-  K* bval = reinterpret_cast<K*>(sm + C::off_bval);
-
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const TileInfo ti = tiles[blockIdx.x];
-  const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt;
-  const uint32_t b0 = bt * kTB;
-  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
-  const uint32_t nint = nb - 1;
-  const K* P = piv + sg.piv_base;
-  if (t < (int)nint) {
-    const uint32_t j = b0 + 1 + t;
-    bval[t] = P[j - 1];
-    bdupv[t] = (j >= 2 && P[j - 2] == P[j - 1]) ? 1u : 0u;
-  }
-  uint32_t oc = ti.out, npc = 0;
-  uint32_t c = 0, o = 0;  // next column and offset inside its run (uniform across the CTA)
-  const int i0 = t * C::VS;
-  const uint32_t* rows = segmat + sg.segmat_base;
-  const uint32_t rstride = sg.nbt + 1;
-
-  while (c < sg.ncols) {
-    // ---- window: the runs of columns c .. c+F-1, prefix-summed; take up to S keys
-    uint32_t len = 0, srcpos = 0;
-    if (t < F && c + t < sg.ncols) {
-      const uint32_t* row = rows + uint64_t(c + t) * rstride;
-      const uint32_t a = row[bt], e = row[bt + 1];
-      const uint32_t skip = t == 0 ? o : 0;
-      len = e - a - skip;
-      srcpos = sg.off + (c + t) * sg.rows + a + skip;
-    }
-    uint32_t wtot;
-    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
-    if (t < F) {
-      fstart[t] = ex;
-      fsrc[t] = srcpos;
-    }
-    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
-    // fragments overlapping [0, S): the runs of the window whose prefix is below S
-    const int inpiece = (t < (int)nwin && ex < (uint32_t)S) ? 1 : 0;
-    const uint32_t nf = __syncthreads_count(inpiece);
-    const uint32_t Pn = min((uint32_t)S, wtot);
-    if (t == 0) fstart[nf] = Pn;  // clips the last fragment at S
-    __syncthreads();
-    uint32_t nc, no;
-    if (wtot <= (uint32_t)S) {  // the whole window fits
-      nc = c + nwin;
-      no = 0;
-    } else {  // the piece ends inside run nf-1: continue there if it has keys left
-      const uint32_t last = nf - 1;
-      const uint32_t used = Pn - fstart[last];
-      const uint32_t* row = rows + uint64_t(c + last) * rstride;
-      const uint32_t base = last == 0 ? o : 0;
-      const uint32_t full = row[bt + 1] - row[bt] - base;
-      if (used < full) {
-        nc = c + last;
-        no = base + used;
-      } else {
-        nc = c + last + 1;
-        no = 0;
-      }
-    }
-    if (Pn > 0) {
-      for (uint32_t i = t; i < nf * kTB; i += NT) table[i] = 0;
-      // ---- load fragments (one warp per fragment, cp.async, coalesced)
-      for (uint32_t f = w; f < nf; f += C::NW) {
-        const uint32_t fs = fstart[f], fe = fstart[f + 1];
-        const K* gs = src + fsrc[f] - fs;
-        const uint32_t* gv = PAIRS ? vsrc + fsrc[f] - fs : nullptr;
-        for (uint32_t q = fs + lane; q < fe; q += 32) {
-          cp_async_elem(&stage[C::pk(q)], &gs[q]);
-          if (PAIRS) cp_async_elem(&vstage[C::pw(q)], &gv[q]);
-          code[C::pw(q)] = f << 8;
-        }
-      }
-      cp_async_wait_all();
-      __syncthreads();
-      // ---- bucket of every key (binary search over the tile's boundaries), striped
-      for (int i = t; i < (int)Pn; i += NT) {
-        const K xk = stage[C::pk(i)];
-        uint32_t lo = 0, hi = nint;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (before_boundary(xk, bval[mid], bdupv[mid] != 0)) hi = mid; else lo = mid + 1;
-        }
-        code[C::pw(i)] |= lo;
-      }
-      __syncthreads();
-      // ---- group heads (fragment or bucket changes); carry = last head before this thread
-      uint32_t last_head = 0;
-      {
-        uint32_t prev = (i0 > 0 && i0 <= (int)Pn) ? code[C::pw(i0 - 1)] : 0xffffffffu;
-        for (int q = 0; q < C::VS; q++) {
-          const int i = i0 + q;
-          if (i < (int)Pn) {
-            const uint32_t cd = code[C::pw(i)];
-            if (i == 0 || cd != prev) last_head = i;
-            prev = cd;
-          }
-        }
-      }
-      const uint32_t carry = block_excl_max<C::NW>(last_head, misc);
-      // ---- group sizes into the (fragment, bucket) table: the last key of a group writes
-      {
-        uint32_t head = carry;
-        uint32_t cur = (i0 > 0 && i0 <= (int)Pn) ? code[C::pw(i0 - 1)] : 0xffffffffu;
-        for (int q = 0; q < C::VS; q++) {
-          const int i = i0 + q;
-          if (i < (int)Pn) {
-            const uint32_t cd = code[C::pw(i)];
-            if (i == 0 || cd != cur) head = i;
-            cur = cd;
-            const bool lastg = (i == (int)Pn - 1) || code[C::pw(i + 1)] != cd;
-            if (lastg) table[(cd >> 8) * kTB + (cd & 0xff)] = (uint16_t)(i - head + 1);
-          }
-        }
-      }
-      __syncthreads();
-      // ---- exclusive scan of the table down the fragments, per bucket (lane = bucket)
-      const uint32_t per = (nf + C::NW - 1) / C::NW;
-      const uint32_t f0 = min(nf, w * per), f1 = min(nf, f0 + per);
-      {
-        uint32_t sum = 0;
-        for (uint32_t f = f0; f < f1; f++) sum += table[f * kTB + lane];
-        wsum[w * 32 + lane] = sum;
-      }
-      __syncthreads();
-      {
-        uint32_t run = 0, total = 0;
-        for (int ww = 0; ww < C::NW; ww++) {
-          const uint32_t v = wsum[ww * 32 + lane];
-          if (ww < w) run += v;
-          total += v;
-        }
-        for (uint32_t f = f0; f < f1; f++) {
-          const uint32_t v = table[f * kTB + lane];
-          table[f * kTB + lane] = (uint16_t)run;
-          run += v;
-        }
-        if (w == 0) {
-          ptot[lane] = total;
-          uint32_t v = lane < (int)nb ? total : 0, xs = v;
-          for (int q = 1; q < 32; q <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
-            if (lane >= q) xs += y;
-          }
-          poff[lane] = xs - v;
-          if (lane == 31) poff[kTB] = xs;
-        }
-      }
-      __syncthreads();
-      // ---- scatter into the piece's bucket-major image
-      {
-        uint32_t head = carry;
-        uint32_t cur = (i0 > 0 && i0 <= (int)Pn) ? code[C::pw(i0 - 1)] : 0xffffffffu;
-        for (int q = 0; q < C::VS; q++) {
-          const int i = i0 + q;
-          if (i < (int)Pn) {
-            const uint32_t cd = code[C::pw(i)];
-            if (i == 0 || cd != cur) head = i;
-            cur = cd;
-            const uint32_t b = cd & 0xff;
-            const uint32_t dpos = poff[b] + table[(cd >> 8) * kTB + b] + (i - head);
-            outb[dpos] = stage[C::pk(i)];
-            if (PAIRS) vout[dpos] = vstage[C::pw(i)];
-          }
-        }
-      }
-      __syncthreads();
-      for (uint32_t q = t; q < Pn; q += NT) {
-        dst[oc + q] = outb[q];
-        if (PAIRS) vdst[oc + q] = vout[q];
-      }
-      const uint32_t pe = ti.piece_base + npc;
-      if (t == 0) pout[pe] = oc;
-      if (t <= kTB) ppre[uint64_t(pe) * kPP + t] = (uint16_t)poff[t];
-      oc += Pn;
-      npc++;
-    }
-    c = nc;
-    o = no;
-    __syncthreads();
-  }
-  if (t == 0) tiles[blockIdx.x].npieces = npc;
-}
-
-// ------------------------------------------------------------------------------
 // TMA helpers (cp.async.bulk: SASS UBLKCP) and an mbarrier.
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
@@ -608,332 +365,7 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 
-// ------------------------------------------------------------------------------
-// SkewTranspose, piece-major, TMA-staged.  Same contract as k_transpose_pm.
-// Per piece (up to S keys from up to F runs of the tile's column-major stream):
-//  * every run fragment is fetched with ONE bulk copy (its 16-byte-aligned
-//    envelope, placed so the keys keep their alignment), completion on an
-//    mbarrier;
-//  * warp w owns a contiguous range of fragments: lane b binary-searches the
-//    end of bucket b inside the fragment (a sorted run: each bucket is one
-//    contiguous group), giving the (fragment, bucket) counts and a per-warp
-//    running prefix per bucket;
-//  * a block scan over warps and buckets gives every group's offset in the
-//    piece's bucket-major image; each key finds its bucket by a 5-step shuffle
-//    search over the lanes' bucket ends and is stored at its offset;
-//  * the image is written back with one bulk store (unaligned head and tail
-//    by threads); the bucket prefix goes to the piece tables.
-template <typename K, bool PAIRS, int NT, int S, int F>
-struct TmaCfg {
-  static constexpr int NW = NT / 32;
-  static constexpr int SLK = 48 / (int)sizeof(K);  // slack elements per fragment slot
-  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t STG = al((S + SLK * F + 16) * sizeof(K));
-  static constexpr size_t VSTG = PAIRS ? al((S + 12 * F + 16) * 4) : 0;
-  static constexpr size_t OUT = al((S + 16 / sizeof(K) + 4) * sizeof(K));
-  static constexpr size_t VOUT = PAIRS ? al((S + 8) * 4) : 0;
-  static constexpr size_t CODE = al((S + SLK * F + 16) * 4);
-  static constexpr size_t off_stage = 0;
-  static constexpr size_t off_vstage = off_stage + STG;
-  static constexpr size_t off_code = off_vstage + VSTG;  // per stage slot: bucket | rank << 5
-  static constexpr size_t off_out = off_code + CODE;
-  static constexpr size_t off_vout = off_out + OUT;
-  static constexpr size_t off_frag = al(off_vout + VOUT);  // fstart[F+1], fsrc[F], fe[F], fve[F]
-  static constexpr size_t off_wsum = al(off_frag + (4 * F + 1) * 4);  // NW x 32 u32
-  static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);
-  static constexpr size_t off_bval = al(off_misc + (64 + 2 * 33) * 4);
-  static constexpr size_t off_bar = al(off_bval + kTB * (sizeof(K) + 4));
-  static constexpr size_t SMEM = off_bar + 16;
-};
 
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_tma(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const K* __restrict__ src,
-                K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-                const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint32_t* __restrict__ pout,
-                uint16_t* __restrict__ ppre) {
-  using C = TmaCfg<K, PAIRS, NT, S, F>;
-  static_assert(F <= NT && F % 32 == 0 && S <= 65535 && NT % 32 == 0, "shape");
-  constexpr int EB = sizeof(K);
-  extern __shared__ __align__(128) unsigned char sm[];
-  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
-  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
-  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);
-  unsigned char* outraw = sm + C::off_out;
-  unsigned char* voutraw = sm + C::off_vout;
-  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
-  uint32_t* fsrc = fstart + F + 1;
-  uint32_t* fe = fsrc + F;   // stage element index of the fragment's first key
-  uint32_t* fve = fe + F;    // vstage element index (pairs)
-  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  uint32_t* poff = misc + 64;  // 33 entries: bucket offsets in the piece image
-  K* bval = reinterpret_cast<K*>(sm + C::off_bval);
-  uint32_t* bdupv = reinterpret_cast<uint32_t*>(sm + C::off_bval + kTB * sizeof(K));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::off_bar);
-
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const TileInfo ti = tiles[blockIdx.x];
-  const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt;
-  const uint32_t b0 = bt * kTB;
-  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
-  const K* P = piv + sg.piv_base;
-  if (t < (int)nb - 1) {  // internal boundary b0+1+t ends bucket t of the tile
-    const uint32_t j = b0 + 1 + t;
-    bval[t] = P[j - 1];
-    bdupv[t] = (j >= 2 && P[j - 2] == P[j - 1]) ? 1u : 0u;
-  }
-  if (t == 0) {
-    mbar_init(bar, 1);
-    fence_proxy_async();
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  uint32_t oc = ti.out, npc = 0;
-  uint32_t c = 0, o = 0;
-  const uint32_t* rows = segmat + sg.segmat_base;
-  const uint32_t rstride = sg.nbt + 1;
-
-  while (c < sg.ncols) {
-    // ---- window of F runs, prefix sums; the piece takes up to S keys
-    uint32_t len = 0, srcpos = 0;
-    if (t < F && c + t < sg.ncols) {
-      const uint32_t* row = rows + uint64_t(c + t) * rstride;
-      const uint32_t a = row[bt], e = row[bt + 1];
-      const uint32_t skip = t == 0 ? o : 0;
-      len = e - a - skip;
-      srcpos = sg.off + (c + t) * sg.rows + a + skip;
-    }
-    uint32_t wtot;
-    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
-    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
-    const int inpiece = (t < (int)nwin && ex < (uint32_t)S) ? 1 : 0;
-    const uint32_t nf = __syncthreads_count(inpiece);
-    const uint32_t Pn = min((uint32_t)S, wtot);
-    // ---- issue the bulk copies (thread f owns fragment f)
-    if (t < (int)nf) {
-      const uint32_t flen = min(ex + len, Pn) - ex;
-      fstart[t] = ex;
-      fsrc[t] = srcpos;
-      const uintptr_t ga = reinterpret_cast<uintptr_t>(src + srcpos);
-      const uint32_t mis = (uint32_t)(ga & 15);
-      const uint32_t slot = (uint32_t)C::al((ex + C::SLK * t) * EB);  // byte offset, 16-aligned
-      fe[t] = (slot + mis) / EB;
-      if (flen) {
-        const uint32_t bytes = (mis + flen * EB + 15) & ~15u;
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(reinterpret_cast<unsigned char*>(stage) + slot, reinterpret_cast<const void*>(ga - mis), bytes,
-                 bar);
-      }
-      if (PAIRS) {
-        const uintptr_t va = reinterpret_cast<uintptr_t>(vsrc + srcpos);
-        const uint32_t vmis = (uint32_t)(va & 15);
-        const uint32_t vslot = (uint32_t)C::al((ex + 12 * t) * 4);
-        fve[t] = (vslot + vmis) / 4;
-        if (flen) {
-          const uint32_t vbytes = (vmis + flen * 4 + 15) & ~15u;
-          mbar_expect_tx(bar, vbytes);
-          bulk_g2s(reinterpret_cast<unsigned char*>(vstage) + vslot, reinterpret_cast<const void*>(va - vmis), vbytes,
-                   bar);
-        }
-      }
-    }
-    if (t == 0) fstart[nf] = Pn;
-    // next window position (same rule as k_transpose_pm)
-    uint32_t nc, no;
-    if (wtot <= (uint32_t)S) {
-      nc = c + nwin;
-      no = 0;
-    } else {
-      __syncthreads();
-      const uint32_t last = nf - 1;
-      const uint32_t used = Pn - fstart[last];
-      const uint32_t* row = rows + uint64_t(c + last) * rstride;
-      const uint32_t base = last == 0 ? o : 0;
-      const uint32_t full = row[bt + 1] - row[bt] - base;
-      if (used < full) {
-        nc = c + last;
-        no = base + used;
-      } else {
-        nc = c + last + 1;
-        no = 0;
-      }
-    }
-    __syncthreads();  // all expect_tx posted before the single arrival
-    if (Pn > 0) {
-      if (t == 0) mbar_arrive(bar);
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      // ---- pass 1: warp w walks its fragments in 32-key chunks (sorted keys, one per
-      // lane).  Lane j finds where boundary j falls among the chunk's keys (5 shuffle
-      // steps) -- the end of bucket j in the chunk; each key then finds its bucket
-      // among those ends (5 steps).  Its rank among the warp's keys of that bucket
-      // (stream order) is the bucket's running count plus its offset in the group.
-      const uint32_t per = (nf + C::NW - 1) / C::NW;
-      const uint32_t f0 = min(nf, w * per), f1 = min(nf, f0 + per);
-      const bool has_thr = lane < (int)nb - 1;
-      const K thr_v = has_thr ? bval[lane] : K(0);
-      const bool thr_d = has_thr && bdupv[lane] != 0;
-      uint32_t run = 0;  // lane b: keys of bucket b in this warp's earlier chunks
-      for (uint32_t f = f0; f < f1; f++) {
-        const uint32_t flen = fstart[f + 1] - fstart[f];
-        const K* fk = stage + fe[f];
-        uint32_t* fc = code + fe[f];
-        for (uint32_t c0 = 0; c0 < flen; c0 += 32) {
-          const uint32_t cl = min(32u, flen - c0);
-          const K x = lane < (int)cl ? fk[c0 + lane] : KeyTraits<K>::kMax;
-          uint32_t p = 0;
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) {
-            const K y = __shfl_sync(0xffffffffu, x, p + st - 1);
-            if (has_thr && before_boundary(y, thr_v, thr_d)) p += st;
-          }
-          {  // the 5 steps reach at most 31: all 32 keys may lie before the boundary
-            const K yl = __shfl_sync(0xffffffffu, x, 31);
-            if (p == 31 && has_thr && before_boundary(yl, thr_v, thr_d)) p = 32;
-          }
-          const uint32_t endb = has_thr ? min(p, cl) : cl;
-          uint32_t startb = __shfl_up_sync(0xffffffffu, endb, 1);
-          if (lane == 0) startb = 0;
-          uint32_t bk = 0;
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) {
-            const uint32_t e = __shfl_sync(0xffffffffu, endb, bk + st - 1);
-            if (e <= (uint32_t)lane) bk += st;
-          }
-          const uint32_t rk = __shfl_sync(0xffffffffu, run - startb, bk) + lane;
-          if (lane < (int)cl) fc[c0 + lane] = bk | (rk << 5);
-          run += endb - startb;
-        }
-      }
-      wsum[w * 32 + lane] = run;
-      __syncthreads();
-      // ---- block scan: per bucket, warp bases (exclusive over warps) + bucket offsets in the piece
-      if (w == 0) {
-        uint32_t tot = 0;
-        for (int ww = 0; ww < C::NW; ww++) {
-          const uint32_t v = wsum[ww * 32 + lane];
-          wsum[ww * 32 + lane] = tot;
-          tot += v;
-        }
-        const uint32_t v = lane < (int)nb ? tot : 0;
-        uint32_t xs = v;
-        for (int q = 1; q < 32; q <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
-          if (lane >= q) xs += y;
-        }
-        poff[lane] = xs - v;
-        if (lane == 31) poff[kTB] = xs;
-        for (int ww = 0; ww < C::NW; ww++) wsum[ww * 32 + lane] += xs - v;
-      }
-      __syncthreads();
-      // ---- pass 2: every key to its place in the piece's bucket-major image (shifted for the bulk store)
-      const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
-      K* outb = reinterpret_cast<K*>(outraw) + oshift;
-      const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
-      uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
-      const uint32_t* wbase = wsum + w * 32;
-      for (uint32_t f = f0; f < f1; f++) {
-        const uint32_t flen = fstart[f + 1] - fstart[f];
-        const K* fk = stage + fe[f];
-        const uint32_t* fc = code + fe[f];
-        const uint32_t* fv = PAIRS ? vstage + fve[f] : nullptr;
-        for (uint32_t i = lane; i < flen; i += 32) {
-          const uint32_t cd = fc[i];
-          const uint32_t dpos = wbase[cd & 31] + (cd >> 5);
-          outb[dpos] = fk[i];
-          if (PAIRS) vout[dpos] = fv[i];
-        }
-      }
-      fence_proxy_async();
-      __syncthreads();
-      // ---- write the image: bulk store of the aligned body, threads do head and tail
-      {
-        const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
-        const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
-        const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
-        if (a1 > a0) {
-          if (t == 0) {
-            bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
-                     (uint32_t)(a1 - a0));
-          }
-          const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
-          if (t < (int)nh) dst[oc + t] = outb[t];
-          if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
-        } else {
-          for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
-        }
-        if (PAIRS) {
-          const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
-          const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
-          const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
-          if (c1 > c0) {
-            if (t == 0)
-              bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
-                       (uint32_t)(c1 - c0));
-            const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
-            if (t < (int)nh) vdst[oc + t] = vout[t];
-            if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
-          } else {
-            for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
-          }
-        }
-        if (t == 0) bulk_commit();
-      }
-      const uint32_t pe = ti.piece_base + npc;
-      if (t == 0) pout[pe] = oc;
-      if (t <= kTB) ppre[uint64_t(pe) * kPP + t] = (uint16_t)poff[t];
-      oc += Pn;
-      npc++;
-      if (t == 0) bulk_wait_read0();  // the image buffer may be rewritten next piece
-    }
-    c = nc;
-    o = no;
-    __syncthreads();
-  }
-  if (t == 0) {
-    tiles[blockIdx.x].npieces = npc;
-    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-  }
-}
-
-// ------------------------------------------------------------------------------
-// SkewTranspose, piece-major, TMA-staged, multisplit ranking (the sort path's
-// transpose).  Same contract and piece/window logic as k_transpose_tma; per piece:
-//  * bulk copies of the run fragments into aligned slots, then a warp-per-fragment
-//    compaction into stream order (the tile's column-major order);
-//  * pass 1, warp w over a contiguous range of the stream, 32 keys at a time:
-//    bucket by a branch-free 5-step search over the tile's thresholds, and a
-//    stable rank among the warp's keys of that bucket from 5 ballots (lane j also
-//    gets the count of bucket j) -- no dependence on fragment boundaries;
-//  * a block scan over (warp, bucket) gives the image offsets; pass 2 places every
-//    key; the image is written with one bulk store.
-template <typename K, bool PAIRS, int NT, int S, int F>
-struct MsCfg {
-  static constexpr int NW = NT / 32;
-  static constexpr int SLK = 48 / (int)sizeof(K);
-  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr size_t SLOT = al((S + SLK * F + 16) * sizeof(K));
-  static constexpr size_t VSLOT = PAIRS ? al((S + 12 * F + 16) * 4) : 0;
-  static constexpr size_t off_slot = 0;
-  static constexpr size_t off_vslot = off_slot + SLOT;
-  static constexpr size_t off_stage = off_vslot + VSLOT;                 // S keys, stream order
-  static constexpr size_t off_vstage = off_stage + al(S * sizeof(K));
-  static constexpr size_t off_code = off_vstage + (PAIRS ? al(S * 4) : 0);  // S u32
-  static constexpr size_t off_out = off_code + al(S * 4);  // the piece image (read by the bulk store)
-  static constexpr size_t off_vout = off_out + al((S + 16 / sizeof(K) + 4) * sizeof(K));
-  static constexpr size_t off_frag = off_vout + (PAIRS ? al((S + 8) * 4) : 0);  // fstart[F+1], fsrc[F], fe[F], fve[F]
-  static constexpr size_t off_wcnt = al(off_frag + (4 * F + 1) * 4);  // NW x 32 u32 running bucket counts
-  static constexpr size_t off_wsum = al(off_wcnt + NW * 32 * 4);
-  static constexpr size_t off_misc = al(off_wsum + NW * 32 * 4);
-  static constexpr size_t off_thr = al(off_misc + (64 + 33) * 4);      // 32 thresholds (u64 / pairs of u64)
-  static constexpr size_t off_bar = al(off_thr + 32 * 16);
-  static constexpr size_t SMEM = off_bar + 16;
-};
-
-// "x lies in a bucket after boundary j" for the tile's thresholds, branch-free.
-// u32 keys: threshold t = p + dup as u64 (x >= t).  u64 keys: (p, dup) pair.
 template <typename K> struct Thr;
 template <> struct Thr<uint32_t> {
   uint64_t t;
@@ -948,260 +380,31 @@ template <> struct Thr<uint64_t> {
   __device__ __forceinline__ bool passed(uint64_t x) const { return dup != 2 && (x > p || (x == p && dup == 0)); }
 };
 
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_ms(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const K* __restrict__ src,
-               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint32_t* __restrict__ pout,
-               uint16_t* __restrict__ ppre) {
-  using C = MsCfg<K, PAIRS, NT, S, F>;
-  static_assert(F <= NT && F % 32 == 0 && S <= 65535 && S % (32 * (NT / 32)) == 0, "shape");
-  constexpr int EB = sizeof(K);
-  extern __shared__ __align__(128) unsigned char sm[];
-  K* slot = reinterpret_cast<K*>(sm + C::off_slot);
-  uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot);
-  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
-  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
-  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);
-  unsigned char* outraw = sm + C::off_out;
-  unsigned char* voutraw = sm + C::off_vout;
-  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
-  uint32_t* fsrc = fstart + F + 1;
-  uint32_t* fe = fsrc + F;
-  uint32_t* fve = fe + F;
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(sm + C::off_wcnt);
-  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  uint32_t* poff = misc + 64;
-  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::off_bar);
-
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const TileInfo ti = tiles[blockIdx.x];
-  const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt;
-  const uint32_t b0 = bt * kTB;
-  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
-  const K* P = piv + sg.piv_base;
-  if (t < 32) {  // threshold j ends bucket j of the tile (j < nb-1); the rest never pass
-    const uint32_t j = b0 + 1 + t;
-    const bool real = t < (int)nb - 1;
-    const K pj = real ? P[j - 1] : K(0);
-    const bool dup = real && j >= 2 && P[j - 2] == pj;
-    thr[t] = Thr<K>::make(pj, dup, !real);
-  }
-  if (t == 0) {
-    mbar_init(bar, 1);
-    fence_proxy_async();
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  uint32_t oc = ti.out, npc = 0;
-  uint32_t c = 0, o = 0;
-  const uint32_t* rows = segmat + sg.segmat_base;
-  const uint32_t rstride = sg.nbt + 1;
-  constexpr uint32_t PER_W = S / (NT / 32);  // stream keys per warp
-
-  while (c < sg.ncols) {
-    // ---- window of F runs; the piece takes up to S keys (same rule as k_transpose_tma)
-    uint32_t len = 0, srcpos = 0;
-    if (t < F && c + t < sg.ncols) {
-      const uint32_t* row = rows + uint64_t(c + t) * rstride;
-      const uint32_t a = row[bt], e = row[bt + 1];
-      const uint32_t skip = t == 0 ? o : 0;
-      len = e - a - skip;
-      srcpos = sg.off + (c + t) * sg.rows + a + skip;
-    }
-    uint32_t wtot;
-    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
-    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
-    const int inpiece = (t < (int)nwin && ex < (uint32_t)S) ? 1 : 0;
-    const uint32_t nf = __syncthreads_count(inpiece);
-    const uint32_t Pn = min((uint32_t)S, wtot);
-    if (t < (int)nf) {
-      const uint32_t flen = min(ex + len, Pn) - ex;
-      fstart[t] = ex;
-      fsrc[t] = srcpos;
-      const uintptr_t ga = reinterpret_cast<uintptr_t>(src + srcpos);
-      const uint32_t mis = (uint32_t)(ga & 15);
-      const uint32_t so = (uint32_t)C::al((ex + C::SLK * t) * EB);
-      fe[t] = (so + mis) / EB;
-      if (flen) {
-        const uint32_t bytes = (mis + flen * EB + 15) & ~15u;
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(reinterpret_cast<unsigned char*>(slot) + so, reinterpret_cast<const void*>(ga - mis), bytes, bar);
-      }
-      if (PAIRS) {
-        const uintptr_t va = reinterpret_cast<uintptr_t>(vsrc + srcpos);
-        const uint32_t vmis = (uint32_t)(va & 15);
-        const uint32_t vso = (uint32_t)C::al((ex + 12 * t) * 4);
-        fve[t] = (vso + vmis) / 4;
-        if (flen) {
-          const uint32_t vbytes = (vmis + flen * 4 + 15) & ~15u;
-          mbar_expect_tx(bar, vbytes);
-          bulk_g2s(reinterpret_cast<unsigned char*>(vslot) + vso, reinterpret_cast<const void*>(va - vmis), vbytes,
-                   bar);
-        }
-      }
-    }
-    if (t == 0) fstart[nf] = Pn;
-    uint32_t nc, no;
-    if (wtot <= (uint32_t)S) {
-      nc = c + nwin;
-      no = 0;
-    } else {
-      __syncthreads();
-      const uint32_t last = nf - 1;
-      const uint32_t used = Pn - fstart[last];
-      const uint32_t* row = rows + uint64_t(c + last) * rstride;
-      const uint32_t base = last == 0 ? o : 0;
-      const uint32_t full = row[bt + 1] - row[bt] - base;
-      if (used < full) {
-        nc = c + last;
-        no = base + used;
-      } else {
-        nc = c + last + 1;
-        no = 0;
-      }
-    }
-    __syncthreads();
-    if (Pn > 0) {
-      if (t == 0) mbar_arrive(bar);
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      // ---- compaction into stream order (one warp per fragment)
-      for (uint32_t f = w; f < nf; f += C::NW) {
-        const uint32_t fs = fstart[f], fl = fstart[f + 1] - fs;
-        const K* fk = slot + fe[f];
-        for (uint32_t i = lane; i < fl; i += 32) {
-          stage[fs + i] = fk[i];
-          if (PAIRS) vstage[fs + i] = vslot[fve[f] + i];
-        }
-      }
-      __syncthreads();
-      // ---- pass 1: stable multisplit ranks within each warp's contiguous range
-      uint32_t* wc = wcnt + w * 32;  // this warp's running count per bucket
-      wc[lane] = 0;
-      __syncwarp();
-      const uint32_t q0 = w * PER_W, q1 = min(Pn, q0 + PER_W);
-      const uint32_t lt = (1u << lane) - 1;
-      for (uint32_t qb = q0; qb < q1; qb += 32) {
-        const uint32_t q = qb + lane;
-        const bool valid = q < q1;
-        const K x = valid ? stage[q] : K(0);
-        uint32_t b = 0;
-#pragma unroll
-        for (int st = 16; st >= 1; st >>= 1)
-          if (thr[b + st - 1].passed(x)) b += st;
-        b = valid ? b : 32u + lane;  // invalid lanes match nobody
-        const uint32_t peers = __match_any_sync(0xffffffffu, b);
-        const uint32_t before = __popc(peers & lt);
-        uint32_t rk = 0;
-        if (valid) rk = wc[b] + before;
-        __syncwarp();
-        if (valid && before == 0) wc[b] += __popc(peers);  // one leader per bucket
-        __syncwarp();
-        if (valid) code[q] = b | (rk << 5);
-      }
-      wsum[w * 32 + lane] = wc[lane];
-      __syncthreads();
-      if (w == 0) {
-        uint32_t tot = 0;
-        for (int ww = 0; ww < C::NW; ww++) {
-          const uint32_t v = wsum[ww * 32 + lane];
-          wsum[ww * 32 + lane] = tot;
-          tot += v;
-        }
-        const uint32_t v = lane < (int)nb ? tot : 0;
-        uint32_t xs = v;
-        for (int q = 1; q < 32; q <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
-          if (lane >= q) xs += y;
-        }
-        poff[lane] = xs - v;
-        if (lane == 31) poff[kTB] = xs;
-        for (int ww = 0; ww < C::NW; ww++) wsum[ww * 32 + lane] += xs - v;
-      }
-      __syncthreads();
-      // ---- pass 2: place every key in the piece image (shifted for the bulk store)
-      const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
-      K* outb = reinterpret_cast<K*>(outraw) + oshift;
-      const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
-      uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
-      const uint32_t* wbase = wsum + w * 32;
-      for (uint32_t q = q0 + lane; q < q1; q += 32) {
-        const uint32_t cd = code[q];
-        const uint32_t dpos = wbase[cd & 31] + (cd >> 5);
-        outb[dpos] = stage[q];
-        if (PAIRS) vout[dpos] = vstage[q];
-      }
-      fence_proxy_async();
-      __syncthreads();
-      {
-        const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
-        const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
-        const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
-        if (a1 > a0) {
-          if (t == 0)
-            bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
-                     (uint32_t)(a1 - a0));
-          const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
-          if (t < (int)nh) dst[oc + t] = outb[t];
-          if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
-        } else {
-          for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
-        }
-        if (PAIRS) {
-          const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
-          const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
-          const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
-          if (c1 > c0) {
-            if (t == 0)
-              bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
-                       (uint32_t)(c1 - c0));
-            const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
-            if (t < (int)nh) vdst[oc + t] = vout[t];
-            if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
-          } else {
-            for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
-          }
-        }
-        if (t == 0) bulk_commit();
-      }
-      const uint32_t pe = ti.piece_base + npc;
-      if (t == 0) pout[pe] = oc;
-      if (t <= kTB) ppre[uint64_t(pe) * kPP + t] = (uint16_t)poff[t];
-      oc += Pn;
-      npc++;
-      if (t == 0) bulk_wait_read0();
-    }
-    c = nc;
-    o = no;
-    __syncthreads();
-  }
-  if (t == 0) {
-    tiles[blockIdx.x].npieces = npc;
-    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-  }
-}
-
 // ------------------------------------------------------------------------------
 // Piece plan: the piece boundaries of every bucket tile depend only on the run
 // lengths (segmat), so a light pre-pass (one CTA per tile) computes them with the
 // same window rule as k_transpose_ms (up to S keys from up to F runs), and the
 // transpose then processes pieces as independent work items (no serial chain per
 // tile, no wave tail).
-struct PieceDesc {
-  uint32_t tile, col, off, nf, pn, out;  // pn == 0: unused slot
+// Self-contained piece descriptor (the transpose needs no other metadata load):
+// fragment f (f < nf) is the run of bucket tile `bt` in column col+f, whose key
+// index is src0 + f*rows + segmat[row0 + f*rstride] (+ off for f = 0).
+struct __align__(16) PieceDesc {
+  uint32_t pn, out, nf, off;         // keys, output offset, runs, offset into the first run
+  uint32_t src0, rows, row0, rstride;  // first column's start; column length; segmat index of (col, bt); row stride
+  uint32_t nb, thr0, slot, bt;       // buckets in the tile, pivot index of its first boundary, piece table slot, tile
 };
+
+constexpr uint32_t kPlanBuf = 256;  // pieces of one tile staged by the plan
 
 template <int NT, int S, int F>
 __global__ void __launch_bounds__(NT)
 k_piece_plan(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const uint32_t* __restrict__ segmat,
-             PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pout) {
+             PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pcount, uint32_t* __restrict__ pout) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t misc[64];
   __shared__ uint32_t fst[F + 1];
+  __shared__ PieceDesc pbuf[kPlanBuf];
   const int t = threadIdx.x;
   const TileInfo ti = tiles[blockIdx.x];
   const LevelSeg sg = segs[ti.seg];
@@ -1241,9 +444,16 @@ k_piece_plan(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, co
       }
     }
     if (Pn > 0) {
-      if (t == 0) {
+      if (t == 0) {  // staged here, appended to the dense list once per tile
         const uint32_t pe = ti.piece_base + npc;
-        pieces[pe] = PieceDesc{blockIdx.x, c, o, nf, Pn, oc};
+        if (npc < kPlanBuf)
+          pbuf[npc] = PieceDesc{Pn, oc, nf, o, sg.off + c * sg.rows, sg.rows,
+                                (uint32_t)(sg.segmat_base + uint64_t(c) * rstride + bt), rstride,
+                                min((uint32_t)kTB, sg.k - bt * kTB), sg.piv_base + bt * kTB, pe, bt};
+        else  // (only for very skewed tiles)
+          pieces[atomicAdd(pcount, 1u)] = PieceDesc{Pn, oc, nf, o, sg.off + c * sg.rows, sg.rows,
+                                                     (uint32_t)(sg.segmat_base + uint64_t(c) * rstride + bt), rstride,
+                                                     min((uint32_t)kTB, sg.k - bt * kTB), sg.piv_base + bt * kTB, pe, bt};
         pout[pe] = oc;
       }
       oc += Pn;
@@ -1253,430 +463,13 @@ k_piece_plan(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, co
     o = no;
     __syncthreads();
   }
-  if (t == 0) tiles[blockIdx.x].npieces = npc;
-}
-
-// SkewTranspose of one piece per iteration (persistent grid over the piece slots);
-// per piece exactly the work of k_transpose_ms.
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_pc(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-               const PieceDesc* __restrict__ pieces, uint32_t npslots, const K* __restrict__ src,
-               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
-  using C = MsCfg<K, PAIRS, NT, S, F>;
-  static_assert(F <= NT && F % 32 == 0 && S <= 65535 && S % (32 * (NT / 32)) == 0, "shape");
-  constexpr int EB = sizeof(K);
-  extern __shared__ __align__(128) unsigned char sm[];
-  K* slot = reinterpret_cast<K*>(sm + C::off_slot);
-  uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot);
-  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
-  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
-  uint32_t* code = reinterpret_cast<uint32_t*>(sm + C::off_code);
-  unsigned char* outraw = sm + C::off_out;
-  unsigned char* voutraw = sm + C::off_vout;
-  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
-  uint32_t* fsrc = fstart + F + 1;
-  uint32_t* fe = fsrc + F;
-  uint32_t* fve = fe + F;
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(sm + C::off_wcnt);
-  uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + C::off_wsum);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  uint32_t* poff = misc + 64;
-  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::off_bar);
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  constexpr uint32_t PER_W = S / (NT / 32);
+  __shared__ uint32_t base;
   if (t == 0) {
-    mbar_init(bar, 1);
-    fence_proxy_async();
+    tiles[blockIdx.x].npieces = npc;
+    base = atomicAdd(pcount, min(npc, kPlanBuf));
   }
   __syncthreads();
-  uint32_t phase = 0;
-  for (uint32_t ps = blockIdx.x; ps < npslots; ps += gridDim.x) {
-    const PieceDesc pd = pieces[ps];
-    if (pd.pn == 0) continue;  // uniform across the CTA
-    const TileInfo ti = tiles[pd.tile];
-    const LevelSeg sg = segs[ti.seg];
-    const uint32_t bt = ti.bt;
-    const uint32_t b0 = bt * kTB;
-    const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
-    const uint32_t Pn = pd.pn, nf = pd.nf, oc = pd.out;
-    if (t < 32) {
-      const K* P = piv + sg.piv_base;
-      const uint32_t j = b0 + 1 + t;
-      const bool real = t < (int)nb - 1;
-      const K pj = real ? P[j - 1] : K(0);
-      const bool dup = real && j >= 2 && P[j - 2] == pj;
-      thr[t] = Thr<K>::make(pj, dup, !real);
-    }
-    // ---- fragments: runs of columns col .. col+nf-1 (the first starts at `off`)
-    uint32_t len = 0, srcpos = 0;
-    if (t < (int)nf) {
-      const uint32_t cc = pd.col + t;
-      const uint32_t* row = segmat + sg.segmat_base + uint64_t(cc) * (sg.nbt + 1);
-      const uint32_t a = row[bt] + (t == 0 ? pd.off : 0), e = row[bt + 1];
-      len = e - a;
-      srcpos = sg.off + cc * sg.rows + a;
-    }
-    uint32_t wtot;
-    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
-    if (t < (int)nf) {
-      const uint32_t flen = min(ex + len, Pn) - ex;
-      fstart[t] = ex;
-      const uintptr_t ga = reinterpret_cast<uintptr_t>(src + srcpos);
-      const uint32_t mis = (uint32_t)(ga & 15);
-      const uint32_t so = (uint32_t)C::al((ex + C::SLK * t) * EB);
-      fe[t] = (so + mis) / EB;
-      if (flen) {
-        const uint32_t bytes = (mis + flen * EB + 15) & ~15u;
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(reinterpret_cast<unsigned char*>(slot) + so, reinterpret_cast<const void*>(ga - mis), bytes, bar);
-      }
-      if (PAIRS) {
-        const uintptr_t va = reinterpret_cast<uintptr_t>(vsrc + srcpos);
-        const uint32_t vmis = (uint32_t)(va & 15);
-        const uint32_t vso = (uint32_t)C::al((ex + 12 * t) * 4);
-        fve[t] = (vso + vmis) / 4;
-        if (flen) {
-          const uint32_t vbytes = (vmis + flen * 4 + 15) & ~15u;
-          mbar_expect_tx(bar, vbytes);
-          bulk_g2s(reinterpret_cast<unsigned char*>(vslot) + vso, reinterpret_cast<const void*>(va - vmis), vbytes,
-                   bar);
-        }
-      }
-    }
-    if (t == 0) fstart[nf] = Pn;
-    __syncthreads();
-    if (t == 0) mbar_arrive(bar);
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    // ---- compaction into stream order
-    for (uint32_t f = w; f < nf; f += C::NW) {
-      const uint32_t fs = fstart[f], fl = fstart[f + 1] - fs;
-      const K* fk = slot + fe[f];
-      for (uint32_t i = lane; i < fl; i += 32) {
-        stage[fs + i] = fk[i];
-        if (PAIRS) vstage[fs + i] = vslot[fve[f] + i];
-      }
-    }
-    __syncthreads();
-    // ---- pass 1: stable multisplit ranks (ballots) in each warp's contiguous range
-    uint32_t run = 0;
-    const uint32_t q0 = w * PER_W, q1 = min(Pn, q0 + PER_W);
-    for (uint32_t qb = q0; qb < q1; qb += 32) {
-      const uint32_t q = qb + lane;
-      const bool valid = q < q1;
-      const K x = valid ? stage[q] : K(0);
-      uint32_t b = 0;
-#pragma unroll
-      for (int st = 16; st >= 1; st >>= 1)
-        if (thr[b + st - 1].passed(x)) b += st;
-      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-      uint32_t peers = vm, mine = vm;
-#pragma unroll
-      for (int k = 0; k < 5; k++) {
-        const uint32_t bk = __ballot_sync(0xffffffffu, (b >> k) & 1);
-        peers &= ((b >> k) & 1) ? bk : ~bk;
-        mine &= ((lane >> k) & 1) ? bk : ~bk;
-      }
-      const uint32_t rk = __shfl_sync(0xffffffffu, run, b) + __popc(peers & ((1u << lane) - 1));
-      if (valid) code[q] = b | (rk << 5);
-      run += __popc(mine);
-    }
-    wsum[w * 32 + lane] = run;
-    __syncthreads();
-    if (w == 0) {
-      uint32_t tot = 0;
-      for (int ww = 0; ww < C::NW; ww++) {
-        const uint32_t v = wsum[ww * 32 + lane];
-        wsum[ww * 32 + lane] = tot;
-        tot += v;
-      }
-      const uint32_t v = lane < (int)nb ? tot : 0;
-      uint32_t xs = v;
-      for (int q = 1; q < 32; q <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, xs, q);
-        if (lane >= q) xs += y;
-      }
-      poff[lane] = xs - v;
-      if (lane == 31) poff[kTB] = xs;
-      for (int ww = 0; ww < C::NW; ww++) wsum[ww * 32 + lane] += xs - v;
-      if (lane == 0) bulk_wait_read0();  // the previous piece's image has been read out
-    }
-    __syncthreads();
-    // ---- pass 2: every key to its place in the piece image
-    const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
-    K* outb = reinterpret_cast<K*>(outraw) + oshift;
-    const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
-    uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
-    const uint32_t* wbase = wsum + w * 32;
-    for (uint32_t q = q0 + lane; q < q1; q += 32) {
-      const uint32_t cd = code[q];
-      const uint32_t dpos = wbase[cd & 31] + (cd >> 5);
-      outb[dpos] = stage[q];
-      if (PAIRS) vout[dpos] = vstage[q];
-    }
-    fence_proxy_async();
-    __syncthreads();
-    {
-      const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
-      const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
-      const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
-      if (a1 > a0) {
-        if (t == 0)
-          bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
-                   (uint32_t)(a1 - a0));
-        const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
-        if (t < (int)nh) dst[oc + t] = outb[t];
-        if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
-      } else {
-        for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
-      }
-      if (PAIRS) {
-        const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
-        const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
-        const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
-        if (c1 > c0) {
-          if (t == 0)
-            bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
-                     (uint32_t)(c1 - c0));
-          const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
-          if (t < (int)nh) vdst[oc + t] = vout[t];
-          if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
-        } else {
-          for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
-        }
-      }
-      if (t == 0) bulk_commit();
-    }
-    if (t <= kTB) ppre[uint64_t(ps) * kPP + t] = (uint16_t)poff[t];
-    __syncthreads();
-  }
-  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-}
-
-// ------------------------------------------------------------------------------
-// SkewTranspose of one piece per iteration with counter-based ranking (the sort
-// path's transpose).  Per piece:
-//  * every key is fetched with cp.async straight to its stream position (padded
-//    layout: one pad word per 32 keeps the blocked accesses conflict-free);
-//  * thread t owns K = S/NT consecutive stream keys: their buckets come from a
-//    walk over the tile's thresholds (keys of a run are sorted, so a key usually
-//    needs one or two comparisons; a new run restarts with a 5-step search), and
-//    a thread-private counter per bucket gives each key's rank among the
-//    thread's keys of its bucket;
-//  * an exclusive scan of the counters in bucket-major, thread-minor order is the
-//    stable bucket-major position of every key (column order, then row order);
-//  * the piece image goes out with one bulk store; its bucket prefix goes to the
-//    piece tables.
-template <typename K, bool PAIRS, int NT, int S, int F>
-struct RkCfg {
-  static constexpr int NW = NT / 32;
-  static constexpr int KT = S / NT;  // keys per thread
-  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  static constexpr int PADK = 128 / (int)sizeof(K);
-  static constexpr size_t off_stage = 0;  // S keys + pads
-  static constexpr size_t off_vstage = al((S + S / PADK + 1) * sizeof(K));
-  static constexpr size_t off_cnt = off_vstage + (PAIRS ? al((S + S / 32 + 1) * 4) : 0);  // 32 x NT u16
-  static constexpr size_t off_out = off_cnt + al(32 * NT * 2);
-  static constexpr size_t off_vout = off_out + al((S + 16 / sizeof(K) + 4) * sizeof(K));
-  static constexpr size_t off_frag = off_vout + (PAIRS ? al((S + 8) * 4) : 0);  // fstart[F+1], fsrc[F]
-  static constexpr size_t off_misc = al(off_frag + (2 * F + 1) * 4);
-  static constexpr size_t off_thr = al(off_misc + (64 + 33) * 4);
-  static constexpr size_t SMEM = al(off_thr + 32 * 16 + 32 * 4);
-  __device__ __forceinline__ static uint32_t pk(uint32_t i) { return i + i / PADK; }
-  __device__ __forceinline__ static uint32_t pw(uint32_t i) { return i + (i >> 5); }
-};
-
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_rk(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-               const PieceDesc* __restrict__ pieces, uint32_t npslots, const K* __restrict__ src,
-               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
-  using C = RkCfg<K, PAIRS, NT, S, F>;
-  constexpr int KT = C::KT;
-  static_assert(F <= NT && S % NT == 0 && KT <= 16 && S <= 65535, "shape");
-  constexpr int EB = sizeof(K);
-  extern __shared__ __align__(128) unsigned char sm[];
-  K* stage = reinterpret_cast<K*>(sm + C::off_stage);
-  uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(sm + C::off_cnt);  // [bucket][thread]
-  uint32_t* cnt32 = reinterpret_cast<uint32_t*>(sm + C::off_cnt);
-  unsigned char* outraw = sm + C::off_out;
-  unsigned char* voutraw = sm + C::off_vout;
-  uint32_t* fstart = reinterpret_cast<uint32_t*>(sm + C::off_frag);
-  uint32_t* fsrc = fstart + F + 1;
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  uint32_t* poff = misc + 64;
-  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr);
-  uint32_t* thr32 = reinterpret_cast<uint32_t*>(sm + C::off_thr + 32 * 16);
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-
-  for (uint32_t ps = blockIdx.x; ps < npslots; ps += gridDim.x) {
-    const PieceDesc pd = pieces[ps];
-    if (pd.pn == 0) continue;  // uniform across the CTA
-    const TileInfo ti = tiles[pd.tile];
-    const LevelSeg sg = segs[ti.seg];
-    const uint32_t bt = ti.bt;
-    const uint32_t b0 = bt * kTB;
-    const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
-    const uint32_t Pn = pd.pn, nf = pd.nf, oc = pd.out;
-    if (t < 32) {
-      const K* P = piv + sg.piv_base;
-      const uint32_t j = b0 + 1 + t;
-      const bool real = t < (int)nb - 1;
-      const K pj = real ? P[j - 1] : K(0);
-      const bool dup = real && j >= 2 && P[j - 2] == pj;
-      thr[t] = Thr<K>::make(pj, dup, !real);
-      if constexpr (sizeof(K) == 4) {
-        // 32-bit form: passed(x) == (x >= thr32) for every key except 0xffffffff,
-        // whose bucket is the number of real thresholds at most 0xffffffff
-        const uint64_t t64 = real ? uint64_t(pj) + (dup ? 1u : 0u) : (1ull << 32);
-        thr32[t] = t64 > 0xffffffffull ? 0xffffffffu : (uint32_t)t64;
-        const uint32_t cntmax = __popc(__ballot_sync(0xffffffffu, t64 <= 0xffffffffull));
-        if (t == 0) misc[60] = cntmax;
-      }
-    }
-    for (int i = t; i < 32 * NT / 2; i += NT) cnt32[i] = 0;
-    // ---- fragments of the piece, prefix-summed
-    uint32_t len = 0, srcpos = 0;
-    if (t < (int)nf) {
-      const uint32_t cc = pd.col + t;
-      const uint32_t* row = segmat + sg.segmat_base + uint64_t(cc) * (sg.nbt + 1);
-      const uint32_t a = row[bt] + (t == 0 ? pd.off : 0), e = row[bt + 1];
-      len = e - a;
-      srcpos = sg.off + cc * sg.rows + a;
-    }
-    uint32_t wtot;
-    const uint32_t ex = block_excl_sum<C::NW>(len, misc, &wtot);
-    if (t < (int)nf) {
-      fstart[t] = ex;
-      fsrc[t] = srcpos - ex;  // global index of stream position 0 of this fragment's frame
-    }
-    if (t == 0) fstart[nf] = Pn;
-    __syncthreads();
-    // ---- load: one warp per fragment, cp.async to the padded stream positions
-    for (uint32_t f = w; f < nf; f += C::NW) {
-      const uint32_t fs = fstart[f], fe2 = fstart[f + 1];
-      const K* g = src + fsrc[f];
-      const uint32_t* gv = PAIRS ? vsrc + fsrc[f] : nullptr;
-      for (uint32_t q = fs + lane; q < fe2; q += 32) {
-        cp_async_elem(&stage[C::pk(q)], &g[q]);
-        if (PAIRS) cp_async_elem(&vstage[C::pw(q)], &gv[q]);
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    // ---- pass 1: buckets (threshold walk) and thread-private counters
-    const uint32_t q0 = t * KT;
-    K xs[KT];
-    uint32_t code[KT];  // bucket | local rank << 8
-    {
-      const uint32_t bmax = sizeof(K) == 4 ? misc[60] : 0u;
-#pragma unroll
-      for (int j = 0; j < KT; j++) {
-        const uint32_t q = q0 + j;
-        const bool valid = q < Pn;
-        const K x = valid ? stage[C::pk(q)] : K(0);
-        xs[j] = x;
-        uint32_t b = 0;  // branch-free 5-step search: number of thresholds passed
-        if constexpr (sizeof(K) == 4) {
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) b += (uint32_t(x) >= thr32[b + st - 1]) ? st : 0;
-          b = uint32_t(x) == 0xffffffffu ? bmax : b;
-        } else {
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) b += thr[b + st - 1].passed(x) ? st : 0;
-        }
-        if (valid) {
-          uint16_t* cp = &cnt[b * NT + t];
-          const uint32_t lr = *cp;
-          *cp = (uint16_t)(lr + 1);
-          code[j] = b | (lr << 8);
-        } else {
-          code[j] = 0xffffffffu;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- exclusive scan of the counters, bucket-major (u16 pairs: entries 2i, 2i+1)
-    {
-      constexpr int PER = 32 * NT / 2 / NT;  // u32 words per thread = 16
-      uint32_t v[PER];
-      uint32_t sum = 0;
-#pragma unroll
-      for (int i = 0; i < PER; i++) {
-        v[i] = cnt32[t * PER + i];
-        sum += (v[i] & 0xffffu) + (v[i] >> 16);
-      }
-      uint32_t tot;
-      uint32_t run = block_excl_sum<C::NW>(sum, misc, &tot);
-#pragma unroll
-      for (int i = 0; i < PER; i++) {
-        const uint32_t lo = v[i] & 0xffffu, hi = v[i] >> 16;
-        cnt32[t * PER + i] = run | ((run + lo) << 16);
-        run += lo + hi;
-      }
-    }
-    __syncthreads();
-    if (t < 32) poff[t] = t < (int)nb ? cnt[t * NT] : Pn;
-    if (t == 32) poff[kTB] = Pn;
-    // ---- pass 2: scatter into the piece image (shifted for the bulk store)
-    if (t == 0) bulk_wait_read0();  // previous piece's image has been read out
-    __syncthreads();
-    const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
-    K* outb = reinterpret_cast<K*>(outraw) + oshift;
-    const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
-    uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
-#pragma unroll
-    for (int j = 0; j < KT; j++) {
-      const uint32_t cd = code[j];
-      if (cd != 0xffffffffu) {
-        const uint32_t b = cd & 0xff;
-        const uint32_t dpos = cnt[b * NT + t] + (cd >> 8);
-        outb[dpos] = xs[j];
-        if (PAIRS) vout[dpos] = vstage[C::pw(q0 + j)];
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    {
-      const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
-      const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
-      const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
-      if (a1 > a0) {
-        if (t == 0)
-          bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
-                   (uint32_t)(a1 - a0));
-        const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
-        if (t < (int)nh) dst[oc + t] = outb[t];
-        if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
-      } else {
-        for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
-      }
-      if (PAIRS) {
-        const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
-        const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
-        const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
-        if (c1 > c0) {
-          if (t == 0)
-            bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
-                     (uint32_t)(c1 - c0));
-          const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
-          if (t < (int)nh) vdst[oc + t] = vout[t];
-          if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
-        } else {
-          for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
-        }
-      }
-      if (t == 0) bulk_commit();
-    }
-    if (t <= kTB) ppre[uint64_t(ps) * kPP + t] = (uint16_t)poff[t];
-    __syncthreads();
-  }
-  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  for (uint32_t q = t; q < min(npc, kPlanBuf); q += NT) pieces[base + q] = pbuf[q];
 }
 
 // ------------------------------------------------------------------------------

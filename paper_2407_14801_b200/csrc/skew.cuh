@@ -28,289 +28,8 @@
 
 namespace sq {
 
-template <typename K, bool PAIRS, int NT, int S, int F>
-struct MxCfg {
-  static constexpr int NW = NT / 32;
-  static constexpr int EB = sizeof(K);
-  // slot words: every run rounds up to whole 16-byte units around its misalignment
-  static constexpr int SLOTW = S + F * (2 * (16 / EB) - 2) + 16 / EB;
-  static constexpr int NCH = (SLOTW + 31) / 32;     // 32-word chunks
-  static constexpr int CPW = (NCH + NW - 1) / NW;   // chunks per warp
-  __host__ __device__ static constexpr size_t al(size_t x) { return (x + 127) & ~size_t(127); }
-  // double-buffered: slots, value slots, bitmap, thresholds, piece metadata
-  static constexpr size_t SLOT_B = al(size_t(NCH) * 32 * EB);
-  static constexpr size_t VSLOT_B = PAIRS ? al(size_t(NCH) * 32 * 4) : 0;
-  static constexpr size_t BITS_B = al(NCH * 4);
-  static constexpr size_t THR_B = al(32 * 16 + 32 * 4 + 16 * 4);  // Thr<K>[32], thr32[32], meta[16]
-  static constexpr size_t off_slot = 0;
-  static constexpr size_t off_vslot = off_slot + 2 * SLOT_B;
-  static constexpr size_t off_bits = off_vslot + 2 * VSLOT_B;
-  static constexpr size_t off_thr = off_bits + 2 * BITS_B;
-  static constexpr size_t off_out = off_thr + 2 * THR_B;                         // S keys + shift
-  static constexpr size_t off_vout = off_out + al((S + 16 / EB) * EB);
-  static constexpr size_t off_cnt = off_vout + (PAIRS ? al((S + 4) * 4) : 0);     // NCH x 32 u32
-  static constexpr size_t off_misc = off_cnt + al(size_t(NCH) * 32 * 4);
-  static constexpr size_t off_gs = off_misc + al(128 * 4);                        // NW x 32 group sums
-  static constexpr size_t SMEM = off_gs + al(NW * 32 * 4);
-};
-
 // Meta slots of a staged piece.
 enum { kMxPiece = 0, kMxNch, kMxPn, kMxOut, kMxNb, kMxBmax, kMxValid };
-
-// Stage the first non-empty piece at or after `ps` into buffer `b`: fragment
-// table, bitmap, thresholds, async copies (one commit group).  Returns the piece
-// slot staged (npslots if none).
-template <typename K, bool PAIRS, int NT, int S, int F>
-__device__ __forceinline__ uint32_t mx_stage(uint32_t ps, uint32_t npslots, int b, unsigned char* sm,
-                                             const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-                                             const PieceDesc* __restrict__ pieces, const K* __restrict__ src,
-                                             const uint32_t* __restrict__ vsrc, const K* __restrict__ piv,
-                                             const uint32_t* __restrict__ segmat) {
-  using C = MxCfg<K, PAIRS, NT, S, F>;
-  constexpr int EB = sizeof(K), NW = C::NW;
-  const int t = threadIdx.x;
-  while (ps < npslots && pieces[ps].pn == 0) ps += gridDim.x;  // uniform across the CTA
-  uint32_t* meta = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16 + 32 * 4);
-  if (ps >= npslots) {
-    if (t == 0) meta[kMxValid] = 0;
-    asm volatile("cp.async.commit_group;\n" ::: "memory");  // empty group: wait_group counts stay aligned
-    return npslots;
-  }
-  K* slot = reinterpret_cast<K*>(sm + C::off_slot + b * C::SLOT_B);
-  uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot + b * C::VSLOT_B);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(sm + C::off_bits + b * C::BITS_B);
-  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr + b * C::THR_B);
-  uint32_t* thr32 = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  const PieceDesc pd = pieces[ps];
-  const TileInfo ti = tiles[pd.tile];
-  const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt, b0 = bt * kTB;
-  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
-  const uint32_t Pn = pd.pn, nf = pd.nf;
-  if (t < 32) {
-    const K* P = piv + sg.piv_base;
-    const uint32_t j = b0 + 1 + t;
-    const bool real = t < (int)nb - 1;
-    const K pj = real ? P[j - 1] : K(0);
-    const bool dup = real && j >= 2 && P[j - 2] == pj;
-    thr[t] = Thr<K>::make(pj, dup, !real);
-    uint32_t cntmax = 0;
-    if constexpr (sizeof(K) == 4) {
-      // passed(x) == (x >= thr32) for every key except 0xffffffff, whose bucket is
-      // the number of real thresholds that are at most 0xffffffff
-      const uint64_t t64 = real ? uint64_t(pj) + (dup ? 1u : 0u) : (1ull << 32);
-      thr32[t] = t64 > 0xffffffffull ? 0xffffffffu : (uint32_t)t64;
-      cntmax = __popc(__ballot_sync(0xffffffffu, t64 <= 0xffffffffull));
-    }
-    if (t == 0) {
-      meta[kMxPiece] = ps;
-      meta[kMxPn] = Pn;
-      meta[kMxOut] = pd.out;
-      meta[kMxNb] = nb;
-      meta[kMxBmax] = cntmax;
-      meta[kMxValid] = 1;
-    }
-  }
-  // fragments: runs of columns col .. col+nf-1 (the first starts at `off`), clipped
-  // to the piece; packed 16-byte aligned slots
-  uint32_t len = 0, srcpos = 0, mis = 0, sbytes = 0;
-  if (t < (int)nf) {
-    const uint32_t cc = pd.col + t;
-    const uint32_t* row = segmat + sg.segmat_base + uint64_t(cc) * (sg.nbt + 1);
-    const uint32_t a = row[bt] + (t == 0 ? pd.off : 0), e = row[bt + 1];
-    len = e - a;
-    srcpos = sg.off + cc * sg.rows + a;
-  }
-  uint32_t wtot;
-  const uint32_t ex = block_excl_sum<NW>(len, misc, &wtot);
-  const uint32_t flen = t < (int)nf ? min(ex + len, Pn) - min(ex, Pn) : 0;
-  if (flen) {
-    mis = (uint32_t)(reinterpret_cast<uintptr_t>(src + srcpos) & 15);
-    sbytes = (mis + flen * EB + 15) & ~15u;
-  }
-  uint32_t stot;
-  const uint32_t so = block_excl_sum<NW>(sbytes, misc + 32, &stot);  // slot byte offset
-  const uint32_t nch = (stot / EB + 31) / 32;
-  for (uint32_t i = t; i < nch; i += NT) bits[i] = 0;
-  if (t == 0) meta[kMxNch] = nch;
-  __syncthreads();
-  if (flen) {
-    const uint32_t e0 = (so + mis) / EB, e1 = e0 + flen;  // word range of the run's keys
-    for (uint32_t wd = e0 >> 5; wd <= (e1 - 1) >> 5; wd++) {
-      const uint32_t lo = max(e0, wd * 32) - wd * 32, hi = min(e1, wd * 32 + 32) - wd * 32;
-      const uint32_t m = (hi == 32 ? 0xffffffffu : ((1u << hi) - 1)) & ~((1u << lo) - 1);
-      atomicOr(&bits[wd], m);
-    }
-    const uint32_t sdst = smem_addr(slot) + so;
-    const unsigned char* g = reinterpret_cast<const unsigned char*>(src + srcpos) - mis;
-    for (uint32_t v = 0; v < sbytes; v += 16)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
-    if (PAIRS) {  // values at the same word index (per-element async copies)
-      const uint32_t* gv = vsrc + srcpos;
-      for (uint32_t k = 0; k < flen; k++) cp_async_elem(&vslot[e0 + k], &gv[k]);
-    }
-  }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  return ps;
-}
-
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_mx(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-               const PieceDesc* __restrict__ pieces, uint32_t npslots, const K* __restrict__ src,
-               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
-  using C = MxCfg<K, PAIRS, NT, S, F>;
-  constexpr int EB = sizeof(K);
-  constexpr int NW = C::NW, CPW = C::CPW;
-  static_assert(F <= NT && NT % 32 == 0 && S <= 65535 && kTB == 32, "shape");
-  extern __shared__ __align__(128) unsigned char sm[];
-  unsigned char* outraw = sm + C::off_out;
-  unsigned char* voutraw = sm + C::off_vout;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + C::off_cnt);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  uint32_t* poff = misc + 64;
-  uint32_t* gs = reinterpret_cast<uint32_t*>(sm + C::off_gs);
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1;
-
-  int b = 0;
-  uint32_t ps = mx_stage<K, PAIRS, NT, S, F>(blockIdx.x, npslots, 0, sm, segs, tiles, pieces, src, vsrc, piv, segmat);
-  while (ps < npslots) {
-    // stage the next piece into the other buffer while this one is processed
-    const uint32_t nps = mx_stage<K, PAIRS, NT, S, F>(ps + gridDim.x, npslots, b ^ 1, sm, segs, tiles, pieces, src,
-                                                      vsrc, piv, segmat);
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    __syncthreads();
-    const K* slot = reinterpret_cast<const K*>(sm + C::off_slot + b * C::SLOT_B);
-    const uint32_t* vslot = reinterpret_cast<const uint32_t*>(sm + C::off_vslot + b * C::VSLOT_B);
-    const uint32_t* bits = reinterpret_cast<const uint32_t*>(sm + C::off_bits + b * C::BITS_B);
-    const Thr<K>* thr = reinterpret_cast<const Thr<K>*>(sm + C::off_thr + b * C::THR_B);
-    const uint32_t* thr32 = reinterpret_cast<const uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
-    const uint32_t* meta = thr32 + 32;
-    const uint32_t nch = meta[kMxNch], Pn = meta[kMxPn], oc = meta[kMxOut], bmax = meta[kMxBmax];
-    const uint32_t thr_r = sizeof(K) == 4 ? thr32[lane] : 0u;
-    // ---- pass 1: buckets and in-chunk ranks; count rows
-    K xs[CPW];
-    uint32_t code[CPW];  // bucket | rank << 5 | invalid << 15
-#pragma unroll
-    for (int k = 0; k < CPW; k++) {
-      const uint32_t c = w + k * NW;
-      code[k] = 1u << 15;
-      if (c < nch) {
-        const bool v = (bits[c] >> lane) & 1;
-        const K x = slot[c * 32 + lane];
-        xs[k] = x;
-        uint32_t bk = 0;
-        if constexpr (sizeof(K) == 4) {
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1)
-            bk += (uint32_t(x) >= __shfl_sync(0xffffffffu, thr_r, bk + st - 1)) ? st : 0;
-          bk = uint32_t(x) == 0xffffffffu ? bmax : bk;
-        } else {
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) bk += thr[bk + st - 1].passed(x) ? st : 0;
-        }
-        const uint32_t grp = __match_any_sync(0xffffffffu, v ? bk : 32u + lane);
-        const uint32_t rk = __popc(grp & lt_mask);
-        cnt[c * 32 + lane] = 0;
-        __syncwarp();
-        if (v && rk == 0) cnt[c * 32 + bk] = __popc(grp);
-        code[k] = v ? (bk | (rk << 5)) : (1u << 15);
-      }
-    }
-    __syncthreads();
-    // ---- scan: per bucket (lane) down the chunks; warp w owns chunks [w*CG, (w+1)*CG)
-    {
-      const uint32_t CG = (nch + NW - 1) / NW;
-      const uint32_t c0 = w * CG, c1 = min(nch, c0 + CG);
-      uint32_t sum = 0;
-      for (uint32_t c = c0; c < c1; c++) sum += cnt[c * 32 + lane];
-      gs[w * 32 + lane] = sum;
-      __syncthreads();
-      if (w == 0) {
-        uint32_t tot = 0;
-        for (int ww = 0; ww < NW; ww++) {
-          const uint32_t v = gs[ww * 32 + lane];
-          gs[ww * 32 + lane] = tot;
-          tot += v;
-        }
-        uint32_t xsum = tot;
-        for (int q = 1; q < 32; q <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, xsum, q);
-          if (lane >= q) xsum += y;
-        }
-        const uint32_t boff = xsum - tot;
-        poff[lane] = boff;
-        if (lane == 31) poff[kTB] = xsum;
-        for (int ww = 0; ww < NW; ww++) gs[ww * 32 + lane] += boff;
-        if (lane == 0) bulk_wait_read0();  // the previous piece's image has been read out
-      }
-      __syncthreads();
-      uint32_t run = gs[w * 32 + lane];
-      for (uint32_t c = c0; c < c1; c++) {
-        const uint32_t v = cnt[c * 32 + lane];
-        cnt[c * 32 + lane] = run;
-        run += v;
-      }
-      __syncthreads();
-    }
-    // ---- pass 2: scatter into the piece image (shifted for the bulk store)
-    const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
-    K* outb = reinterpret_cast<K*>(outraw) + oshift;
-    const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
-    uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
-#pragma unroll
-    for (int k = 0; k < CPW; k++) {
-      const uint32_t c = w + k * NW;
-      if (!(code[k] >> 15)) {
-        const uint32_t dpos = cnt[c * 32 + (code[k] & 31)] + (code[k] >> 5);
-        outb[dpos] = xs[k];
-        if (PAIRS) vout[dpos] = vslot[c * 32 + lane];
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    {
-      const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
-      const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
-      const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
-      if (a1 > a0) {
-        if (t == 0)
-          bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
-                   (uint32_t)(a1 - a0));
-        const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
-        if (t < (int)nh) dst[oc + t] = outb[t];
-        if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
-      } else {
-        for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
-      }
-      if (PAIRS) {
-        const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
-        const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
-        const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
-        if (c1 > c0) {
-          if (t == 0)
-            bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
-                     (uint32_t)(c1 - c0));
-          const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
-          if (t < (int)nh) vdst[oc + t] = vout[t];
-          if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
-        } else {
-          for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
-        }
-      }
-      if (t == 0) bulk_commit();
-    }
-    if (t <= kTB) ppre[uint64_t(ps) * kPP + t] = (uint16_t)poff[t];
-    __syncthreads();
-    ps = nps;
-    b ^= 1;
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-}
 
 // ------------------------------------------------------------------------------
 // The same SkewTranspose with per-thread counters (the sort path's transpose):
@@ -323,6 +42,7 @@ k_transpose_mx(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
 // group its first image position.  Pass 2 scatters the keys into the image.
 template <typename K, bool PAIRS, int NT, int S, int F>
 struct CtCfg {
+  static constexpr int NB = 2;  // staging buffers (2: the next piece is staged during this one)
   static constexpr int NW = NT / 32;
   static constexpr int EB = sizeof(K);
   static constexpr int VW = 16 / EB;  // words per 16-byte vector
@@ -337,10 +57,10 @@ struct CtCfg {
   static constexpr size_t BITS_B = al((WORDS / 32 + 2) * 4);
   static constexpr size_t THR_B = al(32 * 16 + 32 * 4 + 16 * 4);  // Thr<K>[32], thr32[32], meta[16]
   static constexpr size_t off_slot = 0;
-  static constexpr size_t off_vslot = off_slot + 2 * SLOT_B;
-  static constexpr size_t off_bits = off_vslot + 2 * VSLOT_B;
-  static constexpr size_t off_thr = off_bits + 2 * BITS_B;
-  static constexpr size_t off_out = off_thr + 2 * THR_B;  // S keys + shift
+  static constexpr size_t off_vslot = off_slot + NB * SLOT_B;
+  static constexpr size_t off_bits = off_vslot + NB * VSLOT_B;
+  static constexpr size_t off_thr = off_bits + NB * BITS_B;
+  static constexpr size_t off_out = off_thr + NB * THR_B;  // S keys + shift
   static constexpr size_t off_vout = off_out + al((S + 16 / EB) * EB);
   static constexpr size_t off_cnt = off_vout + (PAIRS ? al((S + 4) * 4) : 0);  // 33 x NT u32
   static constexpr size_t off_misc = off_cnt + al(33 * NT * 4);
@@ -353,19 +73,16 @@ struct CtCfg {
 __device__ __forceinline__ uint32_t cswz(uint32_t e) { return e ^ (((e >> 5) & 7) << 2); }
 
 template <typename K, bool PAIRS, int NT, int S, int F>
-__device__ __forceinline__ uint32_t ct_stage(uint32_t ps, uint32_t npslots, int b, unsigned char* sm,
-                                             const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-                                             const PieceDesc* __restrict__ pieces, const K* __restrict__ src,
-                                             const uint32_t* __restrict__ vsrc, const K* __restrict__ piv,
-                                             const uint32_t* __restrict__ segmat) {
+__device__ __forceinline__ void ct_stage(const PieceDesc& pd, bool valid, int b, unsigned char* sm,
+                                         const K* __restrict__ src, const uint32_t* __restrict__ vsrc,
+                                         const K* __restrict__ piv, const uint32_t* __restrict__ segmat) {
   using C = CtCfg<K, PAIRS, NT, S, F>;
   constexpr int EB = sizeof(K), NW = C::NW;
   const int t = threadIdx.x;
-  while (ps < npslots && pieces[ps].pn == 0) ps += gridDim.x;  // uniform across the CTA
   uint32_t* meta = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16 + 32 * 4);
-  if (ps >= npslots) {
+  if (!valid) {
     asm volatile("cp.async.commit_group;\n" ::: "memory");  // empty group: wait_group counts stay aligned
-    return npslots;
+    return;
   }
   K* slot = reinterpret_cast<K*>(sm + C::off_slot + b * C::SLOT_B);
   uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot + b * C::VSLOT_B);
@@ -373,18 +90,13 @@ __device__ __forceinline__ uint32_t ct_stage(uint32_t ps, uint32_t npslots, int 
   Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr + b * C::THR_B);
   uint32_t* thr32 = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
   uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  const PieceDesc pd = pieces[ps];
-  const TileInfo ti = tiles[pd.tile];
-  const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt, b0 = bt * kTB;
-  const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
+  const uint32_t nb = pd.nb;
   const uint32_t Pn = pd.pn, nf = pd.nf;
   if (t < 32) {
-    const K* P = piv + sg.piv_base;
-    const uint32_t j = b0 + 1 + t;
+    const K* P = piv + pd.thr0;  // boundary j = first+1+t uses pivot P[t], dup if P[t-1] == P[t]
     const bool real = t < (int)nb - 1;
-    const K pj = real ? P[j - 1] : K(0);
-    const bool dup = real && j >= 2 && P[j - 2] == pj;
+    const K pj = real ? P[t] : K(0);
+    const bool dup = real && pd.bt * kTB + t >= 1 && P[t - 1] == pj;
     thr[t] = Thr<K>::make(pj, dup, !real);
     uint32_t cntmax = 0;
     if constexpr (sizeof(K) == 4) {
@@ -395,7 +107,7 @@ __device__ __forceinline__ uint32_t ct_stage(uint32_t ps, uint32_t npslots, int 
       cntmax = __popc(__ballot_sync(0xffffffffu, t64 <= 0xffffffffull));
     }
     if (t == 0) {
-      meta[kMxPiece] = ps;
+      meta[kMxPiece] = pd.slot;
       meta[kMxPn] = Pn;
       meta[kMxOut] = pd.out;
       meta[kMxNb] = nb;
@@ -406,11 +118,10 @@ __device__ __forceinline__ uint32_t ct_stage(uint32_t ps, uint32_t npslots, int 
   // to the piece; packed 16-byte aligned slots
   uint32_t len = 0, srcpos = 0, mis = 0, sbytes = 0;
   if (t < (int)nf) {
-    const uint32_t cc = pd.col + t;
-    const uint32_t* row = segmat + sg.segmat_base + uint64_t(cc) * (sg.nbt + 1);
-    const uint32_t a = row[bt] + (t == 0 ? pd.off : 0), e = row[bt + 1];
+    const uint32_t* row = segmat + pd.row0 + t * pd.rstride;
+    const uint32_t a = row[0] + (t == 0 ? pd.off : 0), e = row[1];
     len = e - a;
-    srcpos = sg.off + cc * sg.rows + a;
+    srcpos = pd.src0 + t * pd.rows + a;
   }
   uint32_t wtot;
   const uint32_t ex = block_excl_sum<NW>(len, misc, &wtot);
@@ -442,18 +153,16 @@ __device__ __forceinline__ uint32_t ct_stage(uint32_t ps, uint32_t npslots, int 
     }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
-  return ps;
 }
 
 template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT)
-k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-               const PieceDesc* __restrict__ pieces, uint32_t npslots, const K* __restrict__ src,
+__global__ void __launch_bounds__(NT, 3)
+k_transpose_ct(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict__ pcount, const K* __restrict__ src,
                K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
                const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
   using C = CtCfg<K, PAIRS, NT, S, F>;
   constexpr int EB = sizeof(K), NW = C::NW, KT = C::KT, VW = C::VW;
-  static_assert(F <= NT && NT % 32 == 0 && S <= 65535 && kTB == 32 && KT < 64, "shape");
+  static_assert(F <= NT && NT % 32 == 0 && S <= 65535 && kTB == 32 && KT < 64 && C::NB == 2, "shape");
   extern __shared__ __align__(128) unsigned char sm[];
   unsigned char* outraw = sm + C::off_out;
   unsigned char* voutraw = sm + C::off_vout;
@@ -461,14 +170,21 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
   uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
   uint32_t* poff = misc + 64;
   const int t = threadIdx.x, lane = t & 31;
+  const uint32_t npieces = *pcount;
 
+  // descriptors are loaded one piece ahead of their staging, which runs one piece
+  // ahead of the processing
   int b = 0;
-  uint32_t ps = ct_stage<K, PAIRS, NT, S, F>(blockIdx.x, npslots, 0, sm, segs, tiles, pieces, src, vsrc, piv, segmat);
-  while (ps < npslots) {
+  uint32_t i = blockIdx.x;
+  PieceDesc nx = i < npieces ? pieces[i] : PieceDesc{};
+  ct_stage<K, PAIRS, NT, S, F>(nx, i < npieces, 0, sm, src, vsrc, piv, segmat);
+  nx = i + gridDim.x < npieces ? pieces[i + gridDim.x] : PieceDesc{};
+  for (; i < npieces; i += gridDim.x) {
     // stage the next piece into the other buffer while this one is processed
-    const uint32_t nps = ct_stage<K, PAIRS, NT, S, F>(ps + gridDim.x, npslots, b ^ 1, sm, segs, tiles, pieces, src,
-                                                      vsrc, piv, segmat);
-    for (int i = t; i < 33 * NT; i += NT) cnt[i] = 0;  // 32 bucket rows + the dummy row
+    const uint32_t in = i + gridDim.x;
+    ct_stage<K, PAIRS, NT, S, F>(nx, in < npieces, b ^ 1, sm, src, vsrc, piv, segmat);
+    nx = in + gridDim.x < npieces ? pieces[in + gridDim.x] : PieceDesc{};
+    for (int q = t; q < 33 * NT; q += NT) cnt[q] = 0;  // 32 bucket rows + the dummy row
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncthreads();
     const K* slot = reinterpret_cast<const K*>(sm + C::off_slot + b * C::SLOT_B);
@@ -490,7 +206,7 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
       if (w0 >= nwords) vb = 0;
     }
     K xs[KT];
-    uint32_t cd[KT];  // bucket | thread-local rank << 8
+    uint32_t cdp[(KT + 1) / 2];  // per key: bucket | thread-local rank << 6, two per word
 #pragma unroll
     for (int q = 0; q < KT / VW; q++) {
       const uint4 v4 = reinterpret_cast<const uint4*>(slot)[t * (KT / VW) + q];
@@ -532,7 +248,9 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
       // shared atomics: the counter updates of one thread are independent (a
       // load/store pair would serialise them through possible aliasing)
       const uint32_t r = atomicAdd(&cnt[cswz(bk * NT + t)], 1u);
-      cd[j] = bk | (r << 8);
+      const uint32_t c = bk | (r << 6);
+      if (j & 1) cdp[j / 2] |= c << 16;
+      else cdp[j / 2] = c;
     }
     __syncthreads();
     // ---- exclusive scan of the counters, bucket-major (thread u: entries 32u .. 32u+31,
@@ -569,10 +287,21 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
     const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
     uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
 #pragma unroll
+    for (int q = 0; q < KT / VW; q++) {  // keys re-read from the stage (fewer live registers)
+      const uint4 v4 = reinterpret_cast<const uint4*>(slot)[t * (KT / VW) + q];
+      if constexpr (sizeof(K) == 4) {
+        xs[4 * q] = v4.x; xs[4 * q + 1] = v4.y; xs[4 * q + 2] = v4.z; xs[4 * q + 3] = v4.w;
+      } else {
+        xs[2 * q] = (uint64_t(v4.y) << 32) | v4.x;
+        xs[2 * q + 1] = (uint64_t(v4.w) << 32) | v4.z;
+      }
+    }
+#pragma unroll
     for (int j = 0; j < KT; j++) {
-      const uint32_t bk = cd[j] & 0xff;
+      const uint32_t c = (cdp[j / 2] >> (16 * (j & 1))) & 0xffffu;
+      const uint32_t bk = c & 63;
       if (bk < 32) {
-        const uint32_t dpos = cnt[cswz(bk * NT + t)] + (cd[j] >> 8);
+        const uint32_t dpos = cnt[cswz(bk * NT + t)] + (c >> 6);
         outb[dpos] = xs[j];
         if (PAIRS) vout[dpos] = vslot[w0 + j];
       }
@@ -610,9 +339,8 @@ k_transpose_ct(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ t
       }
       if (t == 0) bulk_commit();
     }
-    if (t <= kTB) ppre[uint64_t(ps) * kPP + t] = (uint16_t)poff[t];
+    if (t <= kTB) ppre[uint64_t(meta[kMxPiece]) * kPP + t] = (uint16_t)poff[t];
     __syncthreads();
-    ps = nps;
     b ^= 1;
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
