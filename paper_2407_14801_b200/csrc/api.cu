@@ -309,7 +309,7 @@ template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
 template <typename K, bool PAIRS> struct MergeCfg {
-  static constexpr int NT = 256, VM = PAIRS ? 16 : 32;
+  static constexpr int NT = 128, VM = PAIRS ? 16 : 32;
 };
 
 // Side streams for running the bucket-class kernels concurrently.
@@ -664,8 +664,13 @@ struct Engine {
     po.msort_max = po.max_tile;
     po.mtile = MergeCfg<K, PAIRS>::NT * MergeCfg<K, PAIRS>::VM;
     po.mcap = 1;
+    // pair sort: 32-bit keys only, with the default one-CTA cap (not under test hooks)
+    po.pair = 0;  // (k_pairsort measured slower than chunk sorts + merge passes)
+    po.units = (Unit*)ar.alloc(buck_tot * sizeof(Unit));
+    po.nunits = (uint32_t*)ar.alloc(16);
+    SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     if (g_big_mode == 1) {  // multi-CTA merge sort for buckets of up to 16 chunks
-      po.msort_max = 16u * po.max_tile;
+      po.msort_max = 16u * (po.pair ? 2u : 1u) * po.max_tile;
       po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
       ensure_third();
     }
@@ -673,9 +678,9 @@ struct Engine {
     po.mcount = (uint32_t*)ar.alloc(kMaxPasses * 4);
     SQ_CUDA(cudaMemsetAsync(po.mcount, 0, kMaxPasses * 4, st));
     po.cap_per_list = (uint32_t)(buck_tot + level_keys / std::max<uint32_t>(po.max_tile, 1) + 16);
-    po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 2) * po.cap_per_list * 4);
-    po.count = (uint32_t*)ar.alloc((po.ncls + 2) * 4);
-    SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 2) * 4, st));
+    po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 3) * po.cap_per_list * 4);
+    po.count = (uint32_t*)ar.alloc((po.ncls + 3) * 4);
+    SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 3) * 4, st));
     {
       ProfScope ps("plan", st);
       uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
@@ -687,6 +692,8 @@ struct Engine {
       k_bucket_plan<K><<<(uint32_t)((buck_tot + 255) / 256), 256, 0, st>>>(dL, ns, dSegOf, dTileBase, bsize, boff, piv,
                                                                          recs, (uint32_t)buck_tot, po);
       check_launch("k_bucket_plan");
+      k_unit_plan<<<(ntiles + 127) / 128, 128, 0, st>>>(recs, dTiles, dL, ntiles, po);
+      check_launch("k_unit_plan");
     }
     if (dbg) {
       k_bucket_gather<K, 256><<<1024, 256, 0, st>>>(recs, dTiles, nullptr, nullptr, (uint32_t)buck_tot, kb[T],
@@ -713,6 +720,23 @@ struct Engine {
     SQ_CUDA(cudaEventRecord(fork, st));
     for (int i = 0; i < SideStreams::N; i++) SQ_CUDA(cudaStreamWaitEvent(ss.s[i], fork, 0));
     int rr = 0;
+    if constexpr (!PAIRS && sizeof(K) == 4) {
+      if (po.pair) {  // buckets / chunks of 16K < len <= 32K: two-CTA clusters
+        constexpr int NT = 512, V = 32;
+        using BS = BlockSort<K, NT, V>;
+        const size_t smem = BS::SMEM_BYTES + (3 * NT + 64) * 4;
+        auto f = k_pairsort<K, NT, V>;
+        static int grid = 0;
+        if (!grid) {
+          set_smem(f, smem);
+          grid = std::max(2, wave_grid(f, NT, smem) & ~1);
+        }
+        ProfScope ps("pairsort", st);
+        f<<<(uint32_t)grid, NT, smem, st>>>(recs, dTiles, po.list + uint64_t(po.ncls + 2) * po.cap_per_list,
+                                            po.count + po.ncls + 2, kb[T], kb[X], pout, ppre, kb[2]);
+        check_launch("k_pairsort");
+      }
+    }
     for (int c = (int)po.ncls - 1; c >= 0; c--) {  // biggest classes first
       const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
       cudaStream_t cs = g_concurrent_classes ? ss.s[rr++ % SideStreams::N] : st;
@@ -733,7 +757,7 @@ struct Engine {
         ProfScope ps("bucketsort", cs);
         f<<<(uint32_t)std::min<uint64_t>(grid, po.cap_per_list), NT, smem, cs>>>(
             recs, dTiles, lst, po.count + c, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
-            ppre, kb[2], PAIRS ? vb[2] : nullptr);
+            ppre, kb[2], PAIRS ? vb[2] : nullptr, po.units);
         check_launch("k_bucketsort");
       });
     }
@@ -805,6 +829,7 @@ struct Engine {
         g_stats.oversize_keys += hr[i].size;
       }
     }
+    for (void* p : {(void*)po.units, (void*)po.nunits}) ar.release(p);
     for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)po.mlist, (void*)piv,
                     (void*)flags, (void*)p0s, (void*)info, (void*)fix, (void*)segmin})
       ar.release(p);

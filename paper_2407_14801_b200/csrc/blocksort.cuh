@@ -162,6 +162,44 @@ struct BlockSort {
   // never straddle a pad period unevenly, so the offsets are compile-time constants.
   __device__ __forceinline__ static constexpr uint32_t poff(int j) { return uint32_t(j + j / PER); }
 
+  // Merge step of one thread: run A = s[a0, a0+la) ascending, run B = s[a0+la, bend)
+  // DESCENDING (a bitonic pair); the thread produces the V merged keys at positions
+  // [tv, tv+V) of the pair (tv >= a0) into r.  Reading one past the end of A lands on
+  // B's largest key and one past the end of B on A's largest: neither is ever taken
+  // too early, so the merge needs no bounds checks.
+  __device__ __forceinline__ static void merge_bitonic(const K* s, uint32_t a0, uint32_t la, uint32_t bend,
+                                                       uint32_t tv, K (&r)[V]) {
+    const uint32_t lb = bend - a0 - la;
+    const uint32_t diag = tv - a0;
+    // merge path: smallest i with A[i] > B[diag-1-i]; B[k] lives at bend-1-k
+    uint32_t lo = diag > lb ? diag - lb : 0;
+    uint32_t hi = diag < la ? diag : la;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const K x = s[pad(a0 + mid)];
+      const K y = s[pad(bend - diag + mid)];
+      const bool le = x <= y;
+      lo = le ? mid + 1 : lo;
+      hi = le ? hi : mid;
+    }
+    const uint32_t pa = a0 + lo;                 // physical index of the next A key
+    const uint32_t pb = bend - 1 - (diag - lo);  // physical index of the next B key (descending)
+    K a = s[pad(pa)];
+    K b = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
+    uint32_t na = pa + 1, nb = pb - 1;  // the index each run reads next
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+      const bool takeA = a <= b;
+      r[k] = takeA ? a : b;
+      const uint32_t idx = takeA ? na : nb;
+      na += takeA ? 1u : 0u;
+      nb -= takeA ? 0u : 1u;
+      const K v = s[pad(idx)];
+      a = takeA ? v : a;
+      b = takeA ? b : v;
+    }
+  }
+
   // Keys at positions >= len are padding (kMax).  Sorted, every position >= len holds
   // kMax after every merge pass, so threads whose whole block lies there skip the
   // work (and warps entirely in the padding skip the register stages).
@@ -209,34 +247,7 @@ struct BlockSort {
         __syncthreads();
       }
       if (tv >= len) continue;  // r[] stays all kMax
-      const uint32_t diag = t * V - a0;
-      // merge path: smallest i with A[i] > B[diag-1-i]; B[k] lives at bend-1-k
-      uint32_t lo = diag > lb ? diag - lb : 0;
-      uint32_t hi = diag < la ? diag : la;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        const K x = s[pad(a0 + mid)];
-        const K y = s[pad(bend - diag + mid)];
-        const bool le = x <= y;
-        lo = le ? mid + 1 : lo;
-        hi = le ? hi : mid;
-      }
-      const uint32_t pa = a0 + lo;                 // physical index of the next A key
-      const uint32_t pb = bend - 1 - (diag - lo);  // physical index of the next B key (descending)
-      K a = s[pad(pa)];
-      K b = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
-      uint32_t na = pa + 1, nb = pb - 1;  // the index each run reads next
-#pragma unroll
-      for (int k = 0; k < V; k++) {
-        const bool takeA = a <= b;
-        r[k] = takeA ? a : b;
-        const uint32_t idx = takeA ? na : nb;
-        na += takeA ? 1u : 0u;
-        nb -= takeA ? 0u : 1u;
-        const K v = s[pad(idx)];
-        a = takeA ? v : a;
-        b = takeA ? b : v;
-      }
+      merge_bitonic(s, a0, la, bend, tv, r);
     }
     __syncthreads();
     {

@@ -476,6 +476,11 @@ k_piece_plan(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, co
 // Bucket planning, per segment (one CTA): bucket sizes from the piece tables,
 // final offsets (exclusive scan, P:283 / P:461), RNG node keys, and the work
 // lists: single-value buckets (copy), on-chip classes, oversize.
+struct Unit {
+  uint32_t tile, j0, j1, out, size;  // buckets j0..j1 (lanes) of a tile, their output start and total
+};
+constexpr uint32_t kUnitFlag = 0x80000000u;
+
 struct PlanOut {
   uint32_t* list;       // [ncls + 2][cap_per_list] work items (bucket * 16 + chunk)
   uint32_t* count;      // [ncls + 2] atomic counters; ncls = copy list, ncls+1 = oversize
@@ -490,6 +495,14 @@ struct PlanOut {
   MTile* mlist;           // [kMaxPasses][mcap]
   uint32_t* mcount;       // [kMaxPasses]
   uint32_t mcap;
+  // pair sort (k_pairsort): 0 = off; else buckets and chunks of max_tile < len <=
+  // 2*max_tile keys go to list ncls + 2, and merge-sort chunks are 2*max_tile keys
+  uint32_t pair;
+  // units: consecutive buckets of one tile, each of at most max_tile keys, packed
+  // into work items of at most max_tile keys (their keys are value-ordered ranges,
+  // so sorting the concatenation sorts every bucket); items are kUnitFlag | index
+  Unit* units;
+  uint32_t* nunits;
 };
 
 // Bucket sizes from the piece tables: CTA per tile, warp w sums pieces w, w+NW, ...
@@ -576,9 +589,10 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, 
   rc.passes = 0;
   const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
   uint32_t q = 1;  // chunks
+  const uint32_t chunk_len = po.pair ? 2 * po.max_tile : po.max_tile;
   if (size && !single && size > po.max_tile && size <= po.msort_max) {
-    q = (size + po.max_tile - 1) / po.max_tile;
-    rc.chunk = po.max_tile;  // full chunks; the last one takes the remainder
+    q = (size + chunk_len - 1) / chunk_len;
+    rc.chunk = chunk_len;  // full chunks; the last one takes the remainder
     uint32_t np = 0;
     while ((1u << np) < q) np++;
     rc.passes = np;
@@ -596,6 +610,7 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, 
   }
   recs[gi] = rc;
   if (!size) return;
+  if (po.units && size <= po.max_tile) return;  // packed into a unit by k_unit_plan
   if (single || size > po.msort_max) {
     const int cls = single ? po.ncls : po.ncls + 1;
     const uint32_t slot = atomicAdd(&po.count[cls], 1u);
@@ -604,11 +619,52 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, 
     for (uint32_t k = 0; k < q; k++) {
       const uint32_t len = min(rc.chunk, size - k * rc.chunk);
       int cls = 0;
-      while (po.cls_tile[cls] < len) cls++;
+      if (po.pair && len > po.max_tile) cls = po.ncls + 2;
+      else
+        while (po.cls_tile[cls] < len) cls++;
       const uint32_t slot = atomicAdd(&po.count[cls], 1u);
       po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16 + k;
     }
   }
+}
+
+// Packing of the small buckets (size <= max_tile) of every tile into units (greedy,
+// in bucket order, at most max_tile keys each); one thread per tile.
+__global__ void k_unit_plan(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
+                            const LevelSeg* __restrict__ segs, uint32_t ntiles, PlanOut po) {
+  const uint32_t ti_idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ti_idx >= ntiles) return;
+  const TileInfo ti = tiles[ti_idx];
+  const LevelSeg sg = segs[ti.seg];
+  const uint32_t b0 = sg.buck_base + ti.bt * kTB, nb = min((uint32_t)kTB, sg.k - ti.bt * kTB);
+  uint32_t j0 = 0, acc = 0, out0 = 0;
+  auto flush = [&](uint32_t j1) {  // buckets j0..j1-1
+    if (!acc) return;
+    const uint32_t u = atomicAdd(po.nunits, 1u);
+    po.units[u] = Unit{ti_idx, j0, j1 - 1, out0, acc};
+    int cls = 0;
+    while (po.cls_tile[cls] < acc) cls++;
+    const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+    po.list[uint64_t(cls) * po.cap_per_list + slot] = kUnitFlag | u;
+  };
+  for (uint32_t j = 0; j < nb; j++) {
+    const BucketRec rc = recs[b0 + j];
+    const bool small = rc.size <= po.max_tile;
+    if (!small || acc + rc.size > po.max_tile) {
+      flush(j);
+      acc = 0;
+    }
+    if (small && rc.size) {
+      if (!acc) {
+        j0 = j;
+        out0 = rc.out;
+      }
+      acc += rc.size;
+    } else if (small && !acc) {
+      j0 = j + 1;  // empty bucket before any key: skip it
+    }
+  }
+  flush(nb);
 }
 
 // Gather the bucket positions [lo, hi) (piece order = the paper's order) of a
@@ -618,7 +674,8 @@ template <int NT, typename F>
 __device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_j, const uint32_t* __restrict__ pout,
                                               const uint16_t* __restrict__ ppre, uint32_t* s_off, uint32_t* s_len,
                                               uint32_t* s_dst, uint32_t* misc, uint32_t lo, uint32_t hi,
-                                              F&& copy_chunk) {
+                                              F&& copy_chunk, uint32_t lane_end = 0) {
+  if (!lane_end) lane_end = lane_j + 1;  // buckets [lane_j, lane_end) of the tile
   constexpr int NW = NT / 32;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   uint32_t base = 0;
@@ -627,7 +684,7 @@ __device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_
     uint32_t o = 0, l = 0;
     if (q < ti.npieces) {
       const uint16_t* pr = ppre + uint64_t(ti.piece_base + q) * kPP;
-      const uint32_t a = pr[lane_j], e = pr[lane_j + 1];
+      const uint32_t a = pr[lane_j], e = pr[lane_end];
       o = pout[ti.piece_base + q] + a;
       l = e - a;
     }
@@ -658,7 +715,8 @@ __global__ void __launch_bounds__(NT)
 k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
              const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
              const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst, const uint32_t* __restrict__ pout,
-             const uint16_t* __restrict__ ppre, K* __restrict__ dst_odd, uint32_t* __restrict__ vdst_odd) {
+             const uint16_t* __restrict__ ppre, K* __restrict__ dst_odd, uint32_t* __restrict__ vdst_odd,
+             const Unit* __restrict__ units) {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   using BS = BlockSort<SK, NT, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -671,14 +729,32 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
   const uint32_t total = *count;
   for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
     const uint32_t e = list[it];
-    const BucketRec rc = recs[item_bucket(e)];
-    const TileInfo ti = tiles[rc.tile];
-    const uint32_t lo = item_chunk(e) * rc.chunk, hi = min(rc.size, lo + rc.chunk);
+    uint32_t tile, lane0, lane1, lo, hi, outpos, passes;
+    if (e & kUnitFlag) {  // packed run of whole buckets
+      const Unit u = units[e & ~kUnitFlag];
+      tile = u.tile;
+      lane0 = u.j0;
+      lane1 = u.j1 + 1;
+      lo = 0;
+      hi = u.size;
+      outpos = u.out;
+      passes = 0;
+    } else {
+      const BucketRec rc = recs[item_bucket(e)];
+      tile = rc.tile;
+      lane0 = rc.lane;
+      lane1 = rc.lane + 1;
+      lo = item_chunk(e) * rc.chunk;
+      hi = min(rc.size, lo + rc.chunk);
+      outpos = rc.out;
+      passes = rc.passes;
+    }
+    const TileInfo ti = tiles[tile];
     const uint32_t len = hi - lo;
-    K* out = (rc.passes & 1) ? dst_odd : dst;
-    uint32_t* vout = (rc.passes & 1) ? vdst_odd : vdst;
+    K* out = (passes & 1) ? dst_odd : dst;
+    uint32_t* vout = (passes & 1) ? vdst_odd : vdst;
     for (int i = threadIdx.x + len; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
-    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
+    gather_bucket<NT>(ti, lane0, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
@@ -689,7 +765,8 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
                             cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
                           }
                         }
-                      });
+                      },
+                      lane1);
     cp_async_wait_all();
     __syncthreads();
     if constexpr (PAIRS) {  // composite = key << 32 | position (stable order)
@@ -703,10 +780,138 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
       if constexpr (PAIRS) {
-        out[rc.out + lo + i] = uint32_t(x >> 32);
-        vout[rc.out + lo + i] = vs[uint32_t(x)];
+        out[outpos + lo + i] = uint32_t(x >> 32);
+        vout[outpos + lo + i] = vs[uint32_t(x)];
       } else {
-        out[rc.out + lo + i] = x;
+        out[outpos + lo + i] = x;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Pair sort (the GPU's simple_sort for 2*TILE keys, P:259-261 / P:852): a cluster of
+// two CTAs sorts one bucket (or one chunk of a merge-sorted bucket) of TILE < L <=
+// 2*TILE keys without an HBM round trip.  CTA r gathers and sorts its half on chip
+// (A = [0, h) on rank 0, B = [h, L) on rank 1, h = L/2).  The merge-path split x at
+// diagonal h says rank 0's output is A[0,x) u B[0,h-x) and rank 1's is A[x,h) u
+// B[h-x, L-h): the two CTAs swap A[x,h) and B[0,h-x) (equal sizes) through
+// distributed shared memory, arrange each tile as an ascending run followed by a
+// descending one (padding on the descending side) and finish with one guard-free
+// merge step of BlockSort.  Keys only (32-bit).
+template <typename K, int NT, int V>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
+k_pairsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
+           const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
+           const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre, K* __restrict__ dst_odd) {
+  namespace cg = cooperative_groups;
+  using BS = BlockSort<K, NT, V>;
+  constexpr uint32_t TILE = BS::TILE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* s = reinterpret_cast<K*>(smem_raw);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  uint32_t* s_len = s_off + NT;
+  uint32_t* s_dst = s_len + NT;
+  uint32_t* misc = s_dst + NT;
+  __shared__ uint32_t s_split;
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t t = threadIdx.x;
+  for (uint32_t it = blockIdx.x >> 1; it < *count; it += gridDim.x >> 1) {
+    const uint32_t rank = cl.block_rank();
+    {  // gather and sort this CTA's part (only the tile stays live across the sort)
+      const uint32_t e = list[it];
+      const BucketRec rc = recs[item_bucket(e)];
+      const TileInfo ti = tiles[rc.tile];
+      const uint32_t c0 = item_chunk(e) * rc.chunk, c1 = min(rc.size, c0 + rc.chunk);
+      const uint32_t h = (c1 - c0) / 2;  // balanced halves: rank 0 [0, h), rank 1 [h, L)
+      const uint32_t lo = c0 + rank * h, len = rank ? c1 - c0 - h : h;
+      for (uint32_t i = t + len; i < TILE; i += NT) s[BS::pad(i)] = KeyTraits<K>::kMax;
+      gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, lo + len,
+                        [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                          for (uint32_t q = ln; q < l; q += 32) cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
+                        });
+      cp_async_wait_all();
+      __syncthreads();
+      BS::sort_smem(s, len);
+    }
+    const K* sr = cl.map_shared_rank(s, rank ^ 1);  // the partner's tile
+    const uint32_t e = list[it];
+    const BucketRec rc = recs[item_bucket(e)];
+    const uint32_t c0 = item_chunk(e) * rc.chunk, c1 = min(rc.size, c0 + rc.chunk);
+    const uint32_t h = (c1 - c0) / 2, lb = c1 - c0 - h;  // |A| = h (rank 0), |B| = lb (rank 1)
+    const uint32_t lo = c0 + rank * h, len = rank ? lb : h;
+    K* out = (rc.passes & 1) ? dst_odd : dst;
+    cl.sync();  // both tiles sorted and visible
+    // split at diagonal h: smallest i in [h - lb, h] (h - lb <= 0) with A[i] > B[h-1-i]
+    // (ties: A first); warp 0, 32-ary search over both tiles (one of them remote)
+    if (t < 32) {
+      const K* A = rank ? sr : s;
+      const K* B = rank ? s : sr;
+      uint32_t a = 0, b = h;
+      while (b > a) {
+        const uint32_t step = (b - a + 31) / 32;
+        const uint32_t p = a + t * step;
+        const bool gt = p < b ? A[BS::pad(p)] > B[BS::pad(h - 1 - p)] : true;
+        const uint32_t m = __ballot_sync(0xffffffffu, gt);
+        const uint32_t first = m ? (uint32_t)(__ffs(m) - 1) : 32u;
+        if (first == 0) b = a;
+        else {
+          const uint32_t a0 = a;
+          a = a0 + (first - 1) * step + 1;
+          b = min(b, a0 + first * step);
+        }
+      }
+      if (t == 0) s_split = a;
+    }
+    __syncthreads();
+    const uint32_t x = s_split, cnt = h - x;  // A keys moving to rank 1 = B keys moving to rank 0
+    // swap A[x, TILE) (rank 0, positions x + i) with B[0, cnt) (rank 1, positions i):
+    // each key lands at the position its counterpart leaves, so the swap runs in
+    // phases (fewer live registers), each read before the cluster barrier and
+    // written after it
+    constexpr int PH = 4, VP = V / PH;
+#pragma unroll 1
+    for (int ph = 0; ph < PH; ph++) {
+      K v[VP];
+#pragma unroll
+      for (int j = 0; j < VP; j++) {
+        const uint32_t i = t + (ph * VP + j) * NT;
+        if (i < cnt) v[j] = rank ? sr[BS::pad(x + i)] : sr[BS::pad(i)];
+      }
+      cl.sync();
+#pragma unroll
+      for (int j = 0; j < VP; j++) {
+        const uint32_t i = t + (ph * VP + j) * NT;
+        if (i < cnt) s[BS::pad(rank ? i : x + i)] = v[j];
+      }
+    }
+    cl.sync();  // no remote reads of this tile remain
+    // second run descending: rank 0 [x, TILE) = B[0, cnt) + padding;
+    // rank 1 [cnt, TILE) = B[cnt, lb) + padding
+    {
+      const uint32_t r0 = rank ? cnt : x, w = TILE - r0;
+      for (uint32_t i = t; i < w / 2; i += NT) {
+        const uint32_t p = r0 + i, q = TILE - 1 - i;
+        const K a = s[BS::pad(p)], b = s[BS::pad(q)];
+        s[BS::pad(p)] = b;
+        s[BS::pad(q)] = a;
+      }
+    }
+    __syncthreads();
+    K r[V];
+    const uint32_t tv = t * V;
+    if (tv < len) {
+      BS::merge_bitonic(s, 0, rank ? cnt : x, TILE, tv, r);
+      // straight from registers (each thread writes whole 128-byte lines)
+      K* o = out + rc.out + lo + tv;
+      if (tv + V <= len) {
+#pragma unroll
+        for (int j = 0; j < V; j++) o[j] = r[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; j++)
+          if (tv + j < len) o[j] = r[j];
       }
     }
     __syncthreads();
