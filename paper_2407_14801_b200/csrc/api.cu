@@ -667,6 +667,9 @@ struct Engine {
     // pair sort: 32-bit keys only, with the default one-CTA cap (not under test hooks)
     po.pair = 0;  // (k_pairsort measured slower than chunk sorts + merge passes)
     po.units = (Unit*)ar.alloc(buck_tot * sizeof(Unit));
+    po.unit_max = 0;
+    for (uint32_t c = 0; c < po.ncls; c++)
+      if (!cls_cl[c]) po.unit_max = std::max(po.unit_max, po.cls_tile[c]);
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     if (g_big_mode == 1) {  // multi-CTA merge sort for buckets of up to 16 chunks

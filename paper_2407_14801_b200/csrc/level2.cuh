@@ -503,6 +503,7 @@ struct PlanOut {
   // so sorting the concatenation sorts every bucket); items are kUnitFlag | index
   Unit* units;
   uint32_t* nunits;
+  uint32_t unit_max;  // largest unit (and bucket packed into units): the biggest one-CTA class
 };
 
 // Bucket sizes from the piece tables: CTA per tile, warp w sums pieces w, w+NW, ...
@@ -610,7 +611,7 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, 
   }
   recs[gi] = rc;
   if (!size) return;
-  if (po.units && size <= po.max_tile) return;  // packed into a unit by k_unit_plan
+  if (po.units && size <= po.unit_max) return;  // packed into a unit by k_unit_plan
   if (single || size > po.msort_max) {
     const int cls = single ? po.ncls : po.ncls + 1;
     const uint32_t slot = atomicAdd(&po.count[cls], 1u);
@@ -649,8 +650,8 @@ __global__ void k_unit_plan(const BucketRec* __restrict__ recs, const TileInfo* 
   };
   for (uint32_t j = 0; j < nb; j++) {
     const BucketRec rc = recs[b0 + j];
-    const bool small = rc.size <= po.max_tile;
-    if (!small || acc + rc.size > po.max_tile) {
+    const bool small = rc.size <= po.unit_max;
+    if (!small || acc + rc.size > po.unit_max) {
       flush(j);
       acc = 0;
     }
