@@ -621,17 +621,17 @@ struct Engine {
         k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout);
         check_launch("k_piece_plan");
       }
-      using XC = CtCfg<K, PAIRS, TC::XNT, TC::S, TC::F>;
-      auto f = k_transpose_ct<K, PAIRS, TC::XNT, TC::S, TC::F>;
+      using XC = WsCfg<K, PAIRS, TC::S, TC::F>;
+      auto f = k_transpose_ws<K, PAIRS, TC::S, TC::F>;
       static int grid = 0;
       if (!grid) {
         set_smem(f, XC::SMEM);
-        grid = wave_grid(f, TC::XNT, XC::SMEM);
+        grid = wave_grid(f, XC::NT, XC::SMEM);
       }
       ProfScope ps("transpose", st);
-      f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), TC::XNT, XC::SMEM, st>>>(
+      f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), XC::NT, XC::SMEM, st>>>(
           pieces, pcount, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv, segmat, ppre);
-      check_launch("k_transpose_ct");
+      check_launch("k_transpose_ws");
       ar.release(pcount);
       ar.release(pieces);
     }
