@@ -146,7 +146,7 @@ __device__ __forceinline__ void ct_stage(const PieceDesc& pd, bool valid, int b,
     const uint32_t sdst = smem_addr(slot) + so;
     const unsigned char* g = reinterpret_cast<const unsigned char*>(src + srcpos) - mis;
     for (uint32_t v = 0; v < sbytes; v += 16)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
     if (PAIRS) {  // values at the same word index (per-element async copies)
       const uint32_t* gv = vsrc + srcpos;
       for (uint32_t k = 0; k < flen; k++) cp_async_elem(&vslot[e0 + k], &gv[k]);
@@ -511,7 +511,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
           const uint32_t sdst = smem_addr(slot) + so;
           const unsigned char* g = reinterpret_cast<const unsigned char*>(src + srcpos) - mis;
           for (uint32_t v = 0; v < sbytes; v += 16)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
           if (PAIRS) {
             const uint32_t* gv = vsrc + srcpos;
             for (uint32_t kk = 0; kk < flen; kk++) cp_async_elem(&vslot[e0 + kk], &gv[kk]);
