@@ -290,6 +290,7 @@ template <> struct TrCfg<uint32_t, false> { static constexpr int NT = 256, S = 4
 template <> struct TrCfg<uint32_t, true> { static constexpr int NT = 256, S = 4096, G = 256; };
 template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
 // piece-major transpose (sort path): threads, piece size, fragments per piece
+constexpr int kPlanFW = 120;  // piece-plan window (columns); <= the transpose's F = 128
 template <typename K, bool PAIRS> struct PmTr;
 template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
 template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
@@ -508,9 +509,10 @@ struct Engine {
       cand_tot += uint64_t(kCap) * np;
       tile_base[s] = (uint32_t)tiles.size();
       for (uint32_t bt = 0; bt < l.nbt; bt++) tiles.push_back({s, bt, 0, 0, 0, 0});
-      const uint32_t gpt = (m + TC::F - 1) / TC::F;
+      // windows per tile (plan_fw): at most ceil(m / kPlanFW) + size * 32 / (31 S) + 2
+      const uint32_t gpt = (m + kPlanFW - 1) / kPlanFW + 2;
       piece_seg_base[s] = (uint32_t)piece_tot;
-      piece_tot += g.len / TC::S + uint64_t(l.nbt) * (1 + gpt) + 1;
+      piece_tot += 3 * (g.len / TC::S) + uint64_t(l.nbt) * (1 + gpt) + 1;
       for (uint32_t c = 0; c < m; c++) {
         const uint64_t a = uint64_t(c) * m;
         if (a >= g.len) break;
@@ -609,7 +611,7 @@ struct Engine {
       ProfScope ps("tiles", st);
       k_tile_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, segmat);
       check_launch("k_tile_sizes");
-      k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, TC::F, dPieceBase);
+      k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, kPlanFW, dPieceBase);
       check_launch("k_tile_scan");
     }
     {
@@ -618,8 +620,8 @@ struct Engine {
       SQ_CUDA(cudaMemsetAsync(pcount, 0, 4, st));
       {
         ProfScope ps("tiles", st);
-        k_piece_plan<256, TC::S, TC::F><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout);
-        check_launch("k_piece_plan");
+        k_piece_plan2<256, TC::S, kPlanFW><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout);
+        check_launch("k_piece_plan2");
       }
       using XC = WsCfg<K, PAIRS, TC::S, TC::F>;
       auto f = k_transpose_ws<K, PAIRS, TC::S, TC::F>;

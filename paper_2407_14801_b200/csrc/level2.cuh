@@ -273,6 +273,14 @@ __global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __rest
 // Per segment: tile output offsets (exclusive scan of sizes) and piece-table
 // bases (capacity ceil(size/S) + ceil(ncols/G) pieces per tile).  Also resets
 // the per-segment bucket bookkeeping.  One CTA per segment (tiles contiguous).
+// Piece-plan window of a bucket tile: columns per window chosen so that a window
+// holds ~31/32 of a piece on average (runs average size/ncols keys), at most FWMAX.
+__host__ __device__ __forceinline__ uint32_t plan_fw(uint32_t size, uint32_t ncols, uint32_t S, uint32_t FWMAX) {
+  if (!size) return FWMAX;
+  const uint64_t fw = (uint64_t(S) * 31 / 32) * ncols / size;
+  return (uint32_t)max((uint64_t)1, min((uint64_t)FWMAX, fw));
+}
+
 __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
                             TileInfo* __restrict__ tiles, uint32_t S, uint32_t G,
                             const uint32_t* __restrict__ piece_seg_base) {
@@ -284,13 +292,13 @@ __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* _
     carry_piece = piece_seg_base[blockIdx.x];
   }
   __syncthreads();
-  const uint32_t gpt = (sg.ncols + G - 1) / G;
   for (uint32_t c0 = 0; c0 < nt; c0 += blockDim.x) {
     const uint32_t i = c0 + threadIdx.x;
     uint32_t sz = 0, cp = 0;
     if (i < nt) {
       sz = tiles[t0 + i].size;
-      cp = (sz + S - 1) / S + gpt;
+      const uint32_t fw = plan_fw(sz, sg.ncols, S, G);
+      cp = (sz + S - 1) / S + (sg.ncols + fw - 1) / fw;
     }
     // block scan of (sz, cp)
     __shared__ uint32_t ws[32], wc[32];
@@ -395,81 +403,127 @@ struct __align__(16) PieceDesc {
   uint32_t nb, thr0, slot, bt;       // buckets in the tile, pivot index of its first boundary, piece table slot, tile
 };
 
-constexpr uint32_t kPlanBuf = 256;  // pieces of one tile staged by the plan
-
-template <int NT, int S, int F>
+// Piece plan, parallel form: every bucket tile's stream is cut into windows of FW
+// consecutive columns; a window of T keys gives ceil(T / S) pieces (one for the
+// usual T <= S), cut at stream positions that are multiples of S.  CTA per tile;
+// warps work on windows independently (no serial chain over the tile).
+template <int NT, int S, int FW>
 __global__ void __launch_bounds__(NT)
-k_piece_plan(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const uint32_t* __restrict__ segmat,
-             PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pcount, uint32_t* __restrict__ pout) {
-  constexpr int NW = NT / 32;
+k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const uint32_t* __restrict__ segmat,
+              PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pcount, uint32_t* __restrict__ pout) {
+  constexpr int NW = NT / 32, PL = (FW + 31) / 32;  // columns per lane within a window
+  constexpr uint32_t MAXW = 1024;                    // windows per chunk
+  static_assert(FW <= 128, "window");
+  __shared__ uint32_t wtot[MAXW], wpc[MAXW], woff[MAXW], wpb[MAXW];
   __shared__ uint32_t misc[64];
-  __shared__ uint32_t fst[F + 1];
-  __shared__ PieceDesc pbuf[kPlanBuf];
-  const int t = threadIdx.x;
+  __shared__ uint32_t base, carry_o, carry_p;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const TileInfo ti = tiles[blockIdx.x];
   const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt;
+  const uint32_t bt = ti.bt, rstride = sg.nbt + 1;
   const uint32_t* rows = segmat + sg.segmat_base;
-  const uint32_t rstride = sg.nbt + 1;
-  uint32_t c = 0, o = 0, oc = ti.out, npc = 0;
-  while (c < sg.ncols) {
-    uint32_t len = 0;
-    if (t < F && c + t < sg.ncols) {
-      const uint32_t* row = rows + uint64_t(c + t) * rstride;
-      len = row[bt + 1] - row[bt] - (t == 0 ? o : 0);
-    }
-    uint32_t wtot;
-    const uint32_t ex = block_excl_sum<NW>(len, misc, &wtot);
-    const uint32_t nwin = min((uint32_t)F, sg.ncols - c);
-    const uint32_t nf = __syncthreads_count(t < (int)nwin && ex < (uint32_t)S);
-    const uint32_t Pn = min((uint32_t)S, wtot);
-    if (t < F) fst[t] = ex;
-    __syncthreads();
-    uint32_t nc, no;
-    if (wtot <= (uint32_t)S) {
-      nc = c + nwin;
-      no = 0;
-    } else {
-      const uint32_t last = nf - 1;
-      const uint32_t used = Pn - fst[last];
-      const uint32_t* row = rows + uint64_t(c + last) * rstride;
-      const uint32_t base = last == 0 ? o : 0;
-      const uint32_t full = row[bt + 1] - row[bt] - base;
-      if (used < full) {
-        nc = c + last;
-        no = base + used;
-      } else {
-        nc = c + last + 1;
-        no = 0;
-      }
-    }
-    if (Pn > 0) {
-      if (t == 0) {  // staged here, appended to the dense list once per tile
-        const uint32_t pe = ti.piece_base + npc;
-        if (npc < kPlanBuf)
-          pbuf[npc] = PieceDesc{Pn, oc, nf, o, sg.off + c * sg.rows, sg.rows,
-                                (uint32_t)(sg.segmat_base + uint64_t(c) * rstride + bt), rstride,
-                                min((uint32_t)kTB, sg.k - bt * kTB), sg.piv_base + bt * kTB, pe, bt};
-        else  // (only for very skewed tiles)
-          pieces[atomicAdd(pcount, 1u)] = PieceDesc{Pn, oc, nf, o, sg.off + c * sg.rows, sg.rows,
-                                                     (uint32_t)(sg.segmat_base + uint64_t(c) * rstride + bt), rstride,
-                                                     min((uint32_t)kTB, sg.k - bt * kTB), sg.piv_base + bt * kTB, pe, bt};
-        pout[pe] = oc;
-      }
-      oc += Pn;
-      npc++;
-    }
-    c = nc;
-    o = no;
-    __syncthreads();
-  }
-  __shared__ uint32_t base;
+  const uint32_t fw = plan_fw(ti.size, sg.ncols, S, FW);  // columns per window (<= FW)
+  const uint32_t nwin = (sg.ncols + fw - 1) / fw;
+  const uint32_t nb = min((uint32_t)kTB, sg.k - bt * kTB);
+  auto run_len = [&](uint32_t c) -> uint32_t {
+    if (c >= sg.ncols) return 0u;
+    const uint32_t* row = rows + uint64_t(c) * rstride + bt;
+    return row[1] - row[0];
+  };
   if (t == 0) {
-    tiles[blockIdx.x].npieces = npc;
-    base = atomicAdd(pcount, min(npc, kPlanBuf));
+    carry_o = 0;
+    carry_p = 0;
   }
-  __syncthreads();
-  for (uint32_t q = t; q < min(npc, kPlanBuf); q += NT) pieces[base + q] = pbuf[q];
+  for (uint32_t w0 = 0; w0 < nwin; w0 += MAXW) {
+    const uint32_t nw = min(MAXW, nwin - w0);
+    for (uint32_t wi = w; wi < nw; wi += NW) {  // window totals
+      const uint32_t win = w0 + wi;
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < PL; q++) {
+        const uint32_t j = lane * PL + q;
+        if (j < fw) sum += run_len(win * fw + j);
+      }
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        wtot[wi] = sum;
+        wpc[wi] = (sum + S - 1) / S;
+      }
+    }
+    __syncthreads();
+    {  // exclusive scans over the windows of the chunk: stream offsets and piece indices
+      uint32_t co = carry_o, cp = carry_p;
+      for (uint32_t c0 = 0; c0 < nw; c0 += NT) {
+        const uint32_t i = c0 + t;
+        const uint32_t a = i < nw ? wtot[i] : 0u, b = i < nw ? wpc[i] : 0u;
+        uint32_t ta, tb;
+        const uint32_t ea = block_excl_sum<NW>(a, misc, &ta);
+        const uint32_t eb = block_excl_sum<NW>(b, misc + 32, &tb);
+        if (i < nw) {
+          woff[i] = co + ea;
+          wpb[i] = cp + eb;
+        }
+        co += ta;
+        cp += tb;
+      }
+      __syncthreads();
+      if (t == 0) {
+        base = atomicAdd(pcount, cp - carry_p) - carry_p;  // dense-list position of piece index carry_p
+        carry_o = co;
+        carry_p = cp;
+      }
+      __syncthreads();
+    }
+    for (uint32_t wi = w; wi < nw; wi += NW) {  // emit the pieces of each window
+      const uint32_t win = w0 + wi;
+      const uint32_t T = wtot[wi], npc = wpc[wi];
+      if (!npc) continue;
+      const uint32_t c0 = win * fw, ncw = min(fw, sg.ncols - c0);
+      // run lengths of the window's columns, lane-major (lane holds PL columns)
+      uint32_t lens[PL], incl[PL], acc = 0;
+#pragma unroll
+      for (int q = 0; q < PL; q++) {
+        lens[q] = (lane * PL + q < ncw) ? run_len(c0 + lane * PL + q) : 0u;
+        acc += lens[q];
+        incl[q] = acc;
+      }
+      uint32_t x = acc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t lane_ex = x - acc;  // keys before this lane's first column
+      for (uint32_t p = 0; p < npc; p++) {
+        const uint32_t sp = p * S, ep = min(sp + S, T);  // stream range [sp, ep) of the window
+        // first column holding stream position sp; last column with keys before ep
+        uint32_t cfirst = 0xffffffffu, clast = 0, offs = 0;
+#pragma unroll
+        for (int q = 0; q < PL; q++) {
+          const uint32_t j = lane * PL + q;
+          const uint32_t ex = lane_ex + incl[q] - lens[q], in = lane_ex + incl[q];
+          if (j < ncw && in > sp && ex <= sp && lens[q]) {
+            cfirst = j;
+            offs = sp - ex;
+          }
+          if (j < ncw && ex < ep) clast = j;
+        }
+        const uint32_t cf = __reduce_min_sync(0xffffffffu, cfirst);
+        const uint32_t cl = __reduce_max_sync(0xffffffffu, clast);
+        const uint32_t of = __shfl_sync(0xffffffffu, offs, cf / PL);
+        if (lane == 0) {
+          const uint32_t j = wpb[wi] + p;  // piece index within the tile
+          const uint32_t pe = ti.piece_base + j, oc = ti.out + woff[wi] + sp;
+          const uint32_t col = c0 + cf;
+          pieces[base + j] = PieceDesc{ep - sp, oc, cl - cf + 1, of, sg.off + col * sg.rows, sg.rows,
+                                       (uint32_t)(sg.segmat_base + uint64_t(col) * rstride + bt), rstride, nb,
+                                       sg.piv_base + bt * kTB, pe, bt};
+          pout[pe] = oc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) tiles[blockIdx.x].npieces = carry_p;
 }
 
 // ------------------------------------------------------------------------------
