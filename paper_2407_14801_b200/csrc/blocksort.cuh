@@ -184,19 +184,26 @@ struct BlockSort {
     }
     const uint32_t pa = a0 + lo;                 // physical index of the next A key
     const uint32_t pb = bend - 1 - (diag - lo);  // physical index of the next B key (descending)
-    K a = s[pad(pa)];
-    K b = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
+    // state: h = head of run L (initially A), o = head of the other run.  The taken
+    // key is min(h, o), the untaken head max(h, o); the next key comes from the run
+    // just taken from, so the new h is always the key just loaded.  (Ties may take
+    // either run: equal keys carry equal values, and the pair composites of the
+    // stable sorts are unique.)
+    K h = s[pad(pa)];
+    K o = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
+    bool L = true;                      // h belongs to A
     uint32_t na = pa + 1, nb = pb - 1;  // the index each run reads next
 #pragma unroll
     for (int k = 0; k < V; k++) {
-      const bool takeA = a <= b;
-      r[k] = takeA ? a : b;
-      const uint32_t idx = takeA ? na : nb;
-      na += takeA ? 1u : 0u;
-      nb -= takeA ? 0u : 1u;
-      const K v = s[pad(idx)];
-      a = takeA ? v : a;
-      b = takeA ? b : v;
+      const bool takeL = h <= o;
+      r[k] = takeL ? h : o;
+      const K mx = takeL ? o : h;
+      L = takeL ? L : !L;  // the run taken from
+      const uint32_t idx = L ? na : nb;
+      if (L) na = idx + 1;
+      else nb = idx - 1;
+      h = s[pad(idx)];
+      o = mx;
     }
   }
 
