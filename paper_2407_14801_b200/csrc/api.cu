@@ -513,13 +513,18 @@ struct Engine {
       const uint32_t gpt = (m + kPlanFW - 1) / kPlanFW + 2;
       piece_seg_base[s] = (uint32_t)piece_tot;
       piece_tot += 3 * (g.len / TC::S) + uint64_t(l.nbt) * (1 + gpt) + 1;
-      for (uint32_t c = 0; c < m; c++) {
-        const uint64_t a = uint64_t(c) * m;
-        if (a >= g.len) break;
-        const uint32_t lc = (uint32_t)std::min<uint64_t>(m, g.len - a);
-        allcols.push_back({uint32_t(g.off + a), lc, child_key(g.node, 0, c)});
-        if (lc > cap) generic = true;
-        colcls[std::max<uint32_t>(64, tile_for(lc))].push_back({uint32_t(g.off + a), lc, s, c});
+      // columns: fc full ones of m keys, then at most one ragged one
+      const uint32_t fc = (uint32_t)std::min<uint64_t>(m, g.len / m);
+      const uint32_t rem = fc < m ? (uint32_t)(g.len - uint64_t(fc) * m) : 0u;
+      if (m > cap) {
+        generic = true;
+        for (uint32_t c = 0; c < fc + (rem ? 1u : 0u); c++)
+          allcols.push_back({uint32_t(g.off + uint64_t(c) * m), c < fc ? m : rem, child_key(g.node, 0, c)});
+      } else {
+        std::vector<ColDesc>& full = colcls[std::max<uint32_t>(64, tile_for(m))];
+        full.reserve(full.size() + fc);
+        for (uint32_t c = 0; c < fc; c++) full.push_back({uint32_t(g.off + uint64_t(c) * m), m, s, c});
+        if (rem) colcls[std::max<uint32_t>(64, tile_for(rem))].push_back({uint32_t(g.off + uint64_t(fc) * m), rem, s, fc});
       }
       for (uint32_t c0 = 0; c0 < m; c0 += 64) mtasks.push_back({s, c0, std::min(m, c0 + 64)});
     }
