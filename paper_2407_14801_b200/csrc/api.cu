@@ -648,8 +648,11 @@ struct Engine {
     int cls_cl[20] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
     {
       const uint32_t one = g_big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
+      // smallest bucket-sort class 1K keys: smaller chunks share it (their padding is
+      // skipped), instead of a latency-bound launch per tiny class
+      const uint32_t lower = std::min<uint32_t>(1024u, one);
       for (uint32_t t : kTiles)
-        if (t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
+        if (t >= lower && t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
       po.max_tile = one;
       if (g_big_mode == 2) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
         const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
@@ -702,7 +705,7 @@ struct Engine {
       k_bucket_plan<K><<<(uint32_t)((buck_tot + 255) / 256), 256, 0, st>>>(dL, ns, dSegOf, dTileBase, bsize, boff, piv,
                                                                          recs, (uint32_t)buck_tot, po);
       check_launch("k_bucket_plan");
-      k_unit_plan<<<(ntiles + 127) / 128, 128, 0, st>>>(recs, dTiles, dL, ntiles, po);
+      k_unit_plan<<<(ntiles * 32 + 127) / 128, 128, 0, st>>>(recs, dTiles, dL, ntiles, po);
       check_launch("k_unit_plan");
     }
     if (dbg) {

@@ -22,7 +22,7 @@ struct LevelSeg {
   uint32_t rows, ncols, k, nbt;  // nbt = ceil(k / kTB) bucket tiles
   uint32_t piv_base;             // pivots arena: k-1 entries
   uint32_t buck_base;            // bucket arrays (counts, starts): k entries
-  uint64_t segmat_base;          // per column (nbt+1) tile-boundary positions
+  uint64_t segmat_base;          // (nbt+1) tile-boundary positions per column (sort path: tile-major)
   uint64_t cand_base;            // sampler candidates: (R+1) slots of k-1 entries
   uint64_t node;                 // RNG node key
 };

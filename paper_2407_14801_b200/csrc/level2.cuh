@@ -189,7 +189,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   }
   // epilogue: tile boundaries of this column
   const K* P = piv + sg.piv_base;
-  uint32_t* row = segmat + sg.segmat_base + uint64_t(d.col) * (sg.nbt + 1);
+  uint32_t* row = segmat + sg.segmat_base + d.col;  // tile-major: entry (bt, c) at bt * ncols + c
   for (uint32_t bt = threadIdx.x; bt <= sg.nbt; bt += NT) {
     uint32_t pos;
     const uint32_t j = bt * kTB;  // boundary index (bucket j starts here)
@@ -205,7 +205,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
       }
       pos = lo;
     }
-    row[bt] = pos;
+    row[uint64_t(bt) * sg.ncols] = pos;
   }
   if (threadIdx.x == 0 && d.len) {
     if constexpr (sizeof(K) == 4) atomicMin((unsigned int*)&segmin[d.seg], (unsigned int)key_at(0));
@@ -228,7 +228,7 @@ __global__ void k_segmat(const LevelSeg* __restrict__ segs, const TaskDesc* __re
     const uint64_t a = uint64_t(c) * sg.rows;
     const uint32_t L = (uint32_t)(a < sg.len ? min((uint64_t)sg.rows, (uint64_t)(sg.len - a)) : 0);
     const K* col = data + sg.off + a;
-    uint32_t* row = segmat + sg.segmat_base + uint64_t(c) * (sg.nbt + 1);
+    uint32_t* row = segmat + sg.segmat_base + c;  // tile-major
     for (uint32_t bt = threadIdx.x; bt <= sg.nbt; bt += blockDim.x) {
       const uint32_t j = bt * kTB;
       uint32_t pos;
@@ -244,7 +244,7 @@ __global__ void k_segmat(const LevelSeg* __restrict__ segs, const TaskDesc* __re
         }
         pos = lo;
       }
-      row[bt] = pos;
+      row[uint64_t(bt) * sg.ncols] = pos;
     }
   }
 }
@@ -256,8 +256,8 @@ __global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __rest
   const LevelSeg sg = segs[ti.seg];
   uint32_t sum = 0;
   for (uint32_t c = threadIdx.x; c < sg.ncols; c += blockDim.x) {
-    const uint32_t* row = segmat + sg.segmat_base + uint64_t(c) * (sg.nbt + 1);
-    sum += row[ti.bt + 1] - row[ti.bt];
+    const uint32_t* row = segmat + sg.segmat_base + uint64_t(ti.bt) * sg.ncols + c;  // tile-major
+    sum += row[sg.ncols] - row[0];
   }
   __shared__ uint32_t red[32];
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -396,10 +396,11 @@ template <> struct Thr<uint64_t> {
 // tile, no wave tail).
 // Self-contained piece descriptor (the transpose needs no other metadata load):
 // fragment f (f < nf) is the run of bucket tile `bt` in column col+f, whose key
-// index is src0 + f*rows + segmat[row0 + f*rstride] (+ off for f = 0).
+// run is [segmat[row0 + f], segmat[row0 + f + rstride]) within its column (segmat is
+// tile-major: entry (bt, c) at bt * ncols + c), keys src0 + f*rows + that (+ off for f = 0).
 struct __align__(16) PieceDesc {
   uint32_t pn, out, nf, off;         // keys, output offset, runs, offset into the first run
-  uint32_t src0, rows, row0, rstride;  // first column's start; column length; segmat index of (col, bt); row stride
+  uint32_t src0, rows, row0, rstride;  // first column's start; column length; segmat index of (bt, col); ncols
   uint32_t nb, thr0, slot, bt;       // buckets in the tile, pivot index of its first boundary, piece table slot, tile
 };
 
@@ -420,15 +421,14 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const TileInfo ti = tiles[blockIdx.x];
   const LevelSeg sg = segs[ti.seg];
-  const uint32_t bt = ti.bt, rstride = sg.nbt + 1;
-  const uint32_t* rows = segmat + sg.segmat_base;
+  const uint32_t bt = ti.bt, rstride = sg.ncols;  // tile-major segmat: (bt+1, c) is ncols after (bt, c)
+  const uint32_t* rows = segmat + sg.segmat_base + uint64_t(bt) * sg.ncols;
   const uint32_t fw = plan_fw(ti.size, sg.ncols, S, FW);  // columns per window (<= FW)
   const uint32_t nwin = (sg.ncols + fw - 1) / fw;
   const uint32_t nb = min((uint32_t)kTB, sg.k - bt * kTB);
   auto run_len = [&](uint32_t c) -> uint32_t {
     if (c >= sg.ncols) return 0u;
-    const uint32_t* row = rows + uint64_t(c) * rstride + bt;
-    return row[1] - row[0];
+    return rows[c + rstride] - rows[c];
   };
   if (t == 0) {
     carry_o = 0;
@@ -515,7 +515,7 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
           const uint32_t pe = ti.piece_base + j, oc = ti.out + woff[wi] + sp;
           const uint32_t col = c0 + cf;
           pieces[base + j] = PieceDesc{ep - sp, oc, cl - cf + 1, of, sg.off + col * sg.rows, sg.rows,
-                                       (uint32_t)(sg.segmat_base + uint64_t(col) * rstride + bt), rstride, nb,
+                                       (uint32_t)(sg.segmat_base + uint64_t(bt) * sg.ncols + col), rstride, nb,
                                        sg.piv_base + bt * kTB, pe, bt};
           pout[pe] = oc;
         }
@@ -687,13 +687,17 @@ __global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, 
 // in bucket order, at most max_tile keys each); one thread per tile.
 __global__ void k_unit_plan(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
                             const LevelSeg* __restrict__ segs, uint32_t ntiles, PlanOut po) {
-  const uint32_t ti_idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ti_idx >= ntiles) return;
+  // one warp per tile: lane j loads bucket j's record, lane 0 packs (shuffles only)
+  const uint32_t ti_idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (ti_idx >= ntiles) return;  // warp-uniform
   const TileInfo ti = tiles[ti_idx];
   const LevelSeg sg = segs[ti.seg];
   const uint32_t b0 = sg.buck_base + ti.bt * kTB, nb = min((uint32_t)kTB, sg.k - ti.bt * kTB);
+  const uint32_t my_size = lane < nb ? recs[b0 + lane].size : 0u;
+  const uint32_t my_out = lane < nb ? recs[b0 + lane].out : 0u;
   uint32_t j0 = 0, acc = 0, out0 = 0;
-  auto flush = [&](uint32_t j1) {  // buckets j0..j1-1
+  auto flush = [&](uint32_t j1) {  // buckets j0..j1-1 (lane 0 only)
     if (!acc) return;
     const uint32_t u = atomicAdd(po.nunits, 1u);
     po.units[u] = Unit{ti_idx, j0, j1 - 1, out0, acc};
@@ -703,23 +707,22 @@ __global__ void k_unit_plan(const BucketRec* __restrict__ recs, const TileInfo* 
     po.list[uint64_t(cls) * po.cap_per_list + slot] = kUnitFlag | u;
   };
   for (uint32_t j = 0; j < nb; j++) {
-    const BucketRec rc = recs[b0 + j];
-    const bool small = rc.size <= po.unit_max;
-    if (!small || acc + rc.size > po.unit_max) {
+    const uint32_t size = __shfl_sync(0xffffffffu, my_size, j), out = __shfl_sync(0xffffffffu, my_out, j);
+    if (lane != 0) continue;
+    const bool small = size <= po.unit_max;
+    if (!small || acc + size > po.unit_max) {
       flush(j);
       acc = 0;
     }
-    if (small && rc.size) {
+    if (small && size) {
       if (!acc) {
         j0 = j;
-        out0 = rc.out;
+        out0 = out;
       }
-      acc += rc.size;
-    } else if (small && !acc) {
-      j0 = j + 1;  // empty bucket before any key: skip it
+      acc += size;
     }
   }
-  flush(nb);
+  if (lane == 0) flush(nb);
 }
 
 // Gather the bucket positions [lo, hi) (piece order = the paper's order) of a

@@ -118,8 +118,8 @@ __device__ __forceinline__ void ct_stage(const PieceDesc& pd, bool valid, int b,
   // to the piece; packed 16-byte aligned slots
   uint32_t len = 0, srcpos = 0, mis = 0, sbytes = 0;
   if (t < (int)nf) {
-    const uint32_t* row = segmat + pd.row0 + t * pd.rstride;
-    const uint32_t a = row[0] + (t == 0 ? pd.off : 0), e = row[1];
+    const uint32_t* row = segmat + pd.row0 + t;  // tile-major: the next boundary is rstride (= ncols) on
+    const uint32_t a = row[0] + (t == 0 ? pd.off : 0), e = row[pd.rstride];
     len = e - a;
     srcpos = pd.src0 + t * pd.rows + a;
   }
@@ -474,9 +474,9 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
       for (int r = 0; r < F / 32; r++) {
         const uint32_t f = 32 * r + lane;
         if (f < nf) {
-          const uint32_t* row = segmat + pd.row0 + f * pd.rstride;
+          const uint32_t* row = segmat + pd.row0 + f;  // tile-major segmat: coalesced over f
           ra[r] = row[0];
-          rb[r] = row[1];
+          rb[r] = row[pd.rstride];
         }
       }
 #pragma unroll
