@@ -675,7 +675,7 @@ struct Engine {
     po.mtile = MergeCfg<K, PAIRS>::NT * MergeCfg<K, PAIRS>::VM;
     po.mcap = 1;
     // pair sort: 32-bit keys only, with the default one-CTA cap (not under test hooks)
-    po.pair = 0;  // (k_pairsort measured slower than chunk sorts + merge passes)
+    po.pair = 0;  // (a two-CTA cluster pair sort over DSMEM measured slower)
     po.units = (Unit*)ar.alloc(buck_tot * sizeof(Unit));
     po.unit_max = 0;
     for (uint32_t c = 0; c < po.ncls; c++)
@@ -733,23 +733,6 @@ struct Engine {
     SQ_CUDA(cudaEventRecord(fork, st));
     for (int i = 0; i < SideStreams::N; i++) SQ_CUDA(cudaStreamWaitEvent(ss.s[i], fork, 0));
     int rr = 0;
-    if constexpr (!PAIRS && sizeof(K) == 4) {
-      if (po.pair) {  // buckets / chunks of 16K < len <= 32K: two-CTA clusters
-        constexpr int NT = 512, V = 32;
-        using BS = BlockSort<K, NT, V>;
-        const size_t smem = BS::SMEM_BYTES + (3 * NT + 64) * 4;
-        auto f = k_pairsort<K, NT, V>;
-        static int grid = 0;
-        if (!grid) {
-          set_smem(f, smem);
-          grid = std::max(2, wave_grid(f, NT, smem) & ~1);
-        }
-        ProfScope ps("pairsort", st);
-        f<<<(uint32_t)grid, NT, smem, st>>>(recs, dTiles, po.list + uint64_t(po.ncls + 2) * po.cap_per_list,
-                                            po.count + po.ncls + 2, kb[T], kb[X], pout, ppre, kb[2]);
-        check_launch("k_pairsort");
-      }
-    }
     for (int c = (int)po.ncls - 1; c >= 0; c--) {  // biggest classes first
       const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
       cudaStream_t cs = g_concurrent_classes ? ss.s[rr++ % SideStreams::N] : st;

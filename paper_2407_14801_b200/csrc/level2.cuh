@@ -549,7 +549,7 @@ struct PlanOut {
   MTile* mlist;           // [kMaxPasses][mcap]
   uint32_t* mcount;       // [kMaxPasses]
   uint32_t mcap;
-  // pair sort (k_pairsort): 0 = off; else buckets and chunks of max_tile < len <=
+  // pair mode (a two-CTA cluster sort, removed): 0; else buckets and chunks of max_tile < len <=
   // 2*max_tile keys go to list ncls + 2, and merge-sort chunks are 2*max_tile keys
   uint32_t pair;
   // units: consecutive buckets of one tile, each of at most max_tile keys, packed
@@ -842,134 +842,6 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
         vout[outpos + lo + i] = vs[uint32_t(x)];
       } else {
         out[outpos + lo + i] = x;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------------------
-// Pair sort (the GPU's simple_sort for 2*TILE keys, P:259-261 / P:852): a cluster of
-// two CTAs sorts one bucket (or one chunk of a merge-sorted bucket) of TILE < L <=
-// 2*TILE keys without an HBM round trip.  CTA r gathers and sorts its half on chip
-// (A = [0, h) on rank 0, B = [h, L) on rank 1, h = L/2).  The merge-path split x at
-// diagonal h says rank 0's output is A[0,x) u B[0,h-x) and rank 1's is A[x,h) u
-// B[h-x, L-h): the two CTAs swap A[x,h) and B[0,h-x) (equal sizes) through
-// distributed shared memory, arrange each tile as an ascending run followed by a
-// descending one (padding on the descending side) and finish with one guard-free
-// merge step of BlockSort.  Keys only (32-bit).
-template <typename K, int NT, int V>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 2)
-k_pairsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
-           const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
-           const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre, K* __restrict__ dst_odd) {
-  namespace cg = cooperative_groups;
-  using BS = BlockSort<K, NT, V>;
-  constexpr uint32_t TILE = BS::TILE;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* s = reinterpret_cast<K*>(smem_raw);
-  uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
-  uint32_t* s_len = s_off + NT;
-  uint32_t* s_dst = s_len + NT;
-  uint32_t* misc = s_dst + NT;
-  __shared__ uint32_t s_split;
-  cg::cluster_group cl = cg::this_cluster();
-  const uint32_t t = threadIdx.x;
-  for (uint32_t it = blockIdx.x >> 1; it < *count; it += gridDim.x >> 1) {
-    const uint32_t rank = cl.block_rank();
-    {  // gather and sort this CTA's part (only the tile stays live across the sort)
-      const uint32_t e = list[it];
-      const BucketRec rc = recs[item_bucket(e)];
-      const TileInfo ti = tiles[rc.tile];
-      const uint32_t c0 = item_chunk(e) * rc.chunk, c1 = min(rc.size, c0 + rc.chunk);
-      const uint32_t h = (c1 - c0) / 2;  // balanced halves: rank 0 [0, h), rank 1 [h, L)
-      const uint32_t lo = c0 + rank * h, len = rank ? c1 - c0 - h : h;
-      for (uint32_t i = t + len; i < TILE; i += NT) s[BS::pad(i)] = KeyTraits<K>::kMax;
-      gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, lo + len,
-                        [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
-                          for (uint32_t q = ln; q < l; q += 32) cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
-                        });
-      cp_async_wait_all();
-      __syncthreads();
-      BS::sort_smem(s, len);
-    }
-    const K* sr = cl.map_shared_rank(s, rank ^ 1);  // the partner's tile
-    const uint32_t e = list[it];
-    const BucketRec rc = recs[item_bucket(e)];
-    const uint32_t c0 = item_chunk(e) * rc.chunk, c1 = min(rc.size, c0 + rc.chunk);
-    const uint32_t h = (c1 - c0) / 2, lb = c1 - c0 - h;  // |A| = h (rank 0), |B| = lb (rank 1)
-    const uint32_t lo = c0 + rank * h, len = rank ? lb : h;
-    K* out = (rc.passes & 1) ? dst_odd : dst;
-    cl.sync();  // both tiles sorted and visible
-    // split at diagonal h: smallest i in [h - lb, h] (h - lb <= 0) with A[i] > B[h-1-i]
-    // (ties: A first); warp 0, 32-ary search over both tiles (one of them remote)
-    if (t < 32) {
-      const K* A = rank ? sr : s;
-      const K* B = rank ? s : sr;
-      uint32_t a = 0, b = h;
-      while (b > a) {
-        const uint32_t step = (b - a + 31) / 32;
-        const uint32_t p = a + t * step;
-        const bool gt = p < b ? A[BS::pad(p)] > B[BS::pad(h - 1 - p)] : true;
-        const uint32_t m = __ballot_sync(0xffffffffu, gt);
-        const uint32_t first = m ? (uint32_t)(__ffs(m) - 1) : 32u;
-        if (first == 0) b = a;
-        else {
-          const uint32_t a0 = a;
-          a = a0 + (first - 1) * step + 1;
-          b = min(b, a0 + first * step);
-        }
-      }
-      if (t == 0) s_split = a;
-    }
-    __syncthreads();
-    const uint32_t x = s_split, cnt = h - x;  // A keys moving to rank 1 = B keys moving to rank 0
-    // swap A[x, TILE) (rank 0, positions x + i) with B[0, cnt) (rank 1, positions i):
-    // each key lands at the position its counterpart leaves, so the swap runs in
-    // phases (fewer live registers), each read before the cluster barrier and
-    // written after it
-    constexpr int PH = 4, VP = V / PH;
-#pragma unroll 1
-    for (int ph = 0; ph < PH; ph++) {
-      K v[VP];
-#pragma unroll
-      for (int j = 0; j < VP; j++) {
-        const uint32_t i = t + (ph * VP + j) * NT;
-        if (i < cnt) v[j] = rank ? sr[BS::pad(x + i)] : sr[BS::pad(i)];
-      }
-      cl.sync();
-#pragma unroll
-      for (int j = 0; j < VP; j++) {
-        const uint32_t i = t + (ph * VP + j) * NT;
-        if (i < cnt) s[BS::pad(rank ? i : x + i)] = v[j];
-      }
-    }
-    cl.sync();  // no remote reads of this tile remain
-    // second run descending: rank 0 [x, TILE) = B[0, cnt) + padding;
-    // rank 1 [cnt, TILE) = B[cnt, lb) + padding
-    {
-      const uint32_t r0 = rank ? cnt : x, w = TILE - r0;
-      for (uint32_t i = t; i < w / 2; i += NT) {
-        const uint32_t p = r0 + i, q = TILE - 1 - i;
-        const K a = s[BS::pad(p)], b = s[BS::pad(q)];
-        s[BS::pad(p)] = b;
-        s[BS::pad(q)] = a;
-      }
-    }
-    __syncthreads();
-    K r[V];
-    const uint32_t tv = t * V;
-    if (tv < len) {
-      BS::merge_bitonic(s, 0, rank ? cnt : x, TILE, tv, r);
-      // straight from registers (each thread writes whole 128-byte lines)
-      K* o = out + rc.out + lo + tv;
-      if (tv + V <= len) {
-#pragma unroll
-        for (int j = 0; j < V; j++) o[j] = r[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < V; j++)
-          if (tv + j < len) o[j] = r[j];
       }
     }
     __syncthreads();
