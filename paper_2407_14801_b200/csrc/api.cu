@@ -215,6 +215,25 @@ static uint32_t tile_for(uint32_t len) {
   return 0;
 }
 
+// Launch as a programmatic dependent of the previous kernel in the stream (it may
+// start before that one finishes; it must execute griddepcontrol.wait before it
+// touches that kernel's outputs).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*f)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SQ_CUDA(cudaLaunchKernelEx(&cfg, f, std::forward<Args>(args)...));
+}
+
 template <typename F>
 static void set_smem(F f, size_t bytes) {
   SQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -555,6 +574,11 @@ struct Engine {
     SQ_CUDA(cudaMemsetAsync(segmin, 0xff, ns * sizeof(K), st));
     SQ_CUDA(cudaMemsetAsync(segmat, 0, segmat_tot * 4, st));
 
+    // column descriptors go up first: nothing but kernels may sit between the sampler,
+    // the round selection and the column sort (programmatic dependent launch)
+    std::vector<std::pair<uint32_t, const ColDesc*>> coldesc;
+    if (!generic)
+      for (auto& kv : colcls) coldesc.push_back({kv.first, ar.upload(kv.second)});
     // 1. pivots: all rounds in parallel from the level input (L9)
     with_tile<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
       constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
@@ -567,23 +591,33 @@ struct Engine {
     });
     {
       ProfScope ps("select", st);
-      k_select_round<K><<<ns, 256, 0, st>>>(dL, ns, cand, flags, p0s, segmin, piv, info, fix, 0);
-      check_launch("k_select_round");
+      launch_pdl(k_select_round<K>, ns, 256, 0, st, dL, ns, (const K*)cand, (const uint8_t*)flags, (const K*)p0s,
+                 (const K*)segmin, piv, info, fix, 0);
     }
-    // 2. sort every column in place + tile boundaries + min(D)
+    // 2. sort every column in place + tile boundaries + min(D).  The first
+    // class launches as a programmatic dependent: its CTAs load and sort while the
+    // sampler and the round selection still run, and wait for them (griddepcontrol)
+    // before writing keys back (the sampler reads the unsorted level input) and
+    // before reading the pivots.
     if (!generic) {
-      for (auto& kv : colcls) {
-        const ColDesc* dc = ar.upload(kv.second);
-        with_tile<SK>(kv.first, [&](auto nt, auto v) {
+      bool first = true;
+      for (auto& cd : coldesc) {
+        const uint32_t ncol = (uint32_t)colcls[cd.first].size();
+        with_tile<SK>(cd.first, [&](auto nt, auto v) {
           constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
           using BS = BlockSort<SK, NT, V>;
           const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
           static bool init = false;
           if (!init) { set_smem(k_colsort<K, NT, V, PAIRS>, smem); init = true; }
           ProfScope ps("colsort", st);
-          k_colsort<K, NT, V, PAIRS><<<(uint32_t)kv.second.size(), NT, smem, st>>>(
-              dc, dL, kb[X], PAIRS ? vb[X] : nullptr, piv, segmat, segmin);
+          auto f = k_colsort<K, NT, V, PAIRS>;
+          if (first && !g_prof.load())
+            launch_pdl(f, ncol, NT, smem, st, cd.second, (const LevelSeg*)dL, kb[X], PAIRS ? vb[X] : nullptr,
+                       (const K*)piv, segmat, segmin);
+          else
+            f<<<ncol, NT, smem, st>>>(cd.second, dL, kb[X], PAIRS ? vb[X] : nullptr, piv, segmat, segmin);
           check_launch("k_colsort");
+          first = false;
         });
       }
     } else {  // columns longer than a CTA holds: a recursive level sorts them

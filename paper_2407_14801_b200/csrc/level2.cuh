@@ -79,6 +79,7 @@ k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* _
   using BS = BlockSort<K, NT, V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the selection may launch now
   const uint32_t seg = blockIdx.x / kCap, r = blockIdx.x % kCap;
   const LevelSeg sg = segs[seg];
   const uint32_t np = sg.k - 1;
@@ -113,6 +114,10 @@ __global__ void k_select_round(const LevelSeg* __restrict__ segs, uint32_t nseg,
                                const uint8_t* __restrict__ flags, const K* __restrict__ p0s,
                                const K* __restrict__ segmin, K* __restrict__ piv, uint32_t* __restrict__ info,
                                uint32_t* __restrict__ fix, int mode) {
+  // launched as a programmatic dependent: let the column sort start, then wait for
+  // the sampler (and, in mode 1, for the column sort)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const uint32_t seg = blockIdx.x;
   const LevelSeg sg = segs[seg];
   __shared__ uint32_t sel, change;
@@ -174,6 +179,9 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   }
   __syncthreads();
   BS::sort_smem(s, d.len);
+  // (programmatic dependent launch) the sampler must be done reading the unsorted
+  // input, and the pivots must be selected, before this CTA writes or reads them
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   auto key_at = [&](int i) -> K {
     if constexpr (PAIRS) return K(s[BS::pad(i)] >> 32);
     else return s[BS::pad(i)];
