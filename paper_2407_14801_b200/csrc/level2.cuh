@@ -165,17 +165,34 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
   const ColDesc d = cols[blockIdx.x];
   const LevelSeg sg = segs[d.seg];
-  for (int i = threadIdx.x; i < BS::TILE; i += NT) {
-    SK x = KeyTraits<SK>::kMax;
-    if (i < (int)d.len) {
-      if constexpr (PAIRS) {
-        x = (uint64_t(keys[d.off + i]) << 32) | uint32_t(i);
-        vs[i] = vals[d.off + i];
-      } else {
-        x = keys[d.off + i];
-      }
+  constexpr int VW = 16 / sizeof(K), NV = BS::TILE / (NT * VW);  // 16-byte vectors per thread
+  constexpr bool VEC = !PAIRS && NV >= 1 && NV * NT * VW == BS::TILE;
+  if (VEC && d.len == BS::TILE && (reinterpret_cast<uintptr_t>(keys + d.off) & 15) == 0) {
+    // full, aligned column: every vector load in flight before the first store
+    const uint4* g = reinterpret_cast<const uint4*>(keys + d.off);
+    uint4 v[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int q = 0; q < NV; q++) v[q] = g[threadIdx.x + q * NT];
+#pragma unroll
+    for (int q = 0; q < NV; q++) {
+      const uint32_t i0 = (threadIdx.x + q * NT) * VW;
+      const K* e = reinterpret_cast<const K*>(&v[q]);
+#pragma unroll
+      for (int j = 0; j < VW; j++) s[BS::pad(i0 + j)] = SK(e[j]);
     }
-    s[BS::pad(i)] = x;
+  } else {
+    for (int i = threadIdx.x; i < BS::TILE; i += NT) {
+      SK x = KeyTraits<SK>::kMax;
+      if (i < (int)d.len) {
+        if constexpr (PAIRS) {
+          x = (uint64_t(keys[d.off + i]) << 32) | uint32_t(i);
+          vs[i] = vals[d.off + i];
+        } else {
+          x = keys[d.off + i];
+        }
+      }
+      s[BS::pad(i)] = x;
+    }
   }
   __syncthreads();
   BS::sort_smem(s, d.len);
