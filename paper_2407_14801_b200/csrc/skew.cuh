@@ -532,10 +532,14 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + C::off_cnt);  // [bucket][thread], + a dummy row
   uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
   uint32_t* poff = misc + 64;
+  // cswz(bucket * NC + t) == bucket * NC + (t ^ (warp << 2)) since NC is a multiple of 256
+  static_assert(NC % 256 == 0, "swizzle");
+  const uint32_t tsw = t ^ (((t >> 5) & 7) << 2);
   uint32_t k = 0;
   for (uint32_t i = blockIdx.x; i < npieces; i += gridDim.x, k++) {
     const int b = k % NS;
-    for (int q = t; q < 33 * NC; q += NC) cnt[q] = 0;  // 32 bucket rows + the dummy row
+    for (int q = t; q < 33 * NC / 4; q += NC)  // 32 bucket rows + the dummy row
+      reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
     mbar_wait(&full[b], (k / NS) & 1);
     cons_bar();
     const K* slot = reinterpret_cast<const K*>(sm + C::off_slot + b * C::SLOT_B);
@@ -591,7 +595,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
         for (int st = 16; st >= 1; st >>= 1) bk += thr[bk + st - 1].passed(x) ? st : 0;
       }
       bk = ((vb >> j) & 1) ? bk : 32u;
-      const uint32_t r = atomicAdd(&cnt[cswz(bk * NC + t)], 1u);
+      const uint32_t r = atomicAdd(&cnt[bk * NC + tsw], 1u);
       const uint32_t c = bk | (r << 6);
       if (j & 1) cdp[j / 2] |= c << 16;
       else cdp[j / 2] = c;
@@ -633,7 +637,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
       const uint32_t c = (cdp[j / 2] >> (16 * (j & 1))) & 0xffffu;
       const uint32_t bk = c & 63;
       if (bk < 32) {
-        const uint32_t dpos = cnt[cswz(bk * NC + t)] + (c >> 6);
+        const uint32_t dpos = cnt[bk * NC + tsw] + (c >> 6);
         outb[dpos] = xs[j];
         if (PAIRS) vout[dpos] = vslot[w0 + j];
       }
