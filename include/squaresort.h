@@ -77,6 +77,26 @@ int sq_sort_u64_host(uint64_t *keys, size_t n, uint64_t seed, void *stream);
 int sq_sort_pairs_u32_u32_host(uint32_t *keys, uint32_t *vals, size_t n, uint64_t seed,
                                void *stream);
 
+/* A batch of `count` independent sorts of n HOST keys each: item i reads
+ * in[i] and writes the ascending result to out[i] (in[i] == out[i] sorts in
+ * place; several items may share one input buffer).  The items are
+ * pipelined: the host->device copy of item i+1 and the device->host copy of
+ * item i-1 run on two library-owned copy streams while item i sorts on
+ * `stream`, so with pinned buffers the batch costs about
+ * max(copy in, sort, copy out) per item instead of their sum.  Up to three
+ * device buffers of n keys are allocated for the call.  Each item is the same
+ * operation as sq_sort_u32_host / sq_sort_u64_host (same seed).
+ * Requirements: in, out and every in[i], out[i] non-NULL when count > 0;
+ * out[i] must not overlap in[j] for any j > i (a later item's input).
+ * Outputs may be reused: copies out run in item order, so where out[i] and
+ * out[j] (i < j) overlap, item j's result is what remains.
+ * Returns on completion (all items copied out) or at the first error; on
+ * error the contents of out[] are unspecified. */
+int sq_sort_u32_host_batch(const uint32_t *const *in, uint32_t *const *out, size_t n,
+                           size_t count, uint64_t seed, void *stream);
+int sq_sort_u64_host_batch(const uint64_t *const *in, uint64_t *const *out, size_t n,
+                           size_t count, uint64_t seed, void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* SkewTranspose exactly as Alg 2/3 define it.        */
 /* ------------------------------------------------------------------------- */

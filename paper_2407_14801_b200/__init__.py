@@ -20,7 +20,8 @@ SQ_FLAG_VALIDATE = 1
 STATUS = {0: "SQ_OK", 1: "SQ_ERR_INVALID_ARGUMENT", 2: "SQ_ERR_OUT_OF_MEMORY", 3: "SQ_ERR_CUDA",
           4: "SQ_ERR_PRECONDITION", 5: "SQ_ERR_UNSUPPORTED_DEVICE"}
 EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_host",
-           "sq_sort_u64_host", "sq_sort_pairs_u32_u32_host", "sq_skew_transpose",
+           "sq_sort_u64_host", "sq_sort_pairs_u32_u32_host", "sq_sort_u32_host_batch",
+           "sq_sort_u64_host_batch", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode"]
 
@@ -61,6 +62,9 @@ def lib():
             getattr(L, f).restype = ctypes.c_int
         for f in ("sq_sort_pairs_u32_u32", "sq_sort_pairs_u32_u32_host"):
             getattr(L, f).argtypes = [vp, vp, sz, u64, vp]
+            getattr(L, f).restype = ctypes.c_int
+        for f in ("sq_sort_u32_host_batch", "sq_sort_u64_host_batch"):
+            getattr(L, f).argtypes = [vp, vp, sz, sz, u64, vp]
             getattr(L, f).restype = ctypes.c_int
         L.sq_skew_transpose.argtypes = [vp, vp, sz, sz, ctypes.POINTER(SkewParams), vp]
         L.sq_skew_transpose.restype = ctypes.c_int
@@ -180,6 +184,32 @@ def sort_pairs_u32_u32_host(keys, vals, seed: int = 0, stream=None):
     _check(lib().sq_sort_pairs_u32_u32_host(_host_ptr(keys, np.uint32), _host_ptr(vals, np.uint32),
                                             keys.size, _seed(seed), _stream(stream)))
     return keys, vals
+
+
+def _host_batch(fn, ins, outs, dtype, seed, stream):
+    if len(ins) != len(outs):
+        raise ValueError("ins and outs differ in length")
+    n = ins[0].size if ins else 0
+    for a in list(ins) + list(outs):
+        _host_ptr(a, dtype)
+        if a.size != n:
+            raise ValueError("all batch items must have the same length")
+    arr = ctypes.c_void_p * max(1, len(ins))
+    pi = arr(*[a.ctypes.data for a in ins])
+    po = arr(*[a.ctypes.data for a in outs])
+    _check(fn(pi, po, n, len(ins), _seed(seed), _stream(stream)))
+    return outs
+
+
+def sort_u32_host_batch(ins, outs, seed: int = 0, stream=None):
+    """Pipelined batch: outs[i] <- sorted(ins[i]) (numpy uint32 arrays, ideally pinned)."""
+    import numpy as np
+    return _host_batch(lib().sq_sort_u32_host_batch, ins, outs, np.uint32, seed, stream)
+
+
+def sort_u64_host_batch(ins, outs, seed: int = 0, stream=None):
+    import numpy as np
+    return _host_batch(lib().sq_sort_u64_host_batch, ins, outs, np.uint64, seed, stream)
 
 
 # ------------------------------------------------------------------ introspection

@@ -134,6 +134,29 @@ static void check_device() {
   }
 }
 
+// ------------------------------------------------------------------ small transfers
+// Descriptor uploads and size read-backs between pinned (UVA-mapped) host
+// staging and device memory are done by SM loads/stores, not by the copy
+// engines: a 1 GB copy of another batch item queued on a copy engine would
+// otherwise hold the sort's few-KB transfers back (sq_sort_*_host_batch).
+__global__ void k_xfer(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, size_t bytes) {
+  const size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x, T = size_t(gridDim.x) * blockDim.x;
+  if (((uintptr_t(src) | uintptr_t(dst)) & 15) == 0) {
+    const size_t n16 = bytes >> 4;
+    for (size_t i = t; i < n16; i += T) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = (n16 << 4) + t; i < bytes; i += T) dst[i] = src[i];
+  } else {
+    for (size_t i = t; i < bytes; i += T) dst[i] = src[i];
+  }
+}
+
+static void xfer(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  const uint32_t g = (uint32_t)std::min<size_t>((bytes + 4095) / 4096, 148);
+  k_xfer<<<g, 256, 0, st>>>((const uint8_t*)src, (uint8_t*)dst, bytes);
+  check_launch("k_xfer");
+}
+
 // ------------------------------------------------------------------ per-call memory
 // Pinned host staging for descriptor uploads and size read-backs: one bump
 // pool per host thread, reused across calls (page-locking is expensive).
@@ -189,7 +212,7 @@ struct Arena {
     if (!v.empty()) {
       T* h = (T*)pinned(v.size() * sizeof(T));
       memcpy(h, v.data(), v.size() * sizeof(T));
-      SQ_CUDA(cudaMemcpyAsync(d, h, v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+      xfer(d, h, v.size() * sizeof(T), st);
     }
     return d;
   }
@@ -834,8 +857,8 @@ struct Engine {
     // 7. one host read per level: the oversize list (and the round, for stats)
     uint32_t* hcnt = (uint32_t*)ar.pinned((po.ncls + 2) * 4);
     uint32_t* hinfo = (uint32_t*)ar.pinned(4);
-    SQ_CUDA(cudaMemcpyAsync(hcnt, po.count, (po.ncls + 2) * 4, cudaMemcpyDeviceToHost, st));
-    SQ_CUDA(cudaMemcpyAsync(hinfo, info, 4, cudaMemcpyDeviceToHost, st));
+    xfer(hcnt, po.count, (po.ncls + 2) * 4, st);
+    xfer(hinfo, info, 4, st);
     SQ_CUDA(cudaStreamSynchronize(st));
     g_stats.host_syncs++;
     if (depth == 0) {
@@ -846,14 +869,14 @@ struct Engine {
     const uint32_t nos = hcnt[po.ncls + 1];
     std::vector<Seg> over;
     if (nos) {
-      std::vector<uint32_t> hl(nos);
-      SQ_CUDA(cudaMemcpyAsync(hl.data(), po.list + uint64_t(po.ncls + 1) * po.cap_per_list, nos * 4,
-                              cudaMemcpyDeviceToHost, st));
-      std::vector<BucketRec> hr(buck_tot);
-      SQ_CUDA(cudaMemcpyAsync(hr.data(), recs, buck_tot * sizeof(BucketRec), cudaMemcpyDeviceToHost, st));
+      uint32_t* hl = (uint32_t*)ar.pinned(nos * 4);
+      xfer(hl, po.list + uint64_t(po.ncls + 1) * po.cap_per_list, nos * 4, st);
+      BucketRec* hr = (BucketRec*)ar.pinned(buck_tot * sizeof(BucketRec));
+      xfer(hr, recs, buck_tot * sizeof(BucketRec), st);
       SQ_CUDA(cudaStreamSynchronize(st));
       g_stats.host_syncs++;
-      for (uint32_t e : hl) {
+      for (uint32_t q = 0; q < nos; q++) {
+        const uint32_t e = hl[q];
         const uint32_t i = item_bucket(e);
         over.push_back({hr[i].out, hr[i].size, hr[i].node});
         g_stats.oversize_keys += hr[i].size;
@@ -936,6 +959,81 @@ static int sort_entry(K* keys, uint32_t* vals, size_t n, uint64_t seed, void* st
   });
 }
 
+// Pipelined batch of host sorts (sq_sort_*_host_batch): item i's sort on `st`
+// overlaps the H2D copy of item i+1 and the D2H copy of item i-1, each on a
+// library-owned non-blocking copy stream.  Three device buffers rotate, so a
+// buffer's copy-in -> sort -> copy-out cycle (~2 copies + 1 sort) spans three
+// items and the steady state is bound by the copies alone.
+template <typename K>
+static int batch_entry(const K* const* in, K* const* out, size_t n, size_t count, uint64_t seed, void* stream) {
+  struct Res {
+    cudaStream_t st = nullptr, cs[2] = {nullptr, nullptr};
+    cudaEvent_t ev[10] = {};
+    K* buf[3] = {nullptr, nullptr, nullptr};
+    ~Res() {
+      for (auto s : cs)
+        if (s) cudaStreamSynchronize(s);
+      cudaStreamSynchronize(st);
+      for (auto b : buf)  // back to the pool (kept, release threshold = max)
+        if (b) cudaFreeAsync(b, st);
+      cudaStreamSynchronize(st);
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+      for (auto s : cs)
+        if (s) cudaStreamDestroy(s);
+    }
+  };
+  return guarded([&] {
+    if (count == 0) return;
+    need(in != nullptr && out != nullptr, "in/out is NULL");
+    need(n <= (sizeof(K) == 4 ? (size_t(1) << 30) : (size_t(1) << 28)), "n exceeds the supported maximum");
+    const size_t bytes = n * sizeof(K);
+    for (size_t i = 0; i < count; ++i) {
+      need(in[i] != nullptr && out[i] != nullptr, "in[i]/out[i] is NULL");
+      for (size_t j = i + 1; j < count && count <= 4096; ++j)
+        need(!overlap(out[i], bytes, in[j], bytes), "out[i] overlaps in[j] with j > i");
+    }
+    if (n <= 1) {
+      for (size_t i = 0; i < count; ++i)
+        if (n == 1 && out[i] != in[i]) out[i][0] = in[i][0];
+      return;
+    }
+    check_device();
+    cudaStream_t st = (cudaStream_t)stream;
+    Res r;
+    r.st = st;
+    for (auto& s : r.cs) SQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (auto& e : r.ev) SQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int b = 0; b < int(std::min<size_t>(count, 3)); b++) SQ_CUDA(cudaMallocAsync((void**)&r.buf[b], bytes, st));
+    cudaStream_t h2d = r.cs[0], d2h = r.cs[1];
+    SQ_CUDA(cudaEventRecord(r.ev[9], st));  // the buffers exist
+    SQ_CUDA(cudaStreamWaitEvent(h2d, r.ev[9], 0));
+    cudaEvent_t* in_done = r.ev;        // [3]: buffer b holds item i's input
+    cudaEvent_t* sorted = r.ev + 3;     // [3]: item in buffer b is sorted
+    cudaEvent_t* out_done = r.ev + 6;   // [3]: buffer b has been copied out
+    auto copy_in = [&](size_t i) {
+      const int b = int(i % 3);
+      if (i >= 3) SQ_CUDA(cudaStreamWaitEvent(h2d, out_done[b], 0));
+      SQ_CUDA(cudaMemcpyAsync(r.buf[b], in[i], bytes, cudaMemcpyHostToDevice, h2d));
+      SQ_CUDA(cudaEventRecord(in_done[b], h2d));
+    };
+    copy_in(0);
+    for (size_t i = 0; i < count; ++i) {
+      const int b = int(i % 3);
+      if (i + 1 < count) copy_in(i + 1);  // enqueued before the sort's host waits
+      SQ_CUDA(cudaStreamWaitEvent(st, in_done[b], 0));
+      sort_device<K, false>(r.buf[b], nullptr, n, seed, st);
+      SQ_CUDA(cudaEventRecord(sorted[b], st));
+      SQ_CUDA(cudaStreamWaitEvent(d2h, sorted[b], 0));
+      SQ_CUDA(cudaMemcpyAsync(out[i], r.buf[b], bytes, cudaMemcpyDeviceToHost, d2h));
+      SQ_CUDA(cudaEventRecord(out_done[b], d2h));
+    }
+    SQ_CUDA(cudaStreamSynchronize(d2h));
+    SQ_CUDA(cudaStreamSynchronize(h2d));
+    SQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 }  // namespace sq
 
 using namespace sq;
@@ -959,6 +1057,14 @@ int sq_sort_u64_host(uint64_t* keys, size_t n, uint64_t seed, void* stream) {
 }
 int sq_sort_pairs_u32_u32_host(uint32_t* keys, uint32_t* vals, size_t n, uint64_t seed, void* stream) {
   return sort_entry<uint32_t, true>(keys, vals, n, seed, stream, true);
+}
+int sq_sort_u32_host_batch(const uint32_t* const* in, uint32_t* const* out, size_t n, size_t count, uint64_t seed,
+                           void* stream) {
+  return batch_entry<uint32_t>(in, out, n, count, seed, stream);
+}
+int sq_sort_u64_host_batch(const uint64_t* const* in, uint64_t* const* out, size_t n, size_t count, uint64_t seed,
+                           void* stream) {
+  return batch_entry<uint64_t>(in, out, n, count, seed, stream);
 }
 
 int sq_skew_transpose(const uint32_t* src, uint32_t* dst, size_t rows, size_t cols, const sq_skew_params* p,

@@ -73,6 +73,13 @@ def test_argument_errors_without_gpu(libpath):
     p = sq.SkewParams(None, 1, 0, None, ctypes.c_void_p(64), 4, 0)
     assert L.sq_skew_transpose(ctypes.c_void_p(4096), ctypes.c_void_p(4100), 4, 4,
                                ctypes.byref(p), None) == 1  # overlap
+    arr = ctypes.c_void_p * 2
+    a, b = arr(4096, 1 << 20), arr(1 << 24, (1 << 24) + 64)
+    assert L.sq_sort_u32_host_batch(a, b, 10, 0, 0, None) == 0  # count = 0 is a no-op
+    assert L.sq_sort_u32_host_batch(None, b, 10, 2, 0, None) == 1
+    assert L.sq_sort_u32_host_batch(a, arr(1 << 24, 0), 10, 2, 0, None) == 1  # NULL item
+    assert L.sq_sort_u64_host_batch(a, arr((1 << 20) + 8, 1 << 24), 10, 2, 0, None) == 1  # out[0] overlaps in[1]
+    assert L.sq_sort_u32_host(None, 10, 0, None) == 1
     assert L.sq_set_max_tile(100) == 1 and L.sq_set_max_tile(0) == 0
     assert L.sq_last_error_message() is not None
 

@@ -232,6 +232,34 @@ def test_host_entry_points():
     assert np.array_equal(h64, np.sort(k64))
 
 
+def test_host_batch_entry_points():
+    # pipelined batch: distinct inputs, a shared input, an in-place item, a ragged n
+    import torch
+    n = 300001
+    ins = [S.generate("uniform_u32", n, s)[0] for s in (1, 2)]
+    pin = [torch.empty(n, dtype=torch.uint32).pin_memory().numpy() for _ in range(4)]
+    for p, a in zip(pin, ins + ins):
+        np.copyto(p, a)
+    outs = [np.empty(n, np.uint32) for _ in range(3)] + [pin[3]]
+    sq.sort_u32_host_batch([pin[0], pin[1], pin[0], pin[3]], outs, 4)
+    for o, a in zip(outs, [ins[0], ins[1], ins[0], ins[1]]):
+        assert np.array_equal(o, np.sort(a))
+    # a reused output keeps the last item's result
+    r = np.empty(n, np.uint32)
+    sq.sort_u32_host_batch([pin[0], pin[1], pin[0], pin[1]], [r, pin[2], r, pin[2]], 4)
+    assert np.array_equal(r, np.sort(ins[0])) and np.array_equal(pin[2], np.sort(ins[1]))
+    assert np.array_equal(pin[0], ins[0])  # inputs untouched
+    k64 = [S.generate("dup1000_u64", 70001, s)[0] for s in (3, 4, 5)]
+    o64 = [np.empty_like(k) for k in k64]
+    sq.sort_u64_host_batch(k64, o64, 9)
+    for o, a in zip(o64, k64):
+        assert np.array_equal(o, np.sort(a))
+    one = [np.array([7], np.uint32)]
+    o1 = [np.zeros(1, np.uint32)]
+    sq.sort_u32_host_batch(one, o1)
+    assert o1[0][0] == 7
+
+
 # ---------------------------------------------------------------- one level vs the oracle's level
 @pytest.mark.parametrize("n,card", [(1 << 16, 2**32), (1 << 20, 2**32), (100003, 2**32),
                                     (1 << 16, 1000), (50000, 7)])
