@@ -142,7 +142,7 @@ __device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
       if ((i & d) == 0) cas(r[i], r[i + d]);
 }
 
-template <typename K, int NT_, int V_>
+template <typename K, int NT_, int V_, int WGM_ = 16>
 struct BlockSort {
   static constexpr int NT = NT_;
   static constexpr int V = V_;
@@ -207,6 +207,13 @@ struct BlockSort {
     }
   }
 
+  // lanes per run after the warp-shuffle merge levels (a merge pass costs about
+  // as much per key as a warp level of 16-32 lanes; measured: 32 for the column
+  // sorts, 16 for the bucket sorts, whose partial tiles carry padding)
+  static constexpr int WGMAX = WGM_;
+  static constexpr int WG = (NT >= WGMAX && TILE >= WGMAX * V) ? WGMAX
+                            : (NT >= 4 && TILE >= 4 * V) ? 4 : (NT >= 2 && TILE >= 2 * V) ? 2 : 1;
+
   // Keys at positions >= len are padding (kMax).  Sorted, every position >= len holds
   // kMax after every merge pass, so threads whose whole block lies there skip the
   // work (and warps entirely in the padding skip the register stages).
@@ -220,15 +227,17 @@ struct BlockSort {
         for (int j = 0; j < V; j++) r[j] = sb[poff(j)];
       }
       thread_sort<K, V>(r);
-      // the first two merge levels (runs of V -> 2V -> 4V keys) stay in registers
-      constexpr uint32_t WL0 = (TILE >= 4 * V && NT >= 4) ? 4 * V : ((TILE >= 2 * V && NT >= 2) ? 2 * V : V);
-      if constexpr (WL0 >= 2 * V) warp_bitonic_merge<K, V, 2>(r);
-      if constexpr (WL0 >= 4 * V) warp_bitonic_merge<K, V, 4>(r);
+      // the first merge levels (runs of V -> 2V -> ... -> WG*V keys) stay in registers
+      if constexpr (WG >= 2) warp_bitonic_merge<K, V, 2>(r);
+      if constexpr (WG >= 4) warp_bitonic_merge<K, V, 4>(r);
+      if constexpr (WG >= 8) warp_bitonic_merge<K, V, 8>(r);
+      if constexpr (WG >= 16) warp_bitonic_merge<K, V, 16>(r);
+      if constexpr (WG >= 32) warp_bitonic_merge<K, V, 32>(r);
     } else {
 #pragma unroll
       for (int j = 0; j < V; j++) r[j] = KeyTraits<K>::kMax;
     }
-    constexpr uint32_t WL = (TILE >= 4 * V && NT >= 4) ? 4 * V : ((TILE >= 2 * V && NT >= 2) ? 2 * V : V);
+    constexpr uint32_t WL = WG * V;
 #pragma unroll 1
     for (uint32_t w = WL; w < (uint32_t)TILE; w *= 2) {  // w is a power of two
       // Runs of width w: run A = [a0, b0) ascending, run B = [b0, bend) stored

@@ -159,7 +159,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
           uint32_t* __restrict__ vals, const K* __restrict__ piv, uint32_t* __restrict__ segmat,
           K* __restrict__ segmin) {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
-  using BS = BlockSort<SK, NT, V>;
+  using BS = BlockSort<SK, NT, V, 32>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SK* s = reinterpret_cast<SK*>(smem_raw);
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);

@@ -12,7 +12,8 @@ ROLE = [("k_colsort", "colsort"), ("k_transpose", "transpose"), ("k_bucketsort",
         ("k_merge_pass", "merge"), ("k_merge_split", "merge"), ("k_pairsort", "pairsort"), ("k_clustersort", "clustersort"), ("k_sample", "sample"),
         ("k_select", "select"), ("k_segmat", "segmat"), ("k_tile", "tiles"), ("k_piece_plan", "tiles"),
         ("k_bucket_sizes", "plan"), ("k_bucket_offsets", "plan"), ("k_bucket_plan", "plan"),
-        ("k_bucket_gather", "gather"), ("k_blocksort", "smallsort"), ("k_colmin", "colmin")]
+        ("k_bucket_gather", "gather"), ("k_blocksort", "smallsort"), ("k_colmin", "colmin"),
+        ("k_unit_plan", "plan"), ("k_xfer", "xfer")]
 
 
 def role_of(name):
