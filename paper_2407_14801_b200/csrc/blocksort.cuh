@@ -193,11 +193,20 @@ struct BlockSort {
     K o = lb ? s[pad(pb)] : KeyTraits<K>::kMax;
     bool L = true;                      // h belongs to A
     uint32_t na = pa + 1, nb = pb - 1;  // the index each run reads next
+    const uint32_t one = (uint32_t)c_one, mone = (uint32_t)c_mone;
 #pragma unroll
     for (int k = 0; k < V; k++) {
       const bool takeL = h <= o;
       r[k] = takeL ? h : o;
-      const K mx = takeL ? o : h;
+      K mx;
+      if constexpr (sizeof(K) == 4) {  // max = h + o - min on the FMA pipe (the ALU pipe is the bound)
+        uint32_t sum, m;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(sum) : "r"(uint32_t(h)), "r"(one), "r"(uint32_t(o)));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(m) : "r"(uint32_t(r[k])), "r"(mone), "r"(sum));
+        mx = K(m);
+      } else {
+        mx = takeL ? o : h;
+      }
       L = takeL ? L : !L;  // the run taken from
       const uint32_t idx = L ? na : nb;
       if (L) na = idx + 1;
