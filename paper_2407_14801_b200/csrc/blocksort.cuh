@@ -142,7 +142,7 @@ __device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
       if ((i & d) == 0) cas(r[i], r[i + d]);
 }
 
-template <typename K, int NT_, int V_, int WGM_ = 16>
+template <typename K, int NT_, int V_, int WGM_ = 32>
 struct BlockSort {
   static constexpr int NT = NT_;
   static constexpr int V = V_;
@@ -217,8 +217,7 @@ struct BlockSort {
   }
 
   // lanes per run after the warp-shuffle merge levels (a merge pass costs about
-  // as much per key as a warp level of 16-32 lanes; measured: 32 for the column
-  // sorts, 16 for the bucket sorts, whose partial tiles carry padding)
+  // as much per key as a warp level of 16-32 lanes; 32 measured best)
   static constexpr int WGMAX = WGM_;
   static constexpr int WG = (NT >= WGMAX && TILE >= WGMAX * V) ? WGMAX
                             : (NT >= 4 && TILE >= 4 * V) ? 4 : (NT >= 2 && TILE >= 2 * V) ? 2 : 1;
@@ -267,8 +266,16 @@ struct BlockSort {
         const uint32_t q = rev ? 2 * r0 + rlen - V - tv : tv;
         K* sb = s + pad(q);
         __syncthreads();  // previous readers of s are done
+        if (w < 32 * V) {  // rev differs within a warp: per-key selects
 #pragma unroll
-        for (int j = 0; j < V; j++) sb[poff(j)] = rev ? r[V - 1 - j] : r[j];
+          for (int j = 0; j < V; j++) sb[poff(j)] = rev ? r[V - 1 - j] : r[j];
+        } else if (rev) {  // warp-uniform: no selects
+#pragma unroll
+          for (int j = 0; j < V; j++) sb[poff(j)] = r[V - 1 - j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; j++) sb[poff(j)] = r[j];
+        }
         __syncthreads();
       }
       if (tv >= len) continue;  // r[] stays all kMax

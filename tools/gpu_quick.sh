@@ -1,5 +1,5 @@
 #!/bin/bash
 # GPU-box quick check: parity tests + a short bench line (kernel ms per step).
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
-timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench.log 2>&1
+timeout 300 python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench.log 2>&1
 tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],2), 'Gkeys/s', round(d['ms_per_step'],3), 'ms', {k: round(v,3) for k,v in d['kernels_ms_per_step'].items()}, d['output_check'])"
