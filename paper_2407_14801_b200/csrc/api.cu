@@ -678,13 +678,16 @@ struct Engine {
     }
     {
       PieceDesc* pieces = (PieceDesc*)ar.alloc(piece_tot * sizeof(PieceDesc));
-      uint32_t* pcount = (uint32_t*)ar.alloc(16);
-      SQ_CUDA(cudaMemsetAsync(pcount, 0, 4, st));
+      uint32_t* pcount = (uint32_t*)ar.alloc(16);  // [0] pieces, [1] tile tickets
+      SQ_CUDA(cudaMemsetAsync(pcount, 0, 8, st));
+      unsigned long long* pstatus = (unsigned long long*)ar.alloc(uint64_t(ntiles) * 8);
+      SQ_CUDA(cudaMemsetAsync(pstatus, 0, uint64_t(ntiles) * 8, st));
       {
         ProfScope ps("tiles", st);
-        k_piece_plan2<256, TC::S, kPlanFW><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout);
+        k_piece_plan2<256, TC::S, kPlanFW><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout, pstatus);
         check_launch("k_piece_plan2");
       }
+      ar.release(pstatus);
       using XC = WsCfg<K, PAIRS, TC::S, TC::F>;
       auto f = k_transpose_ws<K, PAIRS, TC::S, TC::F>;
       static int grid = 0;

@@ -433,18 +433,50 @@ struct __align__(16) PieceDesc {
 // consecutive columns; a window of T keys gives ceil(T / S) pieces (one for the
 // usual T <= S), cut at stream positions that are multiples of S.  CTA per tile;
 // warps work on windows independently (no serial chain over the tile).
+// Dense list position of a tile's pieces: decoupled look-back over the tiles in
+// ticket order (status[i] = flag << 62 | value; flag 1 = aggregate, 2 = inclusive
+// prefix).  Tickets are taken at CTA start, so every lower ticket belongs to a CTA
+// that is already running and never waits on a higher one.
+__device__ __forceinline__ uint32_t piece_lookback(unsigned long long* status, uint32_t idx, uint32_t agg) {
+  constexpr unsigned long long A = 1ull << 62, P = 2ull << 62, M = (1ull << 62) - 1;
+  if (idx == 0) {
+    atomicExch(&status[0], P | agg);
+    return 0;
+  }
+  atomicExch(&status[idx], A | agg);
+  unsigned long long sum = 0;
+  for (int j = int(idx) - 1;; j--) {
+    unsigned long long v;
+    do {
+      v = *reinterpret_cast<volatile unsigned long long*>(&status[j]);
+    } while (!(v >> 62));
+    sum += v & M;
+    if ((v >> 62) == 2) break;
+  }
+  atomicExch(&status[idx], P | (sum + agg));
+  return uint32_t(sum);
+}
+
+// The pieces are listed in tile order: the transpose takes list positions in
+// order, so the two pieces that share a column's boundary sectors (tiles bt and
+// bt+1 of one window) run close together in time and the shared sectors are read
+// from DRAM once (an arbitrary tile order doubled the transpose's DRAM reads).
 template <int NT, int S, int FW>
 __global__ void __launch_bounds__(NT)
 k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const uint32_t* __restrict__ segmat,
-              PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pcount, uint32_t* __restrict__ pout) {
+              PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pcount, uint32_t* __restrict__ pout,
+              unsigned long long* __restrict__ status) {
   constexpr int NW = NT / 32, PL = (FW + 31) / 32;  // columns per lane within a window
   constexpr uint32_t MAXW = 1024;                    // windows per chunk
   static_assert(FW <= 128, "window");
   __shared__ uint32_t wtot[MAXW], wpc[MAXW], woff[MAXW], wpb[MAXW];
   __shared__ uint32_t misc[64];
-  __shared__ uint32_t base, carry_o, carry_p;
+  __shared__ uint32_t base, carry_o, carry_p, tix;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const TileInfo ti = tiles[blockIdx.x];
+  if (t == 0) tix = atomicAdd(&pcount[1], 1u);
+  __syncthreads();
+  const uint32_t me = tix;
+  const TileInfo ti = tiles[me];
   const LevelSeg sg = segs[ti.seg];
   const uint32_t bt = ti.bt, rstride = sg.ncols;  // tile-major segmat: (bt+1, c) is ncols after (bt, c)
   const uint32_t* rows = segmat + sg.segmat_base + uint64_t(bt) * sg.ncols;
@@ -458,6 +490,26 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
   if (t == 0) {
     carry_o = 0;
     carry_p = 0;
+  }
+  if (nwin > MAXW) {  // several chunks: the tile's piece count first
+    uint32_t cnt = 0;
+    for (uint32_t win = w; win < nwin; win += NW) {
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < PL; q++) {
+        const uint32_t j = lane * PL + q;
+        if (j < fw) sum += run_len(win * fw + j);
+      }
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      cnt += (sum + S - 1) / S;
+    }
+    uint32_t tot;
+    block_excl_sum<NW>(lane == 0 ? cnt : 0u, misc, &tot);
+    if (t == 0) {
+      base = piece_lookback(status, me, tot);
+      atomicAdd(pcount, tot);
+    }
+    __syncthreads();
   }
   for (uint32_t w0 = 0; w0 < nwin; w0 += MAXW) {
     const uint32_t nw = min(MAXW, nwin - w0);
@@ -493,7 +545,10 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
       }
       __syncthreads();
       if (t == 0) {
-        base = atomicAdd(pcount, cp - carry_p) - carry_p;  // dense-list position of piece index carry_p
+        if (nwin <= MAXW) {  // one chunk: cp is the tile's piece count
+          base = piece_lookback(status, me, cp);
+          atomicAdd(pcount, cp);
+        }
         carry_o = co;
         carry_p = cp;
       }
@@ -548,7 +603,7 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
     }
     __syncthreads();
   }
-  if (t == 0) tiles[blockIdx.x].npieces = carry_p;
+  if (t == 0) tiles[me].npieces = carry_p;
 }
 
 // ------------------------------------------------------------------------------
