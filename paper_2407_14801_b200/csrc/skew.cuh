@@ -437,20 +437,33 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
     const int b = (t - NC) >> 5;
     uint32_t k = b;
     for (uint32_t i = blockIdx.x + b * gridDim.x; i < npieces; i += NS * gridDim.x, k += NS) {
-      if (k >= NS) mbar_wait(&empty[b], ((k / NS) - 1) & 1);
+      // the piece's metadata is loaded before waiting for the buffer: the loads
+      // overlap the consumers' work on the buffer's previous piece
       const PieceDesc pd = pieces[i];
+      const uint32_t nb = pd.nb, Pn = pd.pn, nf = pd.nf;
+      const K* P = piv + pd.thr0;
+      const bool real = lane < (int)nb - 1;
+      const K pj = real ? P[lane] : K(0);
+      const K pprev = (real && pd.bt * kTB + lane >= 1) ? P[lane - 1] : K(0);
+      uint32_t ra[F / 32], rb[F / 32];  // all run bounds loaded at once (one latency)
+#pragma unroll
+      for (int r = 0; r < F / 32; r++) {
+        const uint32_t f = 32 * r + lane;
+        if (f < nf) {
+          const uint32_t* row = segmat + pd.row0 + f;  // tile-major segmat: coalesced over f
+          ra[r] = row[0];
+          rb[r] = row[pd.rstride];
+        }
+      }
+      if (k >= NS) mbar_wait(&empty[b], ((k / NS) - 1) & 1);
       K* slot = reinterpret_cast<K*>(sm + C::off_slot + b * C::SLOT_B);
       uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot + b * C::VSLOT_B);
       uint32_t* bits = reinterpret_cast<uint32_t*>(sm + C::off_bits + b * C::BITS_B);
       Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr + b * C::THR_B);
       uint32_t* thr32 = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
       uint32_t* meta = thr32 + 32;
-      const uint32_t nb = pd.nb, Pn = pd.pn, nf = pd.nf;
       {  // thresholds (lane = boundary)
-        const K* P = piv + pd.thr0;
-        const bool real = lane < (int)nb - 1;
-        const K pj = real ? P[lane] : K(0);
-        const bool dup = real && pd.bt * kTB + lane >= 1 && P[lane - 1] == pj;
+        const bool dup = real && pd.bt * kTB + lane >= 1 && pprev == pj;
         thr[lane] = Thr<K>::make(pj, dup, !real);
         uint32_t cntmax = 0;
         if constexpr (sizeof(K) == 4) {
@@ -469,16 +482,6 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
       for (uint32_t q = lane; q < C::BITS_B / 4; q += 32) bits[q] = 0;
       __syncwarp();
       uint32_t carry_len = 0, carry_sb = 0;
-      uint32_t ra[F / 32], rb[F / 32];  // all run bounds loaded at once (one latency)
-#pragma unroll
-      for (int r = 0; r < F / 32; r++) {
-        const uint32_t f = 32 * r + lane;
-        if (f < nf) {
-          const uint32_t* row = segmat + pd.row0 + f;  // tile-major segmat: coalesced over f
-          ra[r] = row[0];
-          rb[r] = row[pd.rstride];
-        }
-      }
 #pragma unroll
       for (int r = 0; r < F / 32; r++) {
         const uint32_t f = 32 * r + lane;
