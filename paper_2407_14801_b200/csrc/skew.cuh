@@ -436,10 +436,13 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
   if (t >= NC) {  // ================= producer warps: warp b stages pieces k = b, b+NS, ... into buffer b
     const int b = (t - NC) >> 5;
     uint32_t k = b;
+    PieceDesc pdn;  // the next piece's descriptor, prefetched one iteration ahead
+    if (blockIdx.x + b * gridDim.x < npieces) pdn = pieces[blockIdx.x + b * gridDim.x];
     for (uint32_t i = blockIdx.x + b * gridDim.x; i < npieces; i += NS * gridDim.x, k += NS) {
       // the piece's metadata is loaded before waiting for the buffer: the loads
       // overlap the consumers' work on the buffer's previous piece
-      const PieceDesc pd = pieces[i];
+      const PieceDesc pd = pdn;
+      if (i + NS * gridDim.x < npieces) pdn = pieces[i + NS * gridDim.x];
       const uint32_t nb = pd.nb, Pn = pd.pn, nf = pd.nf;
       const K* P = piv + pd.thr0;
       const bool real = lane < (int)nb - 1;
