@@ -206,6 +206,27 @@ struct Arena {
     used_host = true;
     return g_pinned.get(bytes);
   }
+  // Several host arrays in one staging block and one transfer (one k_xfer launch
+  // instead of one per array); returns their device addresses in order.
+  std::vector<void*> upload_all(const std::vector<std::pair<const void*, size_t>>& parts) {
+    size_t tot = 0;
+    for (auto& p : parts) tot += (p.second + 15) & ~size_t(15);
+    std::vector<void*> out;
+    char* d = (char*)alloc(tot);
+    char* h = tot ? (char*)pinned(tot) : nullptr;
+    size_t o = 0;
+    for (auto& p : parts) {
+      if (p.second) memcpy(h + o, p.first, p.second);
+      out.push_back(d + o);
+      o += (p.second + 15) & ~size_t(15);
+    }
+    xfer(d, h, tot, st);
+    return out;
+  }
+  template <typename T>
+  static std::pair<const void*, size_t> part(const std::vector<T>& v) {
+    return {v.data(), v.size() * sizeof(T)};
+  }
   template <typename T>
   T* upload(const std::vector<T>& v) {
     T* d = (T*)alloc(v.size() * sizeof(T));
@@ -576,12 +597,21 @@ struct Engine {
     std::vector<uint32_t> seg_of(buck_tot);
     for (uint32_t s2 = 0; s2 < ns; s2++)
       for (uint32_t b = 0; b < L[s2].k; b++) seg_of[L[s2].buck_base + b] = s2;
-    uint32_t* dSegOf = ar.upload(seg_of);
-    LevelSeg* dL = ar.upload(L);
-    TileInfo* dTiles = ar.upload(tiles);
-    uint32_t* dTileBase = ar.upload(tile_base);
-    uint32_t* dPieceBase = ar.upload(piece_seg_base);
-    TaskDesc* dM = ar.upload(mtasks);
+    // every descriptor of the level in one transfer; the column descriptors too:
+    // nothing but kernels may sit between the sampler, the round selection and the
+    // column sort (programmatic dependent launch)
+    std::vector<std::pair<const void*, size_t>> parts = {Arena::part(seg_of), Arena::part(L), Arena::part(tiles),
+                                                        Arena::part(tile_base), Arena::part(piece_seg_base),
+                                                        Arena::part(mtasks)};
+    if (!generic)
+      for (auto& kv : colcls) parts.push_back(Arena::part(kv.second));
+    const std::vector<void*> up = ar.upload_all(parts);
+    uint32_t* dSegOf = (uint32_t*)up[0];
+    LevelSeg* dL = (LevelSeg*)up[1];
+    TileInfo* dTiles = (TileInfo*)up[2];
+    uint32_t* dTileBase = (uint32_t*)up[3];
+    uint32_t* dPieceBase = (uint32_t*)up[4];
+    TaskDesc* dM = (TaskDesc*)up[5];
     K* cand = (K*)ar.alloc(std::max<uint64_t>(cand_tot, 1) * sizeof(K));
     uint8_t* flags = (uint8_t*)ar.alloc(uint64_t(ns) * kCap);
     K* p0s = (K*)ar.alloc(uint64_t(ns) * kCap * sizeof(K));
@@ -597,11 +627,11 @@ struct Engine {
     SQ_CUDA(cudaMemsetAsync(segmin, 0xff, ns * sizeof(K), st));
     SQ_CUDA(cudaMemsetAsync(segmat, 0, segmat_tot * 4, st));
 
-    // column descriptors go up first: nothing but kernels may sit between the sampler,
-    // the round selection and the column sort (programmatic dependent launch)
     std::vector<std::pair<uint32_t, const ColDesc*>> coldesc;
-    if (!generic)
-      for (auto& kv : colcls) coldesc.push_back({kv.first, ar.upload(kv.second)});
+    if (!generic) {
+      size_t q = 6;
+      for (auto& kv : colcls) coldesc.push_back({kv.first, (const ColDesc*)up[q++]});
+    }
     // 1. pivots: all rounds in parallel from the level input (L9)
     with_tile<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
       constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
