@@ -70,6 +70,19 @@ int sq_sort_u64(uint64_t *keys, size_t n, uint64_t seed, void *stream);
  * keys and vals must not overlap. */
 int sq_sort_pairs_u32_u32(uint32_t *keys, uint32_t *vals, size_t n, uint64_t seed, void *stream);
 
+/* Signed and IEEE-754 keys (the paper's workloads are signed
+ * integers): an order-preserving bit map onto unsigned keys of the
+ * same width (signed: flip the sign bit; float/double: flip all bits of a
+ * negative value, the sign bit of a non-negative one), the unsigned sort, and the
+ * inverse map, all on the device and in place.  Floats sort by IEEE 754-2008
+ * totalOrder: -NaN < -inf < ... < -0.0 < +0.0 < ... < +inf < +NaN, NaN payloads
+ * ordered by their bits (reading L25).  Limits and errors as the
+ * unsigned calls of the same width. */
+int sq_sort_i32(int32_t *keys, size_t n, uint64_t seed, void *stream);
+int sq_sort_i64(int64_t *keys, size_t n, uint64_t seed, void *stream);
+int sq_sort_f32(float *keys, size_t n, uint64_t seed, void *stream);
+int sq_sort_f64(double *keys, size_t n, uint64_t seed, void *stream);
+
 /* Same operations on HOST buffers: copy in, sort on the device, copy out,
  * synchronize.  The end-to-end path the bench's `e2e` figure measures. */
 int sq_sort_u32_host(uint32_t *keys, size_t n, uint64_t seed, void *stream);

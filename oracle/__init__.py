@@ -280,3 +280,56 @@ def skew_transpose_matrix(src, rows: int, cols: int, pivots, k: int | None = Non
     lib().sqo_skew_transpose_matrix(_p64(S), _p32(Sv), _p64(dst), _p32(dv), rows, cols, n,
                                     _p64(P), k, _p64(bi), _p64(bo), T)
     return dst, dv, bo
+
+
+# ----------------------------------------------------------------- signed / IEEE keys
+# DESIGN.md reading L25.  The paper sorts integers (P:846,
+# P:1048); signed and floating-point keys are sorted by an order-preserving
+# bijection onto unsigned keys of the same width -- signed: add 2^(w-1), i.e. flip
+# the sign bit; IEEE-754: the totalOrder predicate of IEEE 754-2008 5.10, written
+# out as "negative values in reverse bit order below all non-negative values in
+# bit order".  These functions are the definition, not a port of the kernel's map.
+_UNS = {np.dtype(np.int32): np.uint32, np.dtype(np.int64): np.uint64,
+        np.dtype(np.float32): np.uint32, np.dtype(np.float64): np.uint64}
+
+
+def total_order_key(a):
+    """Unsigned key whose unsigned order is the value order of `a` (ints) or the
+    IEEE totalOrder of `a` (floats).  Element by element, plain Python ints."""
+    a = np.asarray(a)
+    u = _UNS[a.dtype]
+    w = np.dtype(u).itemsize * 8
+    bits = a.view(u)
+    out = np.empty(len(a), u)
+    for i, b in enumerate(bits.tolist()):
+        if a.dtype.kind == "i":
+            v = int(a[i])
+            out[i] = v + (1 << (w - 1))            # -2^(w-1) .. 2^(w-1)-1  ->  0 .. 2^w-1
+        else:
+            neg = b >> (w - 1)
+            mag = b & ((1 << (w - 1)) - 1)         # |x| as an unsigned bit pattern
+            # negatives: larger magnitude first, all below +0; non-negatives above
+            out[i] = ((1 << (w - 1)) - 1 - mag) if neg else ((1 << (w - 1)) + mag)
+    return out
+
+
+def from_total_order_key(k, dtype):
+    """Inverse of total_order_key."""
+    dtype = np.dtype(dtype)
+    u = _UNS[dtype]
+    w = np.dtype(u).itemsize * 8
+    out = np.empty(len(k), u)
+    for i, x in enumerate(np.asarray(k, u).tolist()):
+        if dtype.kind == "i":
+            out[i] = x - (1 << (w - 1)) + (1 << w if x < (1 << (w - 1)) else 0)
+        else:
+            out[i] = (x - (1 << (w - 1))) if x >= (1 << (w - 1)) else \
+                ((1 << (w - 1)) | ((1 << (w - 1)) - 1 - x))
+    return out.view(dtype)
+
+
+def square_sort_mapped(a, seed: int = 0, **kw):
+    """SquareSort of signed / float keys: map, Alg 1 on the unsigned keys, unmap."""
+    a = np.asarray(a)
+    d, _, st = square_sort(total_order_key(a), seed=seed, **kw)
+    return from_total_order_key(d.astype(_UNS[a.dtype]), a.dtype), st

@@ -21,6 +21,7 @@ STATUS = {0: "SQ_OK", 1: "SQ_ERR_INVALID_ARGUMENT", 2: "SQ_ERR_OUT_OF_MEMORY", 3
           4: "SQ_ERR_PRECONDITION", 5: "SQ_ERR_UNSUPPORTED_DEVICE"}
 EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_host",
            "sq_sort_u64_host", "sq_sort_pairs_u32_u32_host", "sq_sort_u32_host_batch",
+           "sq_sort_i32", "sq_sort_i64", "sq_sort_f32", "sq_sort_f64",
            "sq_sort_u64_host_batch", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode"]
@@ -57,7 +58,8 @@ def lib():
                               "(there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         vp, sz, u64, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32
-        for f in ("sq_sort_u32", "sq_sort_u64", "sq_sort_u32_host", "sq_sort_u64_host"):
+        for f in ("sq_sort_u32", "sq_sort_u64", "sq_sort_u32_host", "sq_sort_u64_host", "sq_sort_i32",
+                  "sq_sort_i64", "sq_sort_f32", "sq_sort_f64"):
             getattr(L, f).argtypes = [vp, sz, u64, vp]
             getattr(L, f).restype = ctypes.c_int
         for f in ("sq_sort_pairs_u32_u32", "sq_sort_pairs_u32_u32_host"):
@@ -123,6 +125,30 @@ def sort_u32(keys, seed: int = 0, stream=None):
 def sort_u64(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.uint64 CUDA tensor in place (sq_sort_u64)."""
     _check(lib().sq_sort_u64(_dev(keys, "torch.uint64"), keys.numel(), _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_i32(keys, seed: int = 0, stream=None):
+    """Sort a contiguous torch.int32 CUDA tensor in place (sq_sort_i32)."""
+    _check(lib().sq_sort_i32(_dev(keys, "torch.int32"), keys.numel(), _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_i64(keys, seed: int = 0, stream=None):
+    """Sort a contiguous torch.int64 CUDA tensor in place (sq_sort_i64)."""
+    _check(lib().sq_sort_i64(_dev(keys, "torch.int64"), keys.numel(), _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_f32(keys, seed: int = 0, stream=None):
+    """Sort a contiguous torch.float32 CUDA tensor in place by IEEE totalOrder (sq_sort_f32)."""
+    _check(lib().sq_sort_f32(_dev(keys, "torch.float32"), keys.numel(), _seed(seed), _stream(stream)))
+    return keys
+
+
+def sort_f64(keys, seed: int = 0, stream=None):
+    """Sort a contiguous torch.float64 CUDA tensor in place by IEEE totalOrder (sq_sort_f64)."""
+    _check(lib().sq_sort_f64(_dev(keys, "torch.float64"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 

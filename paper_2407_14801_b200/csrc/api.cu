@@ -992,6 +992,43 @@ static int sort_entry(K* keys, uint32_t* vals, size_t n, uint64_t seed, void* st
   });
 }
 
+// Signed and floating-point keys: an order-preserving bijection
+// onto unsigned keys of the same width, applied in place before the unsigned sort
+// and inverted after it (reading L25).  Signed: flip the sign bit.
+// IEEE-754 binary32/64: flip every bit of a negative value, only the sign bit of a
+// non-negative one -- the totalOrder of IEEE 754-2008 5.10 (-NaN < -inf < ... < -0
+// < +0 < ... < +inf < +NaN).
+template <typename U>
+__global__ void k_key_map(U* __restrict__ k, size_t n, int kind, bool inverse) {
+  constexpr U SIGN = U(1) << (sizeof(U) * 8 - 1);
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const U x = k[i];
+    U y;
+    if (kind == 0) y = x ^ SIGN;                                    // two's complement
+    else if (!inverse) y = (x & SIGN) ? U(~x) : U(x | SIGN);         // float -> ordered
+    else y = (x & SIGN) ? U(x ^ SIGN) : U(~x);                      // ordered -> float
+    k[i] = y;
+  }
+}
+
+template <typename U>
+static int mapped_entry(U* keys, size_t n, uint64_t seed, void* stream, int kind) {
+  return guarded([&] {
+    if (n <= 1) return;
+    need(keys != nullptr, "keys is NULL");
+    need(n <= (sizeof(U) == 4 ? (size_t(1) << 30) : (size_t(1) << 28)), "n exceeds the supported maximum");
+    check_device();
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t g = (uint32_t)std::min<size_t>((n + 1023) / 1024, size_t(num_sms()) * 8);
+    k_key_map<U><<<g, 256, 0, st>>>(keys, n, kind, false);
+    check_launch("k_key_map");
+    sort_device<U, false>(keys, nullptr, n, seed, st);
+    k_key_map<U><<<g, 256, 0, st>>>(keys, n, kind, true);
+    check_launch("k_key_map");
+    SQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 // Pipelined batch of host sorts (sq_sort_*_host_batch): item i's sort on `st`
 // overlaps the H2D copy of item i+1 and the D2H copy of item i-1, each on a
 // library-owned non-blocking copy stream.  Three device buffers rotate, so a
@@ -1090,6 +1127,18 @@ int sq_sort_u64_host(uint64_t* keys, size_t n, uint64_t seed, void* stream) {
 }
 int sq_sort_pairs_u32_u32_host(uint32_t* keys, uint32_t* vals, size_t n, uint64_t seed, void* stream) {
   return sort_entry<uint32_t, true>(keys, vals, n, seed, stream, true);
+}
+int sq_sort_i32(int32_t* keys, size_t n, uint64_t seed, void* stream) {
+  return mapped_entry<uint32_t>(reinterpret_cast<uint32_t*>(keys), n, seed, stream, 0);
+}
+int sq_sort_i64(int64_t* keys, size_t n, uint64_t seed, void* stream) {
+  return mapped_entry<uint64_t>(reinterpret_cast<uint64_t*>(keys), n, seed, stream, 0);
+}
+int sq_sort_f32(float* keys, size_t n, uint64_t seed, void* stream) {
+  return mapped_entry<uint32_t>(reinterpret_cast<uint32_t*>(keys), n, seed, stream, 1);
+}
+int sq_sort_f64(double* keys, size_t n, uint64_t seed, void* stream) {
+  return mapped_entry<uint64_t>(reinterpret_cast<uint64_t*>(keys), n, seed, stream, 1);
 }
 int sq_sort_u32_host_batch(const uint32_t* const* in, uint32_t* const* out, size_t n, size_t count, uint64_t seed,
                            void* stream) {

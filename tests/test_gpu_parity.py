@@ -361,3 +361,32 @@ def test_skew_transpose_validate_flag():
     assert e.value.code == 4
     got, bo = gpu_skew(x, 2, 2, [2, 3], flags=sq.SQ_FLAG_VALIDATE)
     assert got.tolist() == [1, 2, 3, 4] and bo.tolist() == [1, 2, 4]
+
+
+# ---------------------------------------------------------------- signed / IEEE keys (L25)
+@pytest.mark.parametrize("dt", ["int32", "int64", "float32", "float64"])
+@pytest.mark.parametrize("n", [1000, 300007])
+def test_signed_and_float_keys(dt, n):
+    rng = np.random.default_rng(31)
+    npdt = np.dtype(dt)
+    if npdt.kind == "i":
+        info = np.iinfo(npdt)
+        x = rng.integers(info.min, info.max, n, dtype=npdt, endpoint=True)
+        x[:3] = [info.min, info.max, 0]
+        x[3:600] = x[3]  # a run of duplicates
+    else:
+        x = (rng.standard_normal(n) * 10.0 ** rng.integers(-20, 20, n)).astype(npdt)
+        u = np.uint32 if npdt.itemsize == 4 else np.uint64
+        w = npdt.itemsize * 8
+        specials = np.array([np.inf, -np.inf, 0.0, -0.0, np.finfo(npdt).tiny, -np.finfo(npdt).tiny], npdt)
+        nans = np.array([(1 << w) - 1, (1 << (w - 1)) - 1, (1 << (w - 1)) | 1], u).view(npdt)
+        x[: len(specials)] = specials
+        x[len(specials): len(specials) + 3] = nans
+    # expected: the oracle's total-order key, sorted, mapped back (the definition)
+    k = O.total_order_key(x)
+    want = O.from_total_order_key(np.sort(k), npdt)
+    t = torch.from_numpy(x.copy()).cuda()
+    getattr(sq, "sort_" + {"int32": "i32", "int64": "i64", "float32": "f32", "float64": "f64"}[dt])(t, 7)
+    got = t.cpu().numpy()
+    u = np.uint32 if npdt.itemsize == 4 else np.uint64
+    assert np.array_equal(got.view(u), want.view(u))

@@ -405,3 +405,39 @@ def test_level_matches_closed_form():
         assert (post == dc).all() and (be == bc).all()
         Pw, rw, dw = O.sample_pivots(O.root_key(3), x, D)
         assert (P == Pw).all() and r == rw and deg == dw
+
+
+# ---------------------------------------------------------------- signed / IEEE keys (L25)
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+def test_total_order_ints_match_numpy(dt):
+    rng = np.random.default_rng(21)
+    info = np.iinfo(dt)
+    x = rng.integers(info.min, info.max, 3000, dtype=dt, endpoint=True)
+    x[:4] = [info.min, info.max, 0, -1]
+    k = O.total_order_key(x)
+    assert (O.from_total_order_key(k, dt) == x).all()
+    order = np.argsort(k, kind="stable")
+    assert (x[order] == np.sort(x)).all()          # unsigned order of the key = signed order
+    assert k[0] == 0 and k[1] == np.iinfo(k.dtype).max  # extremes map to the extremes
+    d, _ = O.square_sort_mapped(x, seed=4)
+    assert (d == np.sort(x)).all()
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_total_order_floats(dt):
+    rng = np.random.default_rng(22)
+    x = (rng.standard_normal(2000) * 10.0 ** rng.integers(-30, 30, 2000)).astype(dt)
+    k = O.total_order_key(x)
+    assert (O.from_total_order_key(k, dt).view(k.dtype) == x.view(k.dtype)).all()  # bijection
+    d, _ = O.square_sort_mapped(x, seed=5)
+    assert (d == np.sort(x)).all()                  # finite, no -0: numpy's order
+    # the special values, in IEEE 754 totalOrder
+    inf, u = np.inf, (np.uint32 if dt == np.float32 else np.uint64)
+    w = np.dtype(u).itemsize * 8
+    nan = np.array([1 << (w - 1) | ((1 << (w - 1)) - 1)], u).view(dt)[0]   # -NaN (all ones)
+    pnan = np.array([(1 << (w - 1)) - 1], u).view(dt)[0]                   # +NaN
+    want = np.array([nan, -inf, -np.finfo(dt).max, -1.0, -np.finfo(dt).tiny, -0.0, 0.0,
+                     np.finfo(dt).tiny, 1.0, np.finfo(dt).max, inf, pnan], dt)
+    perm = np.random.default_rng(3).permutation(len(want))
+    got, _ = O.square_sort_mapped(want[perm], seed=1, cutoff=4)
+    assert (got.view(u) == want.view(u)).all()
