@@ -1163,6 +1163,86 @@ k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__
   }
 }
 
+// Work units of the copy and oversize lists: a bucket's sub-chunks are gathered by
+// ceil(npieces / GP) units of GP consecutive pieces each, so one huge bucket (a
+// single-value bucket of a low-cardinality input holds up to n/2 keys) is copied
+// by many CTAs instead of one.  One CTA scans the items' unit counts;
+// units[u] = (list position, part).
+constexpr uint32_t kGatherPieces = 256;
+
+__global__ void __launch_bounds__(1024)
+k_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
+               const uint32_t* __restrict__ count, uint2* __restrict__ units, uint32_t* __restrict__ nunits) {
+  __shared__ uint32_t misc[64];
+  const uint32_t total = *count;
+  uint32_t carry = 0;
+  for (uint32_t c0 = 0; c0 < total; c0 += 1024) {
+    const uint32_t it = c0 + threadIdx.x;
+    uint32_t parts = 0;
+    if (it < total) {
+      const BucketRec rc = recs[item_bucket(list[it])];
+      parts = max(1u, (tiles[rc.tile].npieces + kGatherPieces - 1) / kGatherPieces);
+    }
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<32>(parts, misc, &tot);
+    for (uint32_t q = 0; q < parts; q++) units[carry + ex + q] = make_uint2(it, q);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *nunits = carry;
+}
+
+// Copy of the listed buckets, contiguous at rc.out in dst (keys in the paper's
+// order), one unit per CTA iteration: the unit's output offset is the bucket's
+// keys in the pieces before it (block reduction), then its pieces' runs are
+// copied warp per run.
+template <typename K, int NT>
+__global__ void __launch_bounds__(NT)
+k_bucket_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
+                      const uint32_t* __restrict__ list, const uint2* __restrict__ units,
+                      const uint32_t* __restrict__ nunits, const K* __restrict__ src, K* __restrict__ dst,
+                      const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+                      const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
+  static_assert(NT == (int)kGatherPieces, "one piece per thread");
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t s_off[NT], s_len[NT], s_dst[NT], misc[64];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t total = *nunits;
+  for (uint32_t u = blockIdx.x; u < total; u += gridDim.x) {
+    const uint2 un = units[u];
+    const BucketRec rc = recs[item_bucket(list[un.x])];
+    const TileInfo ti = tiles[rc.tile];
+    const uint32_t p0 = un.y * kGatherPieces, p1 = min(ti.npieces, p0 + kGatherPieces);
+    auto len_of = [&](uint32_t p) -> uint32_t {
+      const uint16_t* pr = ppre + uint64_t(ti.piece_base + p) * kPP;
+      return uint32_t(pr[rc.lane + 1]) - uint32_t(pr[rc.lane]);
+    };
+    uint32_t before = 0;  // the bucket's keys in pieces [0, p0)
+    for (uint32_t p = t; p < p0; p += NT) before += len_of(p);
+    uint32_t bt;
+    block_excl_sum<NW>(before, misc, &bt);
+    const uint32_t p = p0 + t;
+    uint32_t o = 0, l = 0;
+    if (p < p1) {
+      o = pout[ti.piece_base + p] + ppre[uint64_t(ti.piece_base + p) * kPP + rc.lane];
+      l = len_of(p);
+    }
+    uint32_t tl;
+    const uint32_t ex = block_excl_sum<NW>(l, misc + 32, &tl);
+    s_off[t] = o;
+    s_len[t] = l;
+    s_dst[t] = rc.out + bt + ex;
+    __syncthreads();
+    for (uint32_t c = w; c < p1 - p0; c += NW) {
+      const uint32_t oo = s_off[c], ll = s_len[c], dd = s_dst[c];
+      for (uint32_t q = lane; q < ll; q += 32) {
+        dst[dd + q] = src[oo + q];
+        if (vsrc) vdst[dd + q] = vsrc[oo + q];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------------
 // Cluster bucket sort (the GPU's simple_sort for buckets larger than one CTA
 // holds, P:259-261 / P:852): a cluster of CL CTAs (CL = 4, 8, 16) sorts one
