@@ -698,7 +698,10 @@ struct Engine {
       check_launch("k_segmat");
     }
     ar.release(cand);
-    // 4. tile sizes and offsets, then the SkewTranspose X -> T
+    // 4. tile sizes and offsets, then the SkewTranspose X -> T; the
+    // transpose also accumulates the bucket sizes
+    uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
+    SQ_CUDA(cudaMemsetAsync(bsize, 0, buck_tot * 4, st));
     {
       ProfScope ps("tiles", st);
       k_tile_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, segmat);
@@ -727,7 +730,7 @@ struct Engine {
       }
       ProfScope ps("transpose", st);
       f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), XC::NT, XC::SMEM, st>>>(
-          pieces, pcount, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv, segmat, ppre);
+          pieces, pcount, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv, segmat, ppre, bsize);
       check_launch("k_transpose_ws");
       ar.release(pcount);
       ar.release(pieces);
@@ -786,9 +789,6 @@ struct Engine {
     SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 3) * 4, st));
     {
       ProfScope ps("plan", st);
-      uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
-      k_bucket_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, ppre, bsize);
-      check_launch("k_bucket_sizes");
       uint32_t* boff = (uint32_t*)ar.alloc(buck_tot * 4);
       k_bucket_offsets<<<ns, 1024, 0, st>>>(dL, bsize, boff);
       check_launch("k_bucket_offsets");

@@ -303,7 +303,9 @@ __global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __rest
 __host__ __device__ __forceinline__ uint32_t plan_fw(uint32_t size, uint32_t ncols, uint32_t S, uint32_t FWMAX) {
   if (!size) return FWMAX;
   const uint64_t fw = (uint64_t(S) * 31 / 32) * ncols / size;
-  return (uint32_t)max((uint64_t)1, min((uint64_t)FWMAX, fw));
+  // at least 32 columns: a huge tile (low-cardinality input) gets windows of many
+  // pieces rather than one window per column, so its plan is not a serial walk
+  return (uint32_t)max((uint64_t)min(32u, FWMAX), min((uint64_t)FWMAX, fw));
 }
 
 __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
@@ -427,6 +429,7 @@ struct __align__(16) PieceDesc {
   uint32_t pn, out, nf, off;         // keys, output offset, runs, offset into the first run
   uint32_t src0, rows, row0, rstride;  // first column's start; column length; segmat index of (bt, col); ncols
   uint32_t nb, thr0, slot, bt;       // buckets in the tile, pivot index of its first boundary, piece table slot, tile
+  uint32_t bbase;                    // index of the tile's first bucket in the level's bucket arrays
 };
 
 // Piece plan, parallel form: every bucket tile's stream is cut into windows of FW
@@ -596,7 +599,7 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
           const uint32_t col = c0 + cf;
           pieces[base + j] = PieceDesc{ep - sp, oc, cl - cf + 1, of, sg.off + col * sg.rows, sg.rows,
                                        (uint32_t)(sg.segmat_base + uint64_t(bt) * sg.ncols + col), rstride, nb,
-                                       sg.piv_base + bt * kTB, pe, bt};
+                                       sg.piv_base + bt * kTB, pe, bt, sg.buck_base + bt * kTB};
           pout[pe] = oc;
         }
       }

@@ -29,7 +29,7 @@
 namespace sq {
 
 // Meta slots of a staged piece.
-enum { kMxPiece = 0, kMxNch, kMxPn, kMxOut, kMxNb, kMxBmax, kMxValid };
+enum { kMxPiece = 0, kMxNch, kMxPn, kMxOut, kMxNb, kMxBmax, kMxValid, kMxBbase };
 
 // ------------------------------------------------------------------------------
 // The same SkewTranspose with per-thread counters (the sort path's transpose):
@@ -415,7 +415,8 @@ template <typename K, bool PAIRS, int S, int F>
 __global__ void __launch_bounds__(WsCfg<K, PAIRS, S, F>::NT, 2)
 k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict__ pcount, const K* __restrict__ src,
                K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
+               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre,
+               uint32_t* __restrict__ bsize) {
   using C = WsCfg<K, PAIRS, S, F>;
   constexpr int EB = sizeof(K), NC = C::NC, KT = C::KT, VW = C::VW, NS = C::NS;
   static_assert(F <= 128 && F % 32 == 0 && S <= 65535 && kTB == 32 && KT < 64, "shape");
@@ -480,6 +481,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
           meta[kMxOut] = pd.out;
           meta[kMxNb] = nb;
           meta[kMxBmax] = cntmax;
+          meta[kMxBbase] = pd.bbase;
         }
       }
       for (uint32_t q = lane; q < C::BITS_B / 4; q += 32) bits[q] = 0;
@@ -555,7 +557,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
     const uint32_t* thr32 = reinterpret_cast<const uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
     const uint32_t* meta = thr32 + 32;
     const uint32_t nwords = meta[kMxNch], Pn = meta[kMxPn], oc = meta[kMxOut], bmax = meta[kMxBmax];
-    const uint32_t nb = meta[kMxNb], pslot = meta[kMxPiece];
+    const uint32_t nb = meta[kMxNb], pslot = meta[kMxPiece], bbase = meta[kMxBbase];
     const uint32_t thr_r = sizeof(K) == 4 ? thr32[lane] : 0u;
     // ---- pass 1: buckets and thread-local ranks
     const uint32_t w0 = t * KT;
@@ -683,6 +685,8 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
       if (t == 0) bulk_commit();
     }
     if (t <= kTB) ppre[uint64_t(pslot) * kPP + t] = (uint16_t)poff[t];
+    // bucket sizes of the level: this piece's count of every bucket of its tile
+    if (t < (int)nb && poff[t + 1] > poff[t]) atomicAdd(&bsize[bbase + t], poff[t + 1] - poff[t]);
     cons_bar();
   }
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");

@@ -5,6 +5,8 @@ import torch
 import paper_2407_14801_b200 as sq
 import sqinputs as S
 kind, n, seed = S.CONFIGS["cfg5"]
+if len(sys.argv) > 1:  # optional: input kind (sqinputs) and log2 n
+    kind, n = sys.argv[1], 1 << int(sys.argv[2]) if len(sys.argv) > 2 else n
 k, _ = S.generate(kind, n, seed)
 w = torch.from_numpy(k).cuda()
 sq.sort_u32(w, seed)
