@@ -878,17 +878,16 @@ struct Engine {
       ar.release(splits);
     }
     {  // single-value buckets (copied) and oversize buckets (made contiguous),
-       // in units of kGatherPieces pieces so that huge buckets are copied by many CTAs
+       // in units of kGatherKeys keys so that huge buckets are copied by many CTAs
       ProfScope ps("gather", st);
-      // an item has ceil(npieces / kGatherPieces) units; a tile lists at most kTB items
-      const uint64_t ucap = buck_tot + piece_tot * kTB / kGatherPieces + 16;
+      const uint64_t ucap = buck_tot + level_keys / kGatherKeys + 16;
       uint2* units = (uint2*)ar.alloc(ucap * sizeof(uint2));
       uint32_t* nun = (uint32_t*)ar.alloc(16);
       for (uint32_t c = po.ncls; c < po.ncls + 2; c++) {
         const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
-        k_gather_units<<<1, 1024, 0, st>>>(recs, dTiles, lst, po.count + c, units, nun);
+        k_gather_units<<<1, 1024, 0, st>>>(recs, lst, po.count + c, units, nun);
         check_launch("k_gather_units");
-        k_bucket_gather_units<K, kGatherPieces><<<4 * num_sms(), kGatherPieces, 0, st>>>(
+        k_bucket_gather_units<K, 256><<<4 * num_sms(), 256, 0, st>>>(
             recs, dTiles, lst, units, nun, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
             ppre);
         check_launch("k_bucket_gather_units");

@@ -1166,15 +1166,15 @@ k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__
   }
 }
 
-// Work units of the copy and oversize lists: a bucket's sub-chunks are gathered by
-// ceil(npieces / GP) units of GP consecutive pieces each, so one huge bucket (a
+// Work units of the copy and oversize lists: a bucket is copied in units of
+// kGatherKeys keys (its key range [q*kGatherKeys, ...)), so one huge bucket (a
 // single-value bucket of a low-cardinality input holds up to n/2 keys) is copied
 // by many CTAs instead of one.  One CTA scans the items' unit counts;
 // units[u] = (list position, part).
-constexpr uint32_t kGatherPieces = 256;
+constexpr uint32_t kGatherKeys = 65536;
 
 __global__ void __launch_bounds__(1024)
-k_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
+k_gather_units(const BucketRec* __restrict__ recs, const uint32_t* __restrict__ list,
                const uint32_t* __restrict__ count, uint2* __restrict__ units, uint32_t* __restrict__ nunits) {
   __shared__ uint32_t misc[64];
   const uint32_t total = *count;
@@ -1182,10 +1182,7 @@ k_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ 
   for (uint32_t c0 = 0; c0 < total; c0 += 1024) {
     const uint32_t it = c0 + threadIdx.x;
     uint32_t parts = 0;
-    if (it < total) {
-      const BucketRec rc = recs[item_bucket(list[it])];
-      parts = max(1u, (tiles[rc.tile].npieces + kGatherPieces - 1) / kGatherPieces);
-    }
+    if (it < total) parts = max(1u, (recs[item_bucket(list[it])].size + kGatherKeys - 1) / kGatherKeys);
     uint32_t tot;
     const uint32_t ex = block_excl_sum<32>(parts, misc, &tot);
     for (uint32_t q = 0; q < parts; q++) units[carry + ex + q] = make_uint2(it, q);
@@ -1195,9 +1192,7 @@ k_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ 
 }
 
 // Copy of the listed buckets, contiguous at rc.out in dst (keys in the paper's
-// order), one unit per CTA iteration: the unit's output offset is the bucket's
-// keys in the pieces before it (block reduction), then its pieces' runs are
-// copied warp per run.
+// order), one unit (a key range of one bucket) per CTA iteration.
 template <typename K, int NT>
 __global__ void __launch_bounds__(NT)
 k_bucket_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
@@ -1205,44 +1200,29 @@ k_bucket_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __rest
                       const uint32_t* __restrict__ nunits, const K* __restrict__ src, K* __restrict__ dst,
                       const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
                       const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
-  static_assert(NT == (int)kGatherPieces, "one piece per thread");
-  constexpr int NW = NT / 32;
   __shared__ uint32_t s_off[NT], s_len[NT], s_dst[NT], misc[64];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t total = *nunits;
   for (uint32_t u = blockIdx.x; u < total; u += gridDim.x) {
     const uint2 un = units[u];
     const BucketRec rc = recs[item_bucket(list[un.x])];
     const TileInfo ti = tiles[rc.tile];
-    const uint32_t p0 = un.y * kGatherPieces, p1 = min(ti.npieces, p0 + kGatherPieces);
-    auto len_of = [&](uint32_t p) -> uint32_t {
-      const uint16_t* pr = ppre + uint64_t(ti.piece_base + p) * kPP;
-      return uint32_t(pr[rc.lane + 1]) - uint32_t(pr[rc.lane]);
-    };
-    uint32_t before = 0;  // the bucket's keys in pieces [0, p0)
-    for (uint32_t p = t; p < p0; p += NT) before += len_of(p);
-    uint32_t bt;
-    block_excl_sum<NW>(before, misc, &bt);
-    const uint32_t p = p0 + t;
-    uint32_t o = 0, l = 0;
-    if (p < p1) {
-      o = pout[ti.piece_base + p] + ppre[uint64_t(ti.piece_base + p) * kPP + rc.lane];
-      l = len_of(p);
-    }
-    uint32_t tl;
-    const uint32_t ex = block_excl_sum<NW>(l, misc + 32, &tl);
-    s_off[t] = o;
-    s_len[t] = l;
-    s_dst[t] = rc.out + bt + ex;
-    __syncthreads();
-    for (uint32_t c = w; c < p1 - p0; c += NW) {
-      const uint32_t oo = s_off[c], ll = s_len[c], dd = s_dst[c];
-      for (uint32_t q = lane; q < ll; q += 32) {
-        dst[dd + q] = src[oo + q];
-        if (vsrc) vdst[dd + q] = vsrc[oo + q];
-      }
-    }
-    __syncthreads();
+    const uint32_t lo = un.y * kGatherKeys, hi = min(rc.size, lo + kGatherKeys);
+    K* out = dst + rc.out + lo;
+    uint32_t* vout = vdst ? vdst + rc.out + lo : nullptr;
+    gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
+                      [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        uint32_t q = ln;
+                        for (; q + 96 < l; q += 128) {  // four independent loads in flight per lane
+                          const K x0 = src[o + q], x1 = src[o + q + 32], x2 = src[o + q + 64], x3 = src[o + q + 96];
+                          out[d + q] = x0;
+                          out[d + q + 32] = x1;
+                          out[d + q + 64] = x2;
+                          out[d + q + 96] = x3;
+                        }
+                        for (; q < l; q += 32) out[d + q] = src[o + q];
+                        if (vsrc)
+                          for (uint32_t v = ln; v < l; v += 32) vout[d + v] = vsrc[o + v];
+                      });
   }
 }
 
