@@ -643,28 +643,6 @@ struct PlanOut {
   uint32_t unit_max;  // largest unit (and bucket packed into units): the biggest one-CTA class
 };
 
-// Bucket sizes from the piece tables: CTA per tile, warp w sums pieces w, w+NW, ...
-__global__ void k_bucket_sizes(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
-                               const uint16_t* __restrict__ ppre, uint32_t* __restrict__ bsize) {
-  const TileInfo ti = tiles[blockIdx.x];
-  const LevelSeg sg = segs[ti.seg];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint32_t sum = 0;
-  for (uint32_t q = w; q < ti.npieces; q += nw) {
-    const uint16_t* pr = ppre + uint64_t(ti.piece_base + q) * kPP;
-    sum += pr[lane + 1] - pr[lane];
-  }
-  __shared__ uint32_t red[32][33];
-  red[w][lane] = sum;
-  __syncthreads();
-  if (w == 0) {
-    uint32_t tot = 0;
-    for (int i = 0; i < nw; i++) tot += red[i][lane];
-    const uint32_t b = ti.bt * kTB + lane;
-    if (b < sg.k) bsize[sg.buck_base + b] = tot;
-  }
-}
-
 // Bucket final offsets: exclusive scan of the sizes per segment (one CTA per
 // segment, P:283 / P:461).
 __global__ void k_bucket_offsets(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ bsize,
