@@ -144,6 +144,23 @@ def run_reference(args, rank):
     }), flush=True)
 
 
+def max_over_ranks(x: float, dist=None) -> float:
+    """The job's time is the slowest rank's (device-timed on each rank)."""
+    if dist is None:
+        return x
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(world: int, n: int, ms_per_step: float) -> float:
+    """Whole-job Gkeys/s of `world` independent replicas of an n-key sort (weak
+    scaling: every rank sorts its own n keys; the step time is the max over ranks)."""
+    return world * n / (ms_per_step / 1e3) / 1e9
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,12 +235,9 @@ def main():
     torch.cuda.synchronize()
     sq.profile(False)
     prof = sq.profile_read()
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, dist)
     ms = total_ms / args.steps
-    value = world * n / (ms / 1e3) / 1e9
+    value = replica_value(world, n, ms)
 
     # sanity: the last step's output is sorted and a permutation (sum check)
     w64 = work.to(torch.int64)
