@@ -976,7 +976,7 @@ __global__ void k_merge_split(const BucketRec* __restrict__ recs, const MTile* _
 }
 
 template <typename K, bool PAIRS, int NT, int VM>
-__global__ void __launch_bounds__(NT, (PAIRS || sizeof(K) == 8) ? 1 : 2048 / NT / 2)  // u32 keys: 64 registers, 32 warps/SM
+__global__ void __launch_bounds__(NT, PAIRS ? 1 : (sizeof(K) == 8 ? 512 : 1024) / NT)  // 64 (u32) / 128 (u64) registers
 k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items, const uint32_t* __restrict__ count,
              uint32_t pass, K* __restrict__ bufX, K* __restrict__ bufU, uint32_t* __restrict__ vX,
              uint32_t* __restrict__ vU, const uint32_t* __restrict__ splits) {
