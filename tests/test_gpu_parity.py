@@ -122,6 +122,37 @@ def test_pairs_scaled_vs_oracle():
     assert np.array_equal(gk, want_k) and np.array_equal(gv, want_v)
 
 
+# ---------------------------------------------------------------- maximum sizes
+def _check_sorted_perm_gpu(src, out):
+    """out is non-decreasing and a permutation of src (sums of x, x^2 mod 2^64 and a
+    histogram of the top byte agree); a few order statistics checked by definition."""
+    a, b = src.to(torch.int64), out.to(torch.int64)
+    assert bool((b[1:] >= b[:-1]).all())
+    assert int(a.sum()) == int(b.sum()) and int((a * a).sum()) == int((b * b).sum())
+    assert torch.equal(torch.bincount(a >> 24, minlength=256), torch.bincount(b >> 24, minlength=256))
+    for i in (0, len(b) // 3, len(b) - 1):
+        x = b[i]
+        assert int((a < x).sum()) <= i < int((a <= x).sum())
+
+
+def test_max_size_u32():
+    # the documented limit n = 2^30 (4 GiB of keys)
+    g = torch.Generator(device="cuda").manual_seed(30)
+    src = torch.randint(0, 2**32, (1 << 30,), device="cuda", dtype=torch.int64, generator=g).to(torch.uint32)
+    out = src.clone()
+    sq.sort_u32(out, 30)
+    _check_sorted_perm_gpu(src, out)
+
+
+def test_max_size_u64():
+    # the documented limit n = 2^28 for 64-bit keys (values below 2^40: int64-safe checks)
+    g = torch.Generator(device="cuda").manual_seed(28)
+    src = torch.randint(0, 2**40, (1 << 28,), device="cuda", dtype=torch.int64, generator=g).to(torch.uint64)
+    out = src.clone()
+    sq.sort_u64(out, 28)
+    _check_sorted_perm_gpu(src.to(torch.int64), out.to(torch.int64))
+
+
 # ---------------------------------------------------------------- edge cases
 EDGE_N = [0, 1, 2, 3, 4, 5, 16, 17, 63, 64, 65, 255, 256, 257, 1000, 4095, 4096, 4097,
           32767, 32768, 32769, 65535, 65536, 65537, 100000, 250001]
