@@ -594,24 +594,20 @@ struct Engine {
     if (maxnp > key_max_tile<K>()) throw Error(SQ_ERR_INVALID_ARGUMENT, "pivot sample too large for one CTA");
     const uint32_t ntiles = (uint32_t)tiles.size();
 
-    std::vector<uint32_t> seg_of(buck_tot);
-    for (uint32_t s2 = 0; s2 < ns; s2++)
-      for (uint32_t b = 0; b < L[s2].k; b++) seg_of[L[s2].buck_base + b] = s2;
     // every descriptor of the level in one transfer; the column descriptors too:
     // nothing but kernels may sit between the sampler, the round selection and the
     // column sort (programmatic dependent launch)
-    std::vector<std::pair<const void*, size_t>> parts = {Arena::part(seg_of), Arena::part(L), Arena::part(tiles),
+    std::vector<std::pair<const void*, size_t>> parts = {Arena::part(L), Arena::part(tiles),
                                                         Arena::part(tile_base), Arena::part(piece_seg_base),
                                                         Arena::part(mtasks)};
     if (!generic)
       for (auto& kv : colcls) parts.push_back(Arena::part(kv.second));
     const std::vector<void*> up = ar.upload_all(parts);
-    uint32_t* dSegOf = (uint32_t*)up[0];
-    LevelSeg* dL = (LevelSeg*)up[1];
-    TileInfo* dTiles = (TileInfo*)up[2];
-    uint32_t* dTileBase = (uint32_t*)up[3];
-    uint32_t* dPieceBase = (uint32_t*)up[4];
-    TaskDesc* dM = (TaskDesc*)up[5];
+    LevelSeg* dL = (LevelSeg*)up[0];
+    TileInfo* dTiles = (TileInfo*)up[1];
+    uint32_t* dTileBase = (uint32_t*)up[2];
+    uint32_t* dPieceBase = (uint32_t*)up[3];
+    TaskDesc* dM = (TaskDesc*)up[4];
     K* cand = (K*)ar.alloc(std::max<uint64_t>(cand_tot, 1) * sizeof(K));
     uint8_t* flags = (uint8_t*)ar.alloc(uint64_t(ns) * kCap);
     K* p0s = (K*)ar.alloc(uint64_t(ns) * kCap * sizeof(K));
@@ -629,7 +625,7 @@ struct Engine {
 
     std::vector<std::pair<uint32_t, const ColDesc*>> coldesc;
     if (!generic) {
-      size_t q = 6;
+      size_t q = 5;
       for (auto& kv : colcls) coldesc.push_back({kv.first, (const ColDesc*)up[q++]});
     }
     // 1. pivots: all rounds in parallel from the level input (L9)
@@ -789,14 +785,8 @@ struct Engine {
     SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 3) * 4, st));
     {
       ProfScope ps("plan", st);
-      uint32_t* boff = (uint32_t*)ar.alloc(buck_tot * 4);
-      k_bucket_offsets<<<ns, 1024, 0, st>>>(dL, bsize, boff);
-      check_launch("k_bucket_offsets");
-      k_bucket_plan<K><<<(uint32_t)((buck_tot + 255) / 256), 256, 0, st>>>(dL, ns, dSegOf, dTileBase, bsize, boff, piv,
-                                                                         recs, (uint32_t)buck_tot, po);
-      check_launch("k_bucket_plan");
-      k_unit_plan<<<(ntiles * 32 + 127) / 128, 128, 0, st>>>(recs, dTiles, dL, ntiles, po);
-      check_launch("k_unit_plan");
+      k_tile_bucket_plan<K><<<(ntiles * 32 + 127) / 128, 128, 0, st>>>(dL, dTiles, ntiles, bsize, piv, recs, po);
+      check_launch("k_tile_bucket_plan");
     }
     if (dbg) {
       k_bucket_gather<K, 256><<<1024, 256, 0, st>>>(recs, dTiles, nullptr, nullptr, (uint32_t)buck_tot, kb[T],

@@ -643,122 +643,83 @@ struct PlanOut {
   uint32_t unit_max;  // largest unit (and bucket packed into units): the biggest one-CTA class
 };
 
-// Bucket final offsets: exclusive scan of the sizes per segment (one CTA per
-// segment, P:283 / P:461).
-__global__ void k_bucket_offsets(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ bsize,
-                                 uint32_t* __restrict__ boff) {
-  const LevelSeg sg = segs[blockIdx.x];
-  __shared__ uint32_t carry;
-  __shared__ uint32_t ws[32];
-  if (threadIdx.x == 0) carry = sg.off;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (uint32_t c0 = 0; c0 < sg.k; c0 += blockDim.x) {
-    const uint32_t b = c0 + threadIdx.x;
-    const uint32_t size = b < sg.k ? bsize[sg.buck_base + b] : 0;
-    uint32_t x = size;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) ws[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      uint32_t a = lane < nw ? ws[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, a, o);
-        if (lane >= o) a += y;
-      }
-      if (lane < nw) ws[lane] = a;
-    }
-    __syncthreads();
-    const uint32_t excl = carry + x - size + (w ? ws[w - 1] : 0);
-    if (b < sg.k) boff[sg.buck_base + b] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + size;
-    __syncthreads();
-  }
-}
-
-// Bucket records and work lists (one thread per bucket, all segments in one
-// grid): single-value buckets (copy), on-chip classes, merge-sorted
-// chunks and their merge tiles, oversize (next level).
+// Bucket plan, one warp per bucket tile: lane j takes bucket j of the tile; its final offset is the tile's
+// offset plus the sizes of the tile's earlier buckets (a warp scan -- the tile
+// offsets are already the segment's prefix, P:283 / P:461); then the records and
+// work lists of k_bucket_plan, and lane 0 packs the small buckets into units.
 template <typename K>
-__global__ void k_bucket_plan(const LevelSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ seg_of,
-                              const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ bsize,
-                              const uint32_t* __restrict__ boff, const K* __restrict__ piv,
-                              BucketRec* __restrict__ recs, uint32_t nbuck, PlanOut po) {
-  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= nbuck) return;
-  const uint32_t sidx = seg_of[gi];
-  const LevelSeg sg = segs[sidx];
-  const uint32_t b = gi - sg.buck_base;
-  const uint32_t size = bsize[gi];
-  const K* P = piv + sg.piv_base;
-  BucketRec rc;
-  rc.tile = tile_base[sidx] + b / kTB;
-  rc.lane = b % kTB;
-  rc.out = boff[gi];
-  rc.size = size;
-  rc.node = child_key(sg.node, 1, b);
-  rc.chunk = size;
-  rc.passes = 0;
-  const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
-  uint32_t q = 1;  // chunks
-  const uint32_t chunk_len = po.pair ? 2 * po.max_tile : po.max_tile;
-  if (size && !single && size > po.max_tile && size <= po.msort_max) {
-    q = (size + chunk_len - 1) / chunk_len;
-    rc.chunk = chunk_len;  // full chunks; the last one takes the remainder
-    uint32_t np = 0;
-    while ((1u << np) < q) np++;
-    rc.passes = np;
-    for (uint32_t p = 0; p < np; p++) {  // merge tiles of every pass
-      const uint32_t R = rc.chunk << p;
-      uint32_t ntile = 0;
-      for (uint32_t j = 0; 2 * j * R < size; j++) ntile += (min(size, (2 * j + 2) * R) - 2 * j * R + po.mtile - 1) / po.mtile;
-      uint32_t slot = atomicAdd(&po.mcount[p], ntile);
-      for (uint32_t j = 0; 2 * j * R < size; j++) {
-        const uint32_t plen = min(size, (2 * j + 2) * R) - 2 * j * R;
-        for (uint32_t t = 0; t * po.mtile < plen; t++)
-          po.mlist[uint64_t(p) * po.mcap + slot++] = MTile{gi, (uint16_t)j, (uint16_t)t};
-      }
-    }
-  }
-  recs[gi] = rc;
-  if (!size) return;
-  if (po.units && size <= po.unit_max) return;  // packed into a unit by k_unit_plan
-  if (single || size > po.msort_max) {
-    const int cls = single ? po.ncls : po.ncls + 1;
-    const uint32_t slot = atomicAdd(&po.count[cls], 1u);
-    po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16;
-  } else {
-    for (uint32_t k = 0; k < q; k++) {
-      const uint32_t len = min(rc.chunk, size - k * rc.chunk);
-      int cls = 0;
-      if (po.pair && len > po.max_tile) cls = po.ncls + 2;
-      else
-        while (po.cls_tile[cls] < len) cls++;
-      const uint32_t slot = atomicAdd(&po.count[cls], 1u);
-      po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16 + k;
-    }
-  }
-}
-
-// Packing of the small buckets (size <= max_tile) of every tile into units (greedy,
-// in bucket order, at most max_tile keys each); one thread per tile.
-__global__ void k_unit_plan(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
-                            const LevelSeg* __restrict__ segs, uint32_t ntiles, PlanOut po) {
-  // one warp per tile: lane j loads bucket j's record, lane 0 packs (shuffles only)
+__global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
+                                   uint32_t ntiles, const uint32_t* __restrict__ bsize, const K* __restrict__ piv,
+                                   BucketRec* __restrict__ recs, PlanOut po) {
   const uint32_t ti_idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (ti_idx >= ntiles) return;  // warp-uniform
   const TileInfo ti = tiles[ti_idx];
   const LevelSeg sg = segs[ti.seg];
-  const uint32_t b0 = sg.buck_base + ti.bt * kTB, nb = min((uint32_t)kTB, sg.k - ti.bt * kTB);
-  const uint32_t my_size = lane < nb ? recs[b0 + lane].size : 0u;
-  const uint32_t my_out = lane < nb ? recs[b0 + lane].out : 0u;
+  const uint32_t nb = min((uint32_t)kTB, sg.k - ti.bt * kTB);
+  const uint32_t b = ti.bt * kTB + lane, gi = sg.buck_base + b;
+  const uint32_t size = lane < nb ? bsize[gi] : 0u;
+  uint32_t x = size;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  const uint32_t out = ti.out + x - size;
+  if (lane < nb) {
+    const K* P = piv + sg.piv_base;
+    BucketRec rc;
+    rc.tile = ti_idx;
+    rc.lane = lane;
+    rc.out = out;
+    rc.size = size;
+    rc.node = child_key(sg.node, 1, b);
+    rc.chunk = size;
+    rc.passes = 0;
+    const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
+    uint32_t q = 1;  // chunks
+    const uint32_t chunk_len = po.pair ? 2 * po.max_tile : po.max_tile;
+    if (size && !single && size > po.max_tile && size <= po.msort_max) {
+      q = (size + chunk_len - 1) / chunk_len;
+      rc.chunk = chunk_len;  // full chunks; the last one takes the remainder
+      uint32_t np = 0;
+      while ((1u << np) < q) np++;
+      rc.passes = np;
+      for (uint32_t p = 0; p < np; p++) {  // merge tiles of every pass
+        const uint32_t R = rc.chunk << p;
+        uint32_t ntile = 0;
+        for (uint32_t j = 0; 2 * j * R < size; j++)
+          ntile += (min(size, (2 * j + 2) * R) - 2 * j * R + po.mtile - 1) / po.mtile;
+        uint32_t slot = atomicAdd(&po.mcount[p], ntile);
+        for (uint32_t j = 0; 2 * j * R < size; j++) {
+          const uint32_t plen = min(size, (2 * j + 2) * R) - 2 * j * R;
+          for (uint32_t t = 0; t * po.mtile < plen; t++)
+            po.mlist[uint64_t(p) * po.mcap + slot++] = MTile{gi, (uint16_t)j, (uint16_t)t};
+        }
+      }
+    }
+    recs[gi] = rc;
+    if (size && !(po.units && size <= po.unit_max)) {  // else packed into a unit below
+      if (single || size > po.msort_max) {
+        const int cls = single ? po.ncls : po.ncls + 1;
+        const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+        po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16;
+      } else {
+        for (uint32_t k = 0; k < q; k++) {
+          const uint32_t len = min(rc.chunk, size - k * rc.chunk);
+          int cls = 0;
+          if (po.pair && len > po.max_tile) cls = po.ncls + 2;
+          else
+            while (po.cls_tile[cls] < len) cls++;
+          const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+          po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16 + k;
+        }
+      }
+    }
+  }
+  if (!po.units) return;
+  // units: greedy, in bucket order, at most unit_max keys each (lane 0, shuffles)
   uint32_t j0 = 0, acc = 0, out0 = 0;
-  auto flush = [&](uint32_t j1) {  // buckets j0..j1-1 (lane 0 only)
+  auto flush = [&](uint32_t j1) {  // buckets j0..j1-1
     if (!acc) return;
     const uint32_t u = atomicAdd(po.nunits, 1u);
     po.units[u] = Unit{ti_idx, j0, j1 - 1, out0, acc};
@@ -768,19 +729,19 @@ __global__ void k_unit_plan(const BucketRec* __restrict__ recs, const TileInfo* 
     po.list[uint64_t(cls) * po.cap_per_list + slot] = kUnitFlag | u;
   };
   for (uint32_t j = 0; j < nb; j++) {
-    const uint32_t size = __shfl_sync(0xffffffffu, my_size, j), out = __shfl_sync(0xffffffffu, my_out, j);
+    const uint32_t sz = __shfl_sync(0xffffffffu, size, j), o = __shfl_sync(0xffffffffu, out, j);
     if (lane != 0) continue;
-    const bool small = size <= po.unit_max;
-    if (!small || acc + size > po.unit_max) {
+    const bool small = sz <= po.unit_max;
+    if (!small || acc + sz > po.unit_max) {
       flush(j);
       acc = 0;
     }
-    if (small && size) {
+    if (small && sz) {
       if (!acc) {
         j0 = j;
-        out0 = out;
+        out0 = o;
       }
-      acc += size;
+      acc += sz;
     }
   }
   if (lane == 0) flush(nb);

@@ -8,7 +8,7 @@ import json
 import sys
 from collections import OrderedDict
 
-ROLE = [("k_colsort", "colsort"), ("k_transpose", "transpose"), ("k_bucketsort", "bucketsort"),
+ROLE = [("k_tile_bucket_plan", "plan"), ("k_colsort", "colsort"), ("k_transpose", "transpose"), ("k_bucketsort", "bucketsort"),
         ("k_merge_pass", "merge"), ("k_merge_split", "merge"), ("k_pairsort", "pairsort"), ("k_clustersort", "clustersort"), ("k_sample", "sample"),
         ("k_select", "select"), ("k_segmat", "segmat"), ("k_tile", "tiles"), ("k_piece_plan", "tiles"),
         ("k_bucket_sizes", "plan"), ("k_bucket_offsets", "plan"), ("k_bucket_plan", "plan"),
