@@ -1,28 +1,25 @@
-// skew.cuh -- the sort path's SkewTranspose (Alg 2/3): slot-staged,
-// match-ranked, one piece per iteration of a persistent grid.
+// skew.cuh -- the sort path's SkewTranspose (Alg 2/3): warp-specialised,
+// counter-ranked, one piece per ring buffer, persistent grid.
 //
 // A piece is up to S consecutive keys of one bucket tile's column-major stream
 // (the runs of kTB = 32 buckets of up to F consecutive columns), planned by
-// k_piece_plan.  Its image in the output is the stable bucket-major order of those
+// k_piece_plan2.  Its image in the output is the stable bucket-major order of those
 // keys (column order, then row order, within each bucket: the order Alg 3 writes,
 // P:438-449); a bucket of the tile is the concatenation of its sub-chunk in every
-// piece, in piece order (L21).  Per piece:
-//  * fragments: run f is copied, 16-byte aligned around its misalignment, into its
-//    own slot by thread f (16-byte cp.async; bulk copies (TMA) of ~128-byte runs
-//    were measured slower); the slots are packed by an exclusive scan of their
-//    rounded sizes, and a bitmap marks the slot words that hold keys of a run.
-//    The next piece is staged into a second buffer while this one is processed;
-//  * pass 1: each 32-word chunk of the slot array is one warp step: a key's bucket
-//    is the number of the tile's 31 thresholds it has passed (branch-free 5-step
-//    search; equal-pivot rule L4), keys of one bucket within the chunk are ranked
-//    with match.any (lane order = stream order) and the group's leader records the
-//    group size in the chunk's count row;
-//  * scan: per bucket, an exclusive scan of the count column down the chunks plus
-//    the bucket's start in the piece image turns every count into the first image
-//    position of its (chunk, bucket) group;
-//  * pass 2: every key goes to base[chunk][bucket] + rank; one bulk store (plus
-//    per-thread head and tail) writes the image; the bucket prefix goes to ppre.
-// Keys and codes stay in registers from pass 1 to pass 2 (each warp owns its chunks).
+// piece, in piece order (L21).  Per piece (k_transpose_ws):
+//  * a producer warp loads the piece descriptor, the tile's thresholds and the run
+//    bounds before waiting for its ring buffer, then copies every run (16-byte
+//    cp.async around its misalignment) into the slot array, marks the slot words
+//    that hold keys in a bitmap, and signals the buffer's mbarrier;
+//  * pass 1 (eight consumer warps): each thread owns KT consecutive slot words; a
+//    key's bucket is found by a branch-free 5-step search over the tile's 31
+//    thresholds (held one per lane, read with shuffles; equal-pivot rule L4) and
+//    ranked among the thread's keys of that bucket by a shared atomic counter;
+//  * scan: the counters in bucket-major, thread-minor order (= stream order within
+//    a bucket) give every (bucket, thread) group its first image position;
+//  * pass 2: every key goes to its image position; one bulk store (plus per-thread
+//    head and tail) writes the image, the bucket prefix goes to ppre and the
+//    piece's bucket counts are added to the level's bucket sizes.
 #pragma once
 #include "level2.cuh"
 
@@ -32,14 +29,9 @@ namespace sq {
 enum { kMxPiece = 0, kMxNch, kMxPn, kMxOut, kMxNb, kMxBmax, kMxValid, kMxBbase };
 
 // ------------------------------------------------------------------------------
-// The same SkewTranspose with per-thread counters (the sort path's transpose):
-// thread t owns KT consecutive words of the staged slot array (KT/VW 16-byte
-// vectors, an odd number, so LDS.128 is conflict-free without padding).  Pass 1:
-// each key's bucket (5-step search over the thresholds, held one per lane and read
-// with shuffles) and its rank among the thread's keys of that bucket (a u16 counter
-// per (bucket, thread)).  An exclusive scan of the counters in bucket-major,
-// thread-minor order (= stream order within a bucket) gives every (bucket, thread)
-// group its first image position.  Pass 2 scatters the keys into the image.
+// Consumer word layout: thread t owns KT consecutive words of the staged slot
+// array (KT/VW 16-byte vectors, an odd number, so LDS.128 is conflict-free without
+// padding); a slot holds S keys plus the alignment padding of up to F runs.
 template <typename K, bool PAIRS, int NT, int S, int F>
 struct CtCfg {
   static constexpr int NB = 2;  // staging buffers (2: the next piece is staged during this one)
@@ -71,281 +63,6 @@ struct CtCfg {
 // (e / 32) % 8, so both the per-thread scan reads (32 consecutive entries) and the
 // per-warp atomics (32 consecutive entries of one bucket) are conflict-free
 __device__ __forceinline__ uint32_t cswz(uint32_t e) { return e ^ (((e >> 5) & 7) << 2); }
-
-template <typename K, bool PAIRS, int NT, int S, int F>
-__device__ __forceinline__ void ct_stage(const PieceDesc& pd, bool valid, int b, unsigned char* sm,
-                                         const K* __restrict__ src, const uint32_t* __restrict__ vsrc,
-                                         const K* __restrict__ piv, const uint32_t* __restrict__ segmat) {
-  using C = CtCfg<K, PAIRS, NT, S, F>;
-  constexpr int EB = sizeof(K), NW = C::NW;
-  const int t = threadIdx.x;
-  uint32_t* meta = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16 + 32 * 4);
-  if (!valid) {
-    asm volatile("cp.async.commit_group;\n" ::: "memory");  // empty group: wait_group counts stay aligned
-    return;
-  }
-  K* slot = reinterpret_cast<K*>(sm + C::off_slot + b * C::SLOT_B);
-  uint32_t* vslot = reinterpret_cast<uint32_t*>(sm + C::off_vslot + b * C::VSLOT_B);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(sm + C::off_bits + b * C::BITS_B);
-  Thr<K>* thr = reinterpret_cast<Thr<K>*>(sm + C::off_thr + b * C::THR_B);
-  uint32_t* thr32 = reinterpret_cast<uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  const uint32_t nb = pd.nb;
-  const uint32_t Pn = pd.pn, nf = pd.nf;
-  if (t < 32) {
-    const K* P = piv + pd.thr0;  // boundary j = first+1+t uses pivot P[t], dup if P[t-1] == P[t]
-    const bool real = t < (int)nb - 1;
-    const K pj = real ? P[t] : K(0);
-    const bool dup = real && pd.bt * kTB + t >= 1 && P[t - 1] == pj;
-    thr[t] = Thr<K>::make(pj, dup, !real);
-    uint32_t cntmax = 0;
-    if constexpr (sizeof(K) == 4) {
-      // passed(x) == (x >= thr32) for every key except 0xffffffff, whose bucket is
-      // the number of real thresholds that are at most 0xffffffff
-      const uint64_t t64 = real ? uint64_t(pj) + (dup ? 1u : 0u) : (1ull << 32);
-      thr32[t] = t64 > 0xffffffffull ? 0xffffffffu : (uint32_t)t64;
-      cntmax = __popc(__ballot_sync(0xffffffffu, t64 <= 0xffffffffull));
-    }
-    if (t == 0) {
-      meta[kMxPiece] = pd.slot;
-      meta[kMxPn] = Pn;
-      meta[kMxOut] = pd.out;
-      meta[kMxNb] = nb;
-      meta[kMxBmax] = cntmax;
-    }
-  }
-  // fragments: runs of columns col .. col+nf-1 (the first starts at `off`), clipped
-  // to the piece; packed 16-byte aligned slots
-  uint32_t len = 0, srcpos = 0, mis = 0, sbytes = 0;
-  if (t < (int)nf) {
-    const uint32_t* row = segmat + pd.row0 + t;  // tile-major: the next boundary is rstride (= ncols) on
-    const uint32_t a = row[0] + (t == 0 ? pd.off : 0), e = row[pd.rstride];
-    len = e - a;
-    srcpos = pd.src0 + t * pd.rows + a;
-  }
-  uint32_t wtot;
-  const uint32_t ex = block_excl_sum<NW>(len, misc, &wtot);
-  const uint32_t flen = t < (int)nf ? min(ex + len, Pn) - min(ex, Pn) : 0;
-  if (flen) {
-    mis = (uint32_t)(reinterpret_cast<uintptr_t>(src + srcpos) & 15);
-    sbytes = (mis + flen * EB + 15) & ~15u;
-  }
-  uint32_t stot;
-  const uint32_t so = block_excl_sum<NW>(sbytes, misc + 32, &stot);  // slot byte offset
-  const uint32_t nbw = (stot / EB + 31) / 32 + 1;                    // bitmap words in use (+1 guard)
-  for (uint32_t i = t; i < nbw; i += NT) bits[i] = 0;
-  if (t == 0) meta[kMxNch] = stot / EB;  // slot words in use
-  __syncthreads();
-  if (flen) {
-    const uint32_t e0 = (so + mis) / EB, e1 = e0 + flen;  // word range of the run's keys
-    for (uint32_t wd = e0 >> 5; wd <= (e1 - 1) >> 5; wd++) {
-      const uint32_t lo = max(e0, wd * 32) - wd * 32, hi = min(e1, wd * 32 + 32) - wd * 32;
-      const uint32_t m = (hi == 32 ? 0xffffffffu : ((1u << hi) - 1)) & ~((1u << lo) - 1);
-      atomicOr(&bits[wd], m);
-    }
-    const uint32_t sdst = smem_addr(slot) + so;
-    const unsigned char* g = reinterpret_cast<const unsigned char*>(src + srcpos) - mis;
-    for (uint32_t v = 0; v < sbytes; v += 16)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
-    if (PAIRS) {  // values at the same word index (per-element async copies)
-      const uint32_t* gv = vsrc + srcpos;
-      for (uint32_t k = 0; k < flen; k++) cp_async_elem(&vslot[e0 + k], &gv[k]);
-    }
-  }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-
-template <typename K, bool PAIRS, int NT, int S, int F>
-__global__ void __launch_bounds__(NT, 3)
-k_transpose_ct(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict__ pcount, const K* __restrict__ src,
-               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-               const K* __restrict__ piv, const uint32_t* __restrict__ segmat, uint16_t* __restrict__ ppre) {
-  using C = CtCfg<K, PAIRS, NT, S, F>;
-  constexpr int EB = sizeof(K), NW = C::NW, KT = C::KT, VW = C::VW;
-  static_assert(F <= NT && NT % 32 == 0 && S <= 65535 && kTB == 32 && KT < 64 && C::NB == 2, "shape");
-  extern __shared__ __align__(128) unsigned char sm[];
-  unsigned char* outraw = sm + C::off_out;
-  unsigned char* voutraw = sm + C::off_vout;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + C::off_cnt);  // [bucket][thread], + a dummy row
-  uint32_t* misc = reinterpret_cast<uint32_t*>(sm + C::off_misc);
-  uint32_t* poff = misc + 64;
-  const int t = threadIdx.x, lane = t & 31;
-  const uint32_t npieces = *pcount;
-
-  // descriptors are loaded one piece ahead of their staging, which runs one piece
-  // ahead of the processing
-  int b = 0;
-  uint32_t i = blockIdx.x;
-  PieceDesc nx = i < npieces ? pieces[i] : PieceDesc{};
-  ct_stage<K, PAIRS, NT, S, F>(nx, i < npieces, 0, sm, src, vsrc, piv, segmat);
-  nx = i + gridDim.x < npieces ? pieces[i + gridDim.x] : PieceDesc{};
-  for (; i < npieces; i += gridDim.x) {
-    // stage the next piece into the other buffer while this one is processed
-    const uint32_t in = i + gridDim.x;
-    ct_stage<K, PAIRS, NT, S, F>(nx, in < npieces, b ^ 1, sm, src, vsrc, piv, segmat);
-    nx = in + gridDim.x < npieces ? pieces[in + gridDim.x] : PieceDesc{};
-    for (int q = t; q < 33 * NT; q += NT) cnt[q] = 0;  // 32 bucket rows + the dummy row
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    __syncthreads();
-    const K* slot = reinterpret_cast<const K*>(sm + C::off_slot + b * C::SLOT_B);
-    const uint32_t* vslot = reinterpret_cast<const uint32_t*>(sm + C::off_vslot + b * C::VSLOT_B);
-    const uint32_t* bits = reinterpret_cast<const uint32_t*>(sm + C::off_bits + b * C::BITS_B);
-    const Thr<K>* thr = reinterpret_cast<const Thr<K>*>(sm + C::off_thr + b * C::THR_B);
-    const uint32_t* thr32 = reinterpret_cast<const uint32_t*>(sm + C::off_thr + b * C::THR_B + 32 * 16);
-    const uint32_t* meta = thr32 + 32;
-    const uint32_t nwords = meta[kMxNch], Pn = meta[kMxPn], oc = meta[kMxOut], bmax = meta[kMxBmax];
-    const uint32_t nb = meta[kMxNb];
-    const uint32_t thr_r = sizeof(K) == 4 ? thr32[lane] : 0u;
-    // ---- pass 1: buckets and thread-local ranks
-    const uint32_t w0 = t * KT;
-    uint32_t vb;  // validity of the thread's KT words
-    {
-      const uint32_t bw = w0 >> 5, sh = w0 & 31;
-      vb = __funnelshift_r(bits[bw], bits[bw + 1], sh);
-      if (KT < 32) vb &= (1u << KT) - 1;
-      if (w0 >= nwords) vb = 0;
-    }
-    K xs[KT];
-    uint32_t cdp[(KT + 1) / 2];  // per key: bucket | thread-local rank << 6, two per word
-#pragma unroll
-    for (int q = 0; q < KT / VW; q++) {
-      const uint4 v4 = reinterpret_cast<const uint4*>(slot)[t * (KT / VW) + q];
-      if constexpr (sizeof(K) == 4) {
-        xs[4 * q] = v4.x; xs[4 * q + 1] = v4.y; xs[4 * q + 2] = v4.z; xs[4 * q + 3] = v4.w;
-      } else {
-        xs[2 * q] = (uint64_t(v4.y) << 32) | v4.x;
-        xs[2 * q + 1] = (uint64_t(v4.w) << 32) | v4.z;
-      }
-    }
-    // thresholds in Eytzinger (BFS) order, lane l holding node l (l = 1..31): the
-    // search is i = 2i + [x >= E[i]] five times from i = 1, bucket = i - 32; the
-    // first two levels use the same three thresholds for every key
-    uint32_t E_r = 0;
-    if constexpr (sizeof(K) == 4) {
-      // node l at depth d = floor(log2 l) covers sorted index (2(l - 2^d) + 1) * 2^(4-d) - 1
-      const uint32_t l = lane ? lane : 1, d = 31 - __clz(l);
-      E_r = __shfl_sync(0xffffffffu, thr_r, ((2 * (l - (1u << d)) + 1) << (4 - d)) - 1);
-    }
-    const uint32_t E1 = __shfl_sync(0xffffffffu, E_r, 1), E2 = __shfl_sync(0xffffffffu, E_r, 2),
-                   E3 = __shfl_sync(0xffffffffu, E_r, 3);
-#pragma unroll
-    for (int j = 0; j < KT; j++) {
-      const K x = xs[j];
-      uint32_t bk = 0;
-      if constexpr (sizeof(K) == 4) {
-        const uint32_t p1 = uint32_t(x) >= E1 ? 1u : 0u;
-        uint32_t i = 2 + p1;
-        i = 2 * i + (uint32_t(x) >= (p1 ? E3 : E2) ? 1u : 0u);
-#pragma unroll
-        for (int st = 0; st < 3; st++) i = 2 * i + (uint32_t(x) >= __shfl_sync(0xffffffffu, E_r, i) ? 1u : 0u);
-        // saturated thresholds: only 0xffffffff can pass them, and its bucket is bmax
-        bk = min(i - 32, bmax);
-      } else {
-#pragma unroll
-        for (int st = 16; st >= 1; st >>= 1) bk += thr[bk + st - 1].passed(x) ? st : 0;
-      }
-      bk = ((vb >> j) & 1) ? bk : 32u;  // invalid words count in a dummy row
-      // shared atomics: the counter updates of one thread are independent (a
-      // load/store pair would serialise them through possible aliasing)
-      const uint32_t r = atomicAdd(&cnt[cswz(bk * NT + t)], 1u);
-      const uint32_t c = bk | (r << 6);
-      if (j & 1) cdp[j / 2] |= c << 16;
-      else cdp[j / 2] = c;
-    }
-    __syncthreads();
-    // ---- exclusive scan of the counters, bucket-major (thread u: entries 32u .. 32u+31,
-    // read as eight 16-byte chunks; the swizzle makes them conflict-free)
-    {
-      uint32_t sum = 0;
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        const uint4 q = *reinterpret_cast<const uint4*>(&cnt[cswz(32 * t + 4 * i)]);
-        sum += q.x + q.y + q.z + q.w;
-      }
-      uint32_t tot;
-      uint32_t run = block_excl_sum<NW>(sum, misc, &tot);
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        uint4* p4 = reinterpret_cast<uint4*>(&cnt[cswz(32 * t + 4 * i)]);
-        const uint4 q = *p4;
-        uint4 o;
-        o.x = run; run += q.x;
-        o.y = run; run += q.y;
-        o.z = run; run += q.z;
-        o.w = run; run += q.w;
-        *p4 = o;
-      }
-    }
-    __syncthreads();
-    if (t < 32) poff[t] = t < (int)nb ? cnt[cswz(t * NT)] : Pn;
-    if (t == 32) poff[kTB] = Pn;
-    if (t == 0) bulk_wait_read0();  // previous piece's image has been read out
-    __syncthreads();
-    // ---- pass 2: scatter into the piece image (shifted for the bulk store)
-    const uint32_t oshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst + oc) & 15) / EB);
-    K* outb = reinterpret_cast<K*>(outraw) + oshift;
-    const uint32_t vshift = PAIRS ? (uint32_t)((reinterpret_cast<uintptr_t>(vdst + oc) & 15) / 4) : 0;
-    uint32_t* vout = reinterpret_cast<uint32_t*>(voutraw) + vshift;
-#pragma unroll
-    for (int q = 0; q < KT / VW; q++) {  // keys re-read from the stage (fewer live registers)
-      const uint4 v4 = reinterpret_cast<const uint4*>(slot)[t * (KT / VW) + q];
-      if constexpr (sizeof(K) == 4) {
-        xs[4 * q] = v4.x; xs[4 * q + 1] = v4.y; xs[4 * q + 2] = v4.z; xs[4 * q + 3] = v4.w;
-      } else {
-        xs[2 * q] = (uint64_t(v4.y) << 32) | v4.x;
-        xs[2 * q + 1] = (uint64_t(v4.w) << 32) | v4.z;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < KT; j++) {
-      const uint32_t c = (cdp[j / 2] >> (16 * (j & 1))) & 0xffffu;
-      const uint32_t bk = c & 63;
-      if (bk < 32) {
-        const uint32_t dpos = cnt[cswz(bk * NT + t)] + (c >> 6);
-        outb[dpos] = xs[j];
-        if (PAIRS) vout[dpos] = vslot[w0 + j];
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    {
-      const uintptr_t g0 = reinterpret_cast<uintptr_t>(dst + oc);
-      const uintptr_t g1 = g0 + uintptr_t(Pn) * EB;
-      const uintptr_t a0 = (g0 + 15) & ~uintptr_t(15), a1 = g1 & ~uintptr_t(15);
-      if (a1 > a0) {
-        if (t == 0)
-          bulk_s2g(reinterpret_cast<void*>(a0), reinterpret_cast<unsigned char*>(outb) + (a0 - g0),
-                   (uint32_t)(a1 - a0));
-        const uint32_t nh = (uint32_t)((a0 - g0) / EB), nt0 = (uint32_t)((a1 - g0) / EB);
-        if (t < (int)nh) dst[oc + t] = outb[t];
-        if (t < (int)(Pn - nt0)) dst[oc + nt0 + t] = outb[nt0 + t];
-      } else {
-        for (uint32_t q = t; q < Pn; q += NT) dst[oc + q] = outb[q];
-      }
-      if (PAIRS) {
-        const uintptr_t h0 = reinterpret_cast<uintptr_t>(vdst + oc);
-        const uintptr_t h1 = h0 + uintptr_t(Pn) * 4;
-        const uintptr_t c0 = (h0 + 15) & ~uintptr_t(15), c1 = h1 & ~uintptr_t(15);
-        if (c1 > c0) {
-          if (t == 0)
-            bulk_s2g(reinterpret_cast<void*>(c0), reinterpret_cast<unsigned char*>(vout) + (c0 - h0),
-                     (uint32_t)(c1 - c0));
-          const uint32_t nh = (uint32_t)((c0 - h0) / 4), nt0 = (uint32_t)((c1 - h0) / 4);
-          if (t < (int)nh) vdst[oc + t] = vout[t];
-          if (t < (int)(Pn - nt0)) vdst[oc + nt0 + t] = vout[nt0 + t];
-        } else {
-          for (uint32_t q = t; q < Pn; q += NT) vdst[oc + q] = vout[q];
-        }
-      }
-      if (t == 0) bulk_commit();
-    }
-    if (t <= kTB) ppre[uint64_t(meta[kMxPiece]) * kPP + t] = (uint16_t)poff[t];
-    __syncthreads();
-    b ^= 1;
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-}
 
 // ------------------------------------------------------------------------------
 // Warp-specialised SkewTranspose (the sort path's transpose): one producer warp
