@@ -92,13 +92,13 @@ class Clocks:
 def cpu_baseline(keys, seconds_hint=True):
     """The oracle as it stands, single-threaded, on a bounded sample of the workload."""
     import oracle as O
-    n = 1 << 22
+    n = 1 << 25  # ~10 s of single-core work
     sample = keys[:n].copy()
     t0 = time.perf_counter()
     O.square_sort(sample, seed=5)
     dt = time.perf_counter() - t0
     return {"value": n / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first 2^22 keys of the cfg5 input (uniform u32, seed 5), oracle SquareSort "
+            "sample": f"first 2^25 keys of the cfg5 input (uniform u32, seed 5), oracle SquareSort "
                       f"cutoff 16 / threshold 4, one run, {dt:.2f} s on 1 host core",
             "host_cpu": _cpu_model(), "host_nproc": os.cpu_count()}
 
