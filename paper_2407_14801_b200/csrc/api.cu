@@ -700,7 +700,7 @@ struct Engine {
     SQ_CUDA(cudaMemsetAsync(bsize, 0, buck_tot * 4, st));
     {
       ProfScope ps("tiles", st);
-      k_tile_sizes<<<ntiles, 256, 0, st>>>(dL, dTiles, segmat);
+      k_tile_sizes<<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat);
       check_launch("k_tile_sizes");
       k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, kPlanFW, dPieceBase);
       check_launch("k_tile_scan");
@@ -713,7 +713,7 @@ struct Engine {
       SQ_CUDA(cudaMemsetAsync(pstatus, 0, uint64_t(ntiles) * 8, st));
       {
         ProfScope ps("tiles", st);
-        k_piece_plan2<256, TC::S, kPlanFW><<<ntiles, 256, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout, pstatus);
+        k_piece_plan2<1024, TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout, pstatus);
         check_launch("k_piece_plan2");
       }
       ar.release(pstatus);
