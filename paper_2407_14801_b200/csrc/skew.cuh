@@ -287,6 +287,12 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
     }
     K xs[KT];
     uint32_t cdp[(KT + 1) / 2];  // per key: bucket | thread-local rank << 6, two per word
+    // warps whose words all lie past the staged runs (the slot is sized for the
+    // worst-case alignment padding; ~1 warp in 8 usually) skip pass 1
+    if (!__any_sync(0xffffffffu, vb != 0)) {
+#pragma unroll
+      for (int q = 0; q < (KT + 1) / 2; q++) cdp[q] = 32u | (32u << 16);
+    } else {
 #pragma unroll
     for (int q = 0; q < KT / VW; q++) {
       const uint4 v4 = reinterpret_cast<const uint4*>(slot)[t * (KT / VW) + q];
@@ -324,6 +330,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
       const uint32_t c = bk | (r << 6);
       if (j & 1) cdp[j / 2] |= c << 16;
       else cdp[j / 2] = c;
+    }
     }
     cons_bar();
     {  // exclusive scan of the counters, bucket-major
