@@ -646,7 +646,7 @@ struct PlanOut {
 // Bucket plan, one warp per bucket tile: lane j takes bucket j of the tile; its final offset is the tile's
 // offset plus the sizes of the tile's earlier buckets (a warp scan -- the tile
 // offsets are already the segment's prefix, P:283 / P:461); then the records and
-// work lists of k_bucket_plan, and lane 0 packs the small buckets into units.
+// work lists (single-value, size classes, merge chunks and tiles, oversize), and lane 0 packs the small buckets into units.
 template <typename K>
 __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const TileInfo* __restrict__ tiles,
                                    uint32_t ntiles, const uint32_t* __restrict__ bsize, const K* __restrict__ piv,
