@@ -96,8 +96,8 @@ def _check(rc: int):
 
 
 def _stream(stream):
-    if stream is not None:
-        return ctypes.c_void_p(int(stream))
+    if stream is not None:  # a torch.cuda.Stream or a raw cudaStream_t handle
+        return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
     import torch
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 

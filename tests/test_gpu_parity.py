@@ -421,3 +421,34 @@ def test_signed_and_float_keys(dt, n):
     got = t.cpu().numpy()
     u = np.uint32 if npdt.itemsize == 4 else np.uint64
     assert np.array_equal(got.view(u), want.view(u))
+
+
+def test_concurrent_calls_two_threads():
+    # the header allows concurrent calls on different streams with disjoint buffers
+    # (per-thread library state); ctypes releases the GIL during the calls
+    import threading
+    rng = np.random.default_rng(41)
+    arrs = [rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32) for n in (3_000_001, 1_500_007)]
+    outs, errs = [None, None], []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                t = torch.from_numpy(arrs[i]).cuda()
+                for _ in range(3):
+                    w = t.clone()
+                    sq.sort_u32(w, i, stream=s)
+                s.synchronize()
+                outs[i] = w.cpu().numpy()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs
+    for a, o in zip(arrs, outs):
+        assert np.array_equal(o, np.sort(a))
