@@ -353,7 +353,7 @@ template <> struct TrCfg<uint32_t, false> { static constexpr int NT = 256, S = 4
 template <> struct TrCfg<uint32_t, true> { static constexpr int NT = 256, S = 4096, G = 256; };
 template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
 // piece-major transpose (sort path): threads, piece size, fragments per piece
-constexpr int kPlanFW = 120;  // piece-plan window (columns); <= the transpose's F = 128
+constexpr int kPlanFW = 128;  // piece-plan window (columns); <= the transpose's F = 128
 template <typename K, bool PAIRS> struct PmTr;
 template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
 template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
