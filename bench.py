@@ -144,6 +144,25 @@ def run_reference(args, rank):
     }), flush=True)
 
 
+def bind_to_gpu_cpus(index: int):
+    """Run on the CPUs NVML reports as affine to the GPU, so the pinned host
+    buffers of the e2e leg are first-touched on the GPU's NUMA node.  Best effort:
+    returns the CPU list, or None when NVML or the affinity call is unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return sorted(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def max_over_ranks(x: float, dist=None) -> float:
     """The job's time is the slowest rank's (device-timed on each rank)."""
     if dist is None:
@@ -185,6 +204,7 @@ def main():
     import sqinputs as S
 
     torch.cuda.set_device(local)
+    affinity = bind_to_gpu_cpus(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -344,6 +364,7 @@ def main():
                       "api": "sq_sort_u32_host_batch (pinned host buffers; every step = H2D of n keys + sort + "
                              "D2H of n keys, consecutive steps pipelined on copy streams)",
                       "output_check": "sorted" if e_ok else "FAILED",
+                      "host_cpus": "GPU-affine (NVML): %s" % (f"{affinity[0]}-{affinity[-1]}" if affinity else "not set"),
                       "unpipelined": {"value": world * n / (sm / 1e3) / 1e9, "ms_per_step": sm,
                                       "api": "sq_sort_u32_host, one call per step"}}
     if rank == 0 and world == 1 and not args.no_cpu:
