@@ -285,7 +285,13 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp))["bytes_per_launch"].get(dname)
+            tj = json.load(open(tp))
+            traffic = tj["bytes_per_launch"].get(dname)
+            # the library may time a role as one span over several kernel launches
+            # (concurrent bucket-sort classes): traffic per timed unit, like `achieved`
+            lpc = tj.get("launches_per_call", {}).get(dname)
+            if traffic is not None and lpc and per_step_launch:
+                traffic = traffic * lpc / per_step_launch
         except Exception:
             traffic = None
     mean_launch_s = dms / dlaunch / 1e3 if dlaunch else 0.0

@@ -49,15 +49,17 @@ def main(path, out_md, out_json, calls):
     lines = [f"# ncu launch list summary ({path}, {calls} sort calls)", "",
              "| role | launches/call | ms/call | share | DRAM read MB/call | DRAM write MB/call | DRAM bytes/launch |",
              "|---|---|---|---|---|---|---|"]
-    traffic = {}
+    traffic, per_call = {}, {}
     for r, (n, ms, rd, wr) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         per_launch = (rd + wr) / n
         traffic[r] = per_launch
+        per_call[r] = n / calls
         lines.append(f"| {r} | {n / calls:g} | {ms / calls:.3f} | {ms / tot_ms * 100:.1f}% | {rd / calls / 1e6:.1f} | "
                      f"{wr / calls / 1e6:.1f} | {per_launch:.4g} |")
     lines.append(f"| total | | {tot_ms / calls:.3f} | | | | |")
     open(out_md, "w").write("\n".join(lines) + "\n")
-    json.dump({"source": path, "sort_calls": calls, "bytes_per_launch": traffic}, open(out_json, "w"), indent=1)
+    json.dump({"source": path, "sort_calls": calls, "bytes_per_launch": traffic, "launches_per_call": per_call},
+              open(out_json, "w"), indent=1)
     print("\n".join(lines))
 
 
