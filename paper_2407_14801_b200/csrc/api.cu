@@ -823,7 +823,10 @@ struct Engine {
     int rr = 0;
     for (int c = (int)po.ncls - 1; c >= 0; c--) {  // biggest classes first
       const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
-      cudaStream_t cs = g_concurrent_classes ? ss.s[rr++ % SideStreams::N] : st;
+      // the biggest class gets a stream of its own; the others share the rest
+      cudaStream_t cs = !g_concurrent_classes ? st
+                        : c == (int)po.ncls - 1 ? ss.s[0]
+                                                : ss.s[1 + rr++ % (SideStreams::N - 1)];
       if (cls_cl[c]) {
         launch_cluster(cls_cl[c], cs, lst, po.count + c, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
         continue;
