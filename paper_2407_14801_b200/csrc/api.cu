@@ -784,9 +784,13 @@ struct Engine {
     po.mcount = (uint32_t*)ar.alloc(kMaxPasses * 4);
     SQ_CUDA(cudaMemsetAsync(po.mcount, 0, kMaxPasses * 4, st));
     po.cap_per_list = (uint32_t)(buck_tot + level_keys / std::max<uint32_t>(po.max_tile, 1) + 16);
-    po.list = (uint32_t*)ar.alloc(uint64_t(po.ncls + 3) * po.cap_per_list * 4);
-    po.count = (uint32_t*)ar.alloc((po.ncls + 3) * 4);
-    SQ_CUDA(cudaMemsetAsync(po.count, 0, (po.ncls + 3) * 4, st));
+    // lists: [0, ncls) classes, ncls copy, ncls+1 oversize, ncls+2 pair, then the
+    // chunks of merge-sorted buckets per class at ncls+3+c (sorted first, so that
+    // the merge passes can overlap the other classes)
+    const uint32_t nlists = 2 * po.ncls + 3;
+    po.list = (uint32_t*)ar.alloc(uint64_t(nlists) * po.cap_per_list * 4);
+    po.count = (uint32_t*)ar.alloc(nlists * 4);
+    SQ_CUDA(cudaMemsetAsync(po.count, 0, nlists * 4, st));
     {
       ProfScope ps("plan", st);
       k_tile_bucket_plan<K><<<(ntiles * 32 + 127) / 128, 128, 0, st>>>(dL, dTiles, ntiles, bsize, piv, recs, po);
@@ -817,19 +821,17 @@ struct Engine {
     // the caller's stream (fork to join); serial classes are timed per launch
     std::optional<ProfScope> span;
     if (g_concurrent_classes) span.emplace("bucketsort", st);
+    const bool merge = g_big_mode == 1;
+    // allocated on st before the fork, released on st after the join
+    uint32_t* splits = merge ? (uint32_t*)ar.alloc(uint64_t(po.mcap) * 4) : nullptr;
     cudaEvent_t fork = pool_event();
     SQ_CUDA(cudaEventRecord(fork, st));
     for (int i = 0; i < SideStreams::N; i++) SQ_CUDA(cudaStreamWaitEvent(ss.s[i], fork, 0));
-    int rr = 0;
-    for (int c = (int)po.ncls - 1; c >= 0; c--) {  // biggest classes first
-      const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
-      // the biggest class gets a stream of its own; the others share the rest
-      cudaStream_t cs = !g_concurrent_classes ? st
-                        : c == (int)po.ncls - 1 ? ss.s[0]
-                                                : ss.s[1 + rr++ % (SideStreams::N - 1)];
+    auto launch_class = [&](int c, uint32_t li, cudaStream_t cs) {
+      const uint32_t* lst = po.list + uint64_t(li) * po.cap_per_list;
       if (cls_cl[c]) {
-        launch_cluster(cls_cl[c], cs, lst, po.count + c, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
-        continue;
+        launch_cluster(cls_cl[c], cs, lst, po.count + li, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
+        return;
       }
       with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
         constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
@@ -844,20 +846,12 @@ struct Engine {
         std::optional<ProfScope> ps;
         if (!g_concurrent_classes) ps.emplace("bucketsort", cs);
         f<<<(uint32_t)std::min<uint64_t>(grid, po.cap_per_list), NT, smem, cs>>>(
-            recs, dTiles, lst, po.count + c, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
+            recs, dTiles, lst, po.count + li, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
             ppre, kb[2], PAIRS ? vb[2] : nullptr, po.units);
         check_launch("k_bucketsort");
       });
-    }
-    for (int i = 0; i < SideStreams::N && g_concurrent_classes; i++) {
-      cudaEvent_t j = pool_event();
-      SQ_CUDA(cudaEventRecord(j, ss.s[i]));
-      SQ_CUDA(cudaStreamWaitEvent(st, j, 0));
-      g_event_pool.push_back(j);
-    }
-    span.reset();
-    g_event_pool.push_back(fork);
-    if (g_big_mode == 1) {  // merge passes of the multi-CTA base case (buffers X <-> U)
+    };
+    auto launch_merges = [&](cudaStream_t ms) {  // merge passes of the multi-CTA base case (X <-> U)
       using MC = MergeCfg<K, PAIRS>;
       using BS = BlockSort<K, MC::NT, MC::VM>;
       const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
@@ -867,18 +861,44 @@ struct Engine {
         set_smem(f, smem);
         grid = wave_grid(f, MC::NT, smem);
       }
-      uint32_t* splits = (uint32_t*)ar.alloc(uint64_t(po.mcap) * 4);
       for (uint32_t p = 0; p < (uint32_t)kMaxPasses; p++) {
-        ProfScope ps("merge", st);
+        ProfScope ps("merge", ms);
         const MTile* items = po.mlist + uint64_t(p) * po.mcap;
-        k_merge_split<K><<<2 * num_sms(), 256, 0, st>>>(recs, items, po.mcount + p, p, po.mtile, kb[X], kb[2], splits);
+        k_merge_split<K><<<2 * num_sms(), 256, 0, ms>>>(recs, items, po.mcount + p, p, po.mtile, kb[X], kb[2], splits);
         check_launch("k_merge_split");
-        f<<<grid, MC::NT, smem, st>>>(recs, items, po.mcount + p, p, kb[X], kb[2], PAIRS ? vb[X] : nullptr,
+        f<<<grid, MC::NT, smem, ms>>>(recs, items, po.mcount + p, p, kb[X], kb[2], PAIRS ? vb[X] : nullptr,
                                       PAIRS ? vb[2] : nullptr, splits);
         check_launch("k_merge_pass");
       }
-      ar.release(splits);
+    };
+
+    if (!g_concurrent_classes) {
+      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, st);
+      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, st);
+      if (merge) launch_merges(st);
+    } else {
+      // streams 0-1: the chunks of merge-sorted buckets, then (stream 0) the merge
+      // passes; streams 2-3: whole buckets and units, which the merges overlap
+      int rc = 0, rw = 0;
+      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, ss.s[rc++ % 2]);
+      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, ss.s[2 + rw++ % 2]);
+      if (merge) {
+        cudaEvent_t e = pool_event();
+        SQ_CUDA(cudaEventRecord(e, ss.s[1]));
+        SQ_CUDA(cudaStreamWaitEvent(ss.s[0], e, 0));
+        g_event_pool.push_back(e);
+        launch_merges(ss.s[0]);
+      }
     }
+    for (int i = 0; i < SideStreams::N && g_concurrent_classes; i++) {
+      cudaEvent_t j = pool_event();
+      SQ_CUDA(cudaEventRecord(j, ss.s[i]));
+      SQ_CUDA(cudaStreamWaitEvent(st, j, 0));
+      g_event_pool.push_back(j);
+    }
+    span.reset();
+    g_event_pool.push_back(fork);
+    if (splits) ar.release(splits);
     {  // single-value buckets (copied) and oversize buckets (made contiguous),
        // in units of kGatherKeys keys so that huge buckets are copied by many CTAs
       ProfScope ps("gather", st);

@@ -704,12 +704,15 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
         const uint32_t slot = atomicAdd(&po.count[cls], 1u);
         po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16;
       } else {
+        const uint32_t lbase = rc.passes ? po.ncls + 3 : 0;  // chunks of merge-sorted buckets: own lists
         for (uint32_t k = 0; k < q; k++) {
           const uint32_t len = min(rc.chunk, size - k * rc.chunk);
-          int cls = 0;
+          uint32_t cls = 0;
           if (po.pair && len > po.max_tile) cls = po.ncls + 2;
-          else
+          else {
             while (po.cls_tile[cls] < len) cls++;
+            cls += lbase;
+          }
           const uint32_t slot = atomicAdd(&po.count[cls], 1u);
           po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16 + k;
         }
