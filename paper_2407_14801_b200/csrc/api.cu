@@ -391,7 +391,12 @@ static SideStreams& side_streams() {
   int dev = 0;
   SQ_CUDA(cudaGetDevice(&dev));
   if (ss.dev != dev) {
-    for (auto& x : ss.s) SQ_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    // streams 0-1 carry the critical path (chunk sorts, then the merge passes):
+    // highest priority, so their CTAs are scheduled before the other classes'
+    int lo = 0, hi = 0;
+    SQ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < SideStreams::N; i++)
+      SQ_CUDA(cudaStreamCreateWithPriority(&ss.s[i], cudaStreamNonBlocking, i < 2 ? hi : lo));
     ss.dev = dev;
   }
   return ss;
