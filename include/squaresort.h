@@ -22,9 +22,13 @@
  *    enqueued on it; the call also blocks the host on it once per recursion
  *    level (a device->host read of the bucket sizes that plans the next
  *    level), and the result is complete when the call returns.
- *  - Scratch: n keys (+ n values) plus O(n / 32) metadata (the paper's O(n)
- *    extra space), allocated stream-ordered from the device's
- *    default memory pool (cudaMallocAsync) and released before return.
+ *  - Scratch: up to 2n keys (+ 2n values when the multi-CTA merge base case
+ *    runs, sq_set_big_bucket_mode 1) plus O(n / 32) metadata (the paper's O(n)
+ *    extra space), allocated stream-ordered from a memory pool the
+ *    library owns (one per device; the device's default pool is not touched)
+ *    and freed into that pool before return.  The pool keeps freed scratch
+ *    reserved so a repeated sort does not re-map it; sq_trim_memory() returns
+ *    it to the system.
  *  - Errors are return codes only (sq_status); nothing is printed, no
  *    exception crosses the ABI.  sq_last_error_message() gives detail for the
  *    calling thread's last non-OK return.
@@ -168,6 +172,11 @@ typedef struct {
   uint32_t top_m;           /* m of the top level (0 if the input fit on chip)         */
   uint64_t oversize_keys;   /* keys in buckets that needed another level               */
 } sq_stats;
+
+/* Release the scratch the library's pool on the current device keeps reserved
+ * between calls (cudaMemPoolTrimTo 0).  Safe to call at any time; memory of
+ * calls still in flight on other streams stays mapped until they finish. */
+int sq_trim_memory(void);
 
 /* Statistics of the calling thread's last sort / transpose call. */
 void sq_get_stats(sq_stats *out);

@@ -24,7 +24,8 @@ EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_h
            "sq_sort_i32", "sq_sort_i64", "sq_sort_f32", "sq_sort_f64",
            "sq_sort_u64_host_batch", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
-           "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode"]
+           "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode",
+           "sq_trim_memory"]
 
 
 class SqError(RuntimeError):
@@ -86,6 +87,8 @@ def lib():
         L.sq_profile_read.restype = ctypes.c_int
         L.sq_debug_level_u32.argtypes = [vp, vp, sz, u64, vp, vp, vp, vp]
         L.sq_debug_level_u32.restype = ctypes.c_int
+        L.sq_trim_memory.argtypes = []
+        L.sq_trim_memory.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -95,20 +98,30 @@ def _check(rc: int):
         raise SqError(rc, lib().sq_last_error_message().decode())
 
 
-def _stream(stream):
+def _stream(stream, device=None):
     if stream is not None:  # a torch.cuda.Stream or a raw cudaStream_t handle
         return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
     import torch
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
-def _dev(t, dtype_name):
+def _dev(t, dtype_name, device=None):
+    """data_ptr() of a contiguous CUDA tensor of the given dtype (on `device` if given)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
         raise TypeError("expected a contiguous CUDA tensor")
     if str(t.dtype) != dtype_name:
         raise TypeError(f"expected {dtype_name}, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"tensor on {t.device}, expected {device}")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _on(t):
+    """Run the library call with the tensor's device current (the library works
+    on the current device and its stream)."""
+    import torch
+    return torch.cuda.device(t.device)
 
 
 def _seed(seed):
@@ -118,37 +131,43 @@ def _seed(seed):
 # ------------------------------------------------------------------ device-buffer calls
 def sort_u32(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.uint32 CUDA tensor in place (sq_sort_u32)."""
-    _check(lib().sq_sort_u32(_dev(keys, "torch.uint32"), keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_u32(_dev(keys, "torch.uint32"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 
 def sort_u64(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.uint64 CUDA tensor in place (sq_sort_u64)."""
-    _check(lib().sq_sort_u64(_dev(keys, "torch.uint64"), keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_u64(_dev(keys, "torch.uint64"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 
 def sort_i32(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.int32 CUDA tensor in place (sq_sort_i32)."""
-    _check(lib().sq_sort_i32(_dev(keys, "torch.int32"), keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_i32(_dev(keys, "torch.int32"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 
 def sort_i64(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.int64 CUDA tensor in place (sq_sort_i64)."""
-    _check(lib().sq_sort_i64(_dev(keys, "torch.int64"), keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_i64(_dev(keys, "torch.int64"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 
 def sort_f32(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.float32 CUDA tensor in place by IEEE totalOrder (sq_sort_f32)."""
-    _check(lib().sq_sort_f32(_dev(keys, "torch.float32"), keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_f32(_dev(keys, "torch.float32"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 
 def sort_f64(keys, seed: int = 0, stream=None):
     """Sort a contiguous torch.float64 CUDA tensor in place by IEEE totalOrder (sq_sort_f64)."""
-    _check(lib().sq_sort_f64(_dev(keys, "torch.float64"), keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_f64(_dev(keys, "torch.float64"), keys.numel(), _seed(seed), _stream(stream)))
     return keys
 
 
@@ -156,33 +175,35 @@ def sort_pairs_u32_u32(keys, vals, seed: int = 0, stream=None):
     """Stable sort of (keys, vals) uint32 CUDA tensors by key, in place."""
     if vals.numel() != keys.numel():
         raise ValueError("keys and vals differ in length")
-    _check(lib().sq_sort_pairs_u32_u32(_dev(keys, "torch.uint32"), _dev(vals, "torch.uint32"),
-                                       keys.numel(), _seed(seed), _stream(stream)))
+    with _on(keys):
+        _check(lib().sq_sort_pairs_u32_u32(_dev(keys, "torch.uint32"), _dev(vals, "torch.uint32", keys.device),
+                                           keys.numel(), _seed(seed), _stream(stream)))
     return keys, vals
 
 
 def skew_transpose(src, dst, rows: int, cols: int, pivots=None, k: int | None = None,
                    n: int = 0, buc_in=None, buc_out=None, naive_threshold: int = 4,
                    flags: int = 0, stream=None):
-    """sq_skew_transpose on torch.uint32 CUDA tensors.  Returns buc_out."""
+    """sq_skew_transpose on torch.uint32 CUDA tensors (all on src's device).  Returns buc_out."""
     import torch
     k = (pivots.numel() + 1 if pivots is not None else 1) if k is None else k
-    if buc_out is None:
-        buc_out = torch.empty(k, dtype=torch.uint32, device=src.device)
-    p = SkewParams(pivots.data_ptr() if pivots is not None and pivots.numel() else None, k, n,
-                   buc_in.data_ptr() if buc_in is not None else None, buc_out.data_ptr(),
-                   naive_threshold, flags)
-    _check(lib().sq_skew_transpose(ctypes.c_void_p(src.data_ptr()) if src.numel() else None,
-                                   ctypes.c_void_p(dst.data_ptr()) if dst.numel() else None,
-                                   rows, cols, ctypes.byref(p), _stream(stream)))
+    dev = src.device
+    with _on(src):
+        if buc_out is None:
+            buc_out = torch.empty(k, dtype=torch.uint32, device=dev)
+        ptr = lambda t: _dev(t, "torch.uint32", dev) if t is not None and t.numel() else None
+        p = SkewParams(ptr(pivots), k, n, ptr(buc_in), ptr(buc_out), naive_threshold, flags)
+        _check(lib().sq_skew_transpose(ptr(src), ptr(dst), rows, cols, ctypes.byref(p), _stream(stream)))
     return buc_out
 
 
 def debug_level_u32(src, dst, seed: int, pivots_out, bucend_out, info_out, stream=None):
-    _check(lib().sq_debug_level_u32(_dev(src, "torch.uint32"), _dev(dst, "torch.uint32"),
-                                    src.numel(), _seed(seed), _dev(pivots_out, "torch.uint32"),
-                                    _dev(bucend_out, "torch.uint32"), _dev(info_out, "torch.uint32"),
-                                    _stream(stream)))
+    d = src.device
+    with _on(src):
+        _check(lib().sq_debug_level_u32(_dev(src, "torch.uint32"), _dev(dst, "torch.uint32", d),
+                                        src.numel(), _seed(seed), _dev(pivots_out, "torch.uint32", d),
+                                        _dev(bucend_out, "torch.uint32", d), _dev(info_out, "torch.uint32", d),
+                                        _stream(stream)))
 
 
 # ------------------------------------------------------------------ host-buffer calls
@@ -255,6 +276,11 @@ BIG_LEVEL, BIG_MERGE, BIG_CLUSTER = 0, 1, 2
 def set_big_bucket_mode(mode: int):
     """0: recurse into a SquareSort level, 1: multi-CTA merge sort (default), 2: clusters."""
     _check(lib().sq_set_big_bucket_mode(mode))
+
+
+def trim_memory():
+    """Return the scratch the library's pool keeps on the current device (sq_trim_memory)."""
+    _check(lib().sq_trim_memory())
 
 
 def profile(enable: bool = True):

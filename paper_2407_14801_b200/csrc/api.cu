@@ -1,1145 +1,15 @@
-// api.cu -- host level scheduler and the C ABI of libsquaresort.so.
+// api.cu -- the C ABI of libsquaresort.so (include/squaresort.h).
 //
-// The scheduler runs SquareSort (Alg 1) level by level: a level is
-// one batched grid per step for ALL segments that are too large to sort on
-// chip, so the recursion -- shallow (O(log log n)) but very wide --
-// costs a handful of launches per level rather than one per recursive call.
-// Segments that fit on chip are sorted by the batched block sort (the GPU's
-// simple_sort), grouped in power-of-two size classes.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <atomic>
-#include <mutex>
-#include <cstdlib>
-#include <cstring>
-#include <map>
-#include <optional>
-#include <stdexcept>
-#include <string>
-#include <type_traits>
-#include <vector>
-#include <optional>
-
-#include "../../include/squaresort.h"
-#include "skew.cuh"
+// Each call validates its arguments (SQ_ERR_INVALID_ARGUMENT), checks the
+// device (SQ_ERR_UNSUPPORTED_DEVICE) and runs the engine (engine.cuh, compiled
+// per key type in inst_*.cu) or the standalone SkewTranspose (below).  No
+// exception crosses the ABI.
+#include "engine.cuh"
 
 namespace sq {
-
-// ------------------------------------------------------------------ errors
-struct Error : std::runtime_error {
-  int code;
-  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-static thread_local std::string g_errmsg;
-static thread_local sq_stats g_stats;
-
-#define SQ_CUDA(call)                                                                        \
-  do {                                                                                       \
-    cudaError_t e_ = (call);                                                                 \
-    if (e_ != cudaSuccess) {                                                                 \
-      if (e_ == cudaErrorMemoryAllocation) throw Error(SQ_ERR_OUT_OF_MEMORY, cudaGetErrorString(e_)); \
-      throw Error(SQ_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
-    }                                                                                        \
-  } while (0)
-
-static void check_launch(const char* what) {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw Error(SQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-  g_stats.kernel_launches++;
-}
-
-// ------------------------------------------------------------------ per-kernel timing
-// When enabled (sq_profile), every launch is bracketed by CUDA events on its
-// stream; elapsed times accumulate per kernel role after the call's final sync.
-struct ProfEntry {
-  const char* name;
-  cudaEvent_t a, b;
-};
-static std::atomic<bool> g_prof{false};
-static thread_local std::vector<ProfEntry> g_prof_pending;
-static thread_local std::vector<cudaEvent_t> g_event_pool;
-static std::mutex g_prof_mu;
-static std::map<std::string, std::pair<uint64_t, double>> g_prof_acc;
-static thread_local const char* g_role = "blocksort";
-
-static cudaEvent_t pool_event() {
-  if (!g_event_pool.empty()) {
-    cudaEvent_t e = g_event_pool.back();
-    g_event_pool.pop_back();
-    return e;
-  }
-  cudaEvent_t e;
-  SQ_CUDA(cudaEventCreate(&e));
-  return e;
-}
-
-struct ProfScope {
-  cudaStream_t st;
-  const char* name;
-  cudaEvent_t a = nullptr;
-  ProfScope(const char* n, cudaStream_t s) : st(s), name(n) {
-    if (g_prof.load()) {
-      a = pool_event();
-      cudaEventRecord(a, st);
-    }
-  }
-  ~ProfScope() {
-    if (a) {
-      cudaEvent_t b = pool_event();
-      cudaEventRecord(b, st);
-      g_prof_pending.push_back({name, a, b});
-    }
-  }
-};
-
-static void prof_collect() {  // after a stream sync
-  if (g_prof_pending.empty()) return;
-  std::lock_guard<std::mutex> lk(g_prof_mu);
-  for (auto& e : g_prof_pending) {
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) {
-      auto& v = g_prof_acc[e.name];
-      v.first++;
-      v.second += ms;
-    }
-    g_event_pool.push_back(e.a);
-    g_event_pool.push_back(e.b);
-  }
-  g_prof_pending.clear();
-}
-
-// ------------------------------------------------------------------ options
-static uint32_t g_max_tile = 0;  // 0 = default
-// buckets larger than one CTA's tile: 0 = another SquareSort level,
-// 1 = multi-CTA merge sort (default), 2 = thread-block cluster sort
-static int g_big_mode = 1;
-// bucket-sort size classes run concurrently on side streams (SQ_CONCURRENT_CLASSES=0
-// serialises them on the caller's stream; measured 6.47 vs 6.61 ms at cfg5)
-static int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv("SQ_CONCURRENT_CLASSES")) : 1;
-
-// ------------------------------------------------------------------ device check
-static void check_device() {
-  int dev = 0;
-  SQ_CUDA(cudaGetDevice(&dev));
-  static int checked[64] = {0};  // 1 ok, 2 bad
-  if (dev >= 0 && dev < 64 && checked[dev] == 1) return;
-  cudaDeviceProp p;
-  SQ_CUDA(cudaGetDeviceProperties(&p, dev));
-  const bool ok = p.major == 10 && p.minor == 0;
-  if (dev >= 0 && dev < 64) checked[dev] = ok ? 1 : 2;
-  if (!ok) throw Error(SQ_ERR_UNSUPPORTED_DEVICE, "device is sm_" + std::to_string(p.major) +
-                                                      std::to_string(p.minor) + ", need sm_100 (B200)");
-  // Keep freed scratch in the default pool between calls (stream-ordered reuse).
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-}
-
-// ------------------------------------------------------------------ small transfers
-// Descriptor uploads and size read-backs between pinned (UVA-mapped) host
-// staging and device memory are done by SM loads/stores, not by the copy
-// engines: a 1 GB copy of another batch item queued on a copy engine would
-// otherwise hold the sort's few-KB transfers back (sq_sort_*_host_batch).
-__global__ void k_xfer(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, size_t bytes) {
-  const size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x, T = size_t(gridDim.x) * blockDim.x;
-  if (((uintptr_t(src) | uintptr_t(dst)) & 15) == 0) {
-    const size_t n16 = bytes >> 4;
-    for (size_t i = t; i < n16; i += T) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
-    for (size_t i = (n16 << 4) + t; i < bytes; i += T) dst[i] = src[i];
-  } else {
-    for (size_t i = t; i < bytes; i += T) dst[i] = src[i];
-  }
-}
-
-static void xfer(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  if (!bytes) return;
-  const uint32_t g = (uint32_t)std::min<size_t>((bytes + 4095) / 4096, 148);
-  k_xfer<<<g, 256, 0, st>>>((const uint8_t*)src, (uint8_t*)dst, bytes);
-  check_launch("k_xfer");
-}
-
-// ------------------------------------------------------------------ per-call memory
-// Pinned host staging for descriptor uploads and size read-backs: one bump
-// pool per host thread, reused across calls (page-locking is expensive).
-struct PinnedPool {
-  std::vector<std::pair<char*, size_t>> blocks;
-  size_t cur = 0, used = 0;
-  void* get(size_t bytes) {
-    bytes = (bytes + 255) & ~size_t(255);
-    while (cur < blocks.size() && used + bytes > blocks[cur].second) {
-      cur++;
-      used = 0;
-    }
-    if (cur == blocks.size()) {
-      size_t sz = std::max<size_t>(bytes, size_t(8) << 20);
-      char* p = nullptr;
-      SQ_CUDA(cudaMallocHost((void**)&p, sz));
-      blocks.push_back({p, sz});
-      used = 0;
-    }
-    void* r = blocks[cur].first + used;
-    used += bytes;
-    return r;
-  }
-  void reset() { cur = 0; used = 0; }
-};
-static thread_local PinnedPool g_pinned;
-
-struct Arena {
-  cudaStream_t st;
-  std::vector<void*> dev;
-  bool used_host = false;
-  explicit Arena(cudaStream_t s) : st(s) {}
-  void* alloc(size_t bytes) {
-    void* p = nullptr;
-    SQ_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, st));
-    dev.push_back(p);
-    return p;
-  }
-  void release(void* p) {
-    auto it = std::find(dev.begin(), dev.end(), p);
-    if (it != dev.end()) {
-      cudaFreeAsync(p, st);
-      dev.erase(it);
-    }
-  }
-  void* pinned(size_t bytes) {
-    used_host = true;
-    return g_pinned.get(bytes);
-  }
-  // Several host arrays in one staging block and one transfer (one k_xfer launch
-  // instead of one per array); returns their device addresses in order.
-  std::vector<void*> upload_all(const std::vector<std::pair<const void*, size_t>>& parts) {
-    size_t tot = 0;
-    for (auto& p : parts) tot += (p.second + 15) & ~size_t(15);
-    std::vector<void*> out;
-    char* d = (char*)alloc(tot);
-    char* h = tot ? (char*)pinned(tot) : nullptr;
-    size_t o = 0;
-    for (auto& p : parts) {
-      if (p.second) memcpy(h + o, p.first, p.second);
-      out.push_back(d + o);
-      o += (p.second + 15) & ~size_t(15);
-    }
-    xfer(d, h, tot, st);
-    return out;
-  }
-  template <typename T>
-  static std::pair<const void*, size_t> part(const std::vector<T>& v) {
-    return {v.data(), v.size() * sizeof(T)};
-  }
-  template <typename T>
-  T* upload(const std::vector<T>& v) {
-    T* d = (T*)alloc(v.size() * sizeof(T));
-    if (!v.empty()) {
-      T* h = (T*)pinned(v.size() * sizeof(T));
-      memcpy(h, v.data(), v.size() * sizeof(T));
-      xfer(d, h, v.size() * sizeof(T), st);
-    }
-    return d;
-  }
-  ~Arena() {
-    for (void* p : dev) cudaFreeAsync(p, st);
-    if (used_host) {
-      cudaStreamSynchronize(st);  // staging may be reused by the next call
-      g_pinned.reset();
-    }
-  }
-};
-
-// ------------------------------------------------------------------ size classes
-// On-chip tiles (threads x keys per thread) for 32-bit sort keys and for
-// 64-bit sort keys (u64 keys, pair composites).
-static const uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 12288, 16384, 24576, 32768};
-
-template <typename SK> constexpr uint32_t key_max_tile() { return sizeof(SK) == 4 ? 32768u : 16384u; }
-
-static uint32_t tile_for(uint32_t len) {
-  for (uint32_t t : kTiles)
-    if (len <= t) return t;
-  return 0;
-}
-
-// Launch as a programmatic dependent of the previous kernel in the stream (it may
-// start before that one finishes; it must execute griddepcontrol.wait before it
-// touches that kernel's outputs).
-template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*f)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  SQ_CUDA(cudaLaunchKernelEx(&cfg, f, std::forward<Args>(args)...));
-}
-
-template <typename F>
-static void set_smem(F f, size_t bytes) {
-  SQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
-template <int N> using IC = std::integral_constant<int, N>;
-
-// f(IC<NT>, IC<V>) for the block shape of `tile` with sort key type SK.
-template <typename SK, typename F>
-static void with_tile(uint32_t tile, F&& f) {
-  if constexpr (sizeof(SK) == 4) {
-    switch (tile) {
-      case 64: return f(IC<32>{}, IC<2>{});
-      case 128: return f(IC<32>{}, IC<4>{});
-      case 256: return f(IC<32>{}, IC<8>{});
-      case 512: return f(IC<64>{}, IC<8>{});
-      case 1024: return f(IC<128>{}, IC<8>{});
-      case 2048: return f(IC<128>{}, IC<16>{});
-      case 3072: return f(IC<96>{}, IC<32>{});
-      case 4096: return f(IC<256>{}, IC<16>{});
-      case 6144: return f(IC<192>{}, IC<32>{});
-      case 8192: return f(IC<512>{}, IC<16>{});
-      case 12288: return f(IC<384>{}, IC<32>{});
-      case 16384: return f(IC<512>{}, IC<32>{});
-      case 24576: return f(IC<768>{}, IC<32>{});
-      case 32768: return f(IC<1024>{}, IC<32>{});
-    }
-  } else {
-    switch (tile) {
-      case 64: return f(IC<32>{}, IC<2>{});
-      case 128: return f(IC<32>{}, IC<4>{});
-      case 256: return f(IC<32>{}, IC<8>{});
-      case 512: return f(IC<64>{}, IC<8>{});
-      case 1024: return f(IC<128>{}, IC<8>{});
-      case 2048: return f(IC<256>{}, IC<8>{});
-      case 3072: return f(IC<192>{}, IC<16>{});
-      case 4096: return f(IC<256>{}, IC<16>{});
-      case 6144: return f(IC<384>{}, IC<16>{});
-      case 8192: return f(IC<512>{}, IC<16>{});
-      case 12288: return f(IC<768>{}, IC<16>{});
-      case 16384: return f(IC<1024>{}, IC<16>{});
-    }
-  }
-  throw Error(SQ_ERR_CUDA, "no block shape for tile " + std::to_string(tile));
-}
-
-static int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    SQ_CUDA(cudaGetDevice(&dev));
-    SQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return sms;
-}
-
-// One full wave of resident CTAs for a persistent kernel.
-template <typename F>
-static int wave_grid(F f, int nt, size_t smem) {
-  int occ = 0;
-  SQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, nt, smem));
-  return std::max(1, occ) * num_sms();
-}
-
-// count kernel configuration per key type (standalone SkewTranspose)
-template <typename K> struct CountCfg;
-template <> struct CountCfg<uint32_t> { static constexpr int NT = 512, STAGE = 16384, KSMEM = 16384; };
-template <> struct CountCfg<uint64_t> { static constexpr int NT = 512, STAGE = 8192, KSMEM = 16384; };
-
-// transpose configuration per (key type, pairs)
-template <typename K, bool PAIRS> struct TrCfg;
-template <> struct TrCfg<uint32_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
-template <> struct TrCfg<uint32_t, true> { static constexpr int NT = 256, S = 4096, G = 256; };
-template <> struct TrCfg<uint64_t, false> { static constexpr int NT = 256, S = 4096, G = 256; };
-// piece-major transpose (sort path): threads, piece size, fragments per piece
-constexpr int kPlanFW = 128;  // piece-plan window (columns); <= the transpose's F = 128
-template <typename K, bool PAIRS> struct PmTr;
-template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
-template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
-template <> struct PmTr<uint64_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
-
-// cluster bucket sort: per-CTA tile (threads x keys) for 32-bit / 64-bit sort keys
-// (small per-CTA tiles keep 3 CTAs per SM resident; the big one serves the
-// rare buckets beyond 16 small tiles)
-template <typename SK> struct ClusterCfg;
-template <> struct ClusterCfg<uint32_t> { static constexpr int NT = 256, V = 32, TILE = 8192; };
-template <> struct ClusterCfg<uint64_t> { static constexpr int NT = 256, V = 16, TILE = 4096; };
-template <typename SK> struct ClusterBig;
-template <> struct ClusterBig<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
-template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
-// largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
-template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
-
-// merge passes: threads x outputs per thread (tile = NT * VM keys)
-template <typename K, bool PAIRS> struct MergeCfg {
-  static constexpr int NT = 128, VM = PAIRS ? 16 : 32;
-};
-
-// Side streams for running the bucket-class kernels concurrently.
-struct SideStreams {
-  static constexpr int N = 4;
-  cudaStream_t s[N] = {};
-  int dev = -1;
-};
-static SideStreams& side_streams() {
-  static thread_local SideStreams ss;
-  int dev = 0;
-  SQ_CUDA(cudaGetDevice(&dev));
-  if (ss.dev != dev) {
-    // streams 0-1 carry the critical path (chunk sorts, then the merge passes):
-    // highest priority, so their CTAs are scheduled before the other classes'
-    int lo = 0, hi = 0;
-    SQ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    for (int i = 0; i < SideStreams::N; i++)
-      SQ_CUDA(cudaStreamCreateWithPriority(&ss.s[i], cudaStreamNonBlocking, i < 2 ? hi : lo));
-    ss.dev = dev;
-  }
-  return ss;
-}
-
-// ------------------------------------------------------------------ the engine
-struct Seg {
-  uint32_t off, len;
-  uint64_t node;
-};
-
-struct DebugOut {  // sq_debug_level_u32
-  uint32_t* dst;
-  uint32_t* pivots;
-  uint32_t* bucend;
-  uint32_t* info;
-};
-
-template <typename K, bool PAIRS>
-struct Engine {
-  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;  // on-chip sort key
-  cudaStream_t st;
-  Arena& ar;
-  K* kb[3];        // [0] caller's buffer, [1] scratch, [2] merge-sort scratch
-  uint32_t* vb[3];
-  size_t n;
-  uint32_t cap;
-
-  Engine(cudaStream_t s, Arena& a, K* keys, uint32_t* vals, size_t n_) : st(s), ar(a), n(n_) {
-    kb[0] = keys;
-    kb[1] = kb[2] = nullptr;
-    vb[0] = vals;
-    vb[1] = vb[2] = nullptr;
-    cap = key_max_tile<SK>();
-    if (g_max_tile && g_max_tile < cap) cap = g_max_tile;
-  }
-
-  void ensure_scratch() {
-    if (!kb[1]) kb[1] = (K*)ar.alloc(n * sizeof(K));
-    if (PAIRS && !vb[1]) vb[1] = (uint32_t*)ar.alloc(n * sizeof(uint32_t));
-  }
-  void ensure_third() {
-    if (!kb[2]) kb[2] = (K*)ar.alloc(n * sizeof(K));
-    if (PAIRS && !vb[2]) vb[2] = (uint32_t*)ar.alloc(n * sizeof(uint32_t));
-  }
-
-  void copy_ranges(const std::vector<SegDesc>& r, int src, int dst) {
-    if (r.empty() || src == dst) return;
-    const SegDesc* d = ar.upload(r);
-    ProfScope ps("copy", st);
-    k_copy_ranges<K><<<(uint32_t)r.size(), 256, 0, st>>>(d, kb[src], kb[dst], PAIRS ? vb[src] : nullptr,
-                                                         PAIRS ? vb[dst] : nullptr);
-    check_launch("k_copy_ranges");
-  }
-
-  // Contiguous segments of at most `cap` keys: one CTA each, by size class.
-  void blocksort(uint32_t tile, const std::vector<SegDesc>& d, int src, int dst, const char* role) {
-    const SegDesc* dd = ar.upload(d);
-    const uint32_t nseg = (uint32_t)d.size();
-    with_tile<SK>(tile, [&](auto nt, auto v) {
-      constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
-      using BS = BlockSort<SK, NT, V>;
-      ProfScope ps(role, st);
-      if constexpr (PAIRS) {
-        const size_t smem = BS::SMEM_BYTES + size_t(BS::TILE) * 4;
-        static bool init = false;
-        if (!init) { set_smem(k_blocksort_pairs<NT, V>, smem); init = true; }
-        k_blocksort_pairs<NT, V><<<nseg, NT, smem, st>>>(dd, kb[src], vb[src], kb[dst], vb[dst]);
-      } else {
-        static bool init = false;
-        if (!init) { set_smem(k_blocksort<K, NT, V>, BS::SMEM_BYTES); init = true; }
-        k_blocksort<K, NT, V><<<nseg, NT, BS::SMEM_BYTES, st>>>(dd, kb[src], kb[dst]);
-      }
-      check_launch("k_blocksort");
-    });
-  }
-
-  void sort_batch(const std::vector<Seg>& segs, int src, int dst, int depth, const char* role) {
-    if (depth > 48) throw Error(SQ_ERR_CUDA, "recursion too deep");
-    std::map<uint32_t, std::vector<SegDesc>> cls;
-    std::vector<Seg> big;
-    std::vector<SegDesc> bigr;
-    for (const Seg& s : segs) {
-      if (s.len == 0) continue;
-      if (s.len > cap) {
-        big.push_back(s);
-        bigr.push_back({s.off, s.len});
-      } else {
-        cls[std::max<uint32_t>(64, tile_for(s.len))].push_back({s.off, s.len});
-      }
-    }
-    for (auto& kv : cls) blocksort(kv.first, kv.second, src, dst, role);
-    if (!big.empty()) {
-      copy_ranges(bigr, src, dst);  // a level sorts a segment where it will end up
-      run_level(big, dst, depth, nullptr);
-    }
-  }
-
-  template <int CL, typename CC>
-  void launch_cluster_t(cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
-                        const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
-                        uint32_t nbuck) {
-    using BS = BlockSort<SK, CC::NT, CC::V>;
-    const size_t smem = 2 * BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * CC::NT + 64) * 4;
-    auto f = k_clustersort<K, CC::NT, CC::V, CL, PAIRS>;
-    static int max_clusters = -1;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(CC::NT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = cs;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (max_clusters < 0) {
-      set_smem(f, smem);
-      if (CL > 8) SQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      cfg.gridDim = dim3(CL * num_sms());
-      int mc = 0;
-      SQ_CUDA(cudaOccupancyMaxActiveClusters(&mc, f, &cfg));
-      max_clusters = mc;
-    }
-    if (max_clusters <= 0) throw Error(SQ_ERR_CUDA, "cluster of " + std::to_string(CL) + " CTAs cannot be scheduled");
-    cfg.gridDim = dim3(CL * std::min<uint32_t>(max_clusters, nbuck));
-    ProfScope ps("clustersort", cs);
-    SQ_CUDA(cudaLaunchKernelEx(&cfg, f, recs, tiles, lst, cnt, (const K*)kb[T], kb[X],
-                               (const uint32_t*)(PAIRS ? vb[T] : nullptr), PAIRS ? vb[X] : nullptr, pout, ppre));
-    check_launch("k_clustersort");
-  }
-
-  // cl > 0: clusters of `cl` small tiles; cl < 0: clusters of -cl big tiles
-  void launch_cluster(int cl, cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
-                      const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
-                      uint32_t nbuck) {
-    using CS = ClusterCfg<SK>;
-    using CB = ClusterBig<SK>;
-    if (cl == 4) launch_cluster_t<4, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
-    else if (cl == 8) launch_cluster_t<8, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
-    else if (cl == 16) launch_cluster_t<16, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
-    else launch_cluster_t<16, CB>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
-  }
-
-  // One SquareSort level (Alg 1) for a batch of segments that live in buffer X,
-  // their final place.  The SkewTranspose writes into the other buffer T; the
-  // bucket sorts gather from T and write the sorted buckets back into X.
-  void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
-    using TC = PmTr<K, PAIRS>;
-    ensure_scratch();
-    g_stats.levels++;
-    const int T = 1 - X;
-    const uint32_t ns = (uint32_t)segs.size();
-    std::vector<LevelSeg> L(ns);
-    std::vector<uint32_t> tile_base(ns), piece_seg_base(ns);
-    std::vector<TileInfo> tiles;
-    std::map<uint32_t, std::vector<ColDesc>> colcls;
-    std::vector<Seg> allcols;
-    std::vector<TaskDesc> mtasks;
-    bool generic = false;
-    uint64_t piv_tot = 0, buck_tot = 0, segmat_tot = 0, cand_tot = 0, piece_tot = 0;
-    uint32_t maxnp = 0;
-    for (uint32_t s = 0; s < ns; s++) {
-      const Seg& g = segs[s];
-      const uint32_t m = (uint32_t)ceil_sqrt(g.len);
-      LevelSeg& l = L[s];
-      l.off = g.off;
-      l.len = g.len;
-      l.rows = l.ncols = l.k = m;
-      l.nbt = (m + kTB - 1) / kTB;
-      l.piv_base = (uint32_t)piv_tot;
-      l.buck_base = (uint32_t)buck_tot;
-      l.segmat_base = segmat_tot;
-      l.cand_base = cand_tot;
-      l.node = g.node;
-      const uint32_t np = m - 1;
-      maxnp = std::max(maxnp, np);
-      piv_tot += np;
-      buck_tot += m;
-      segmat_tot += uint64_t(m) * (l.nbt + 1);
-      cand_tot += uint64_t(kCap) * np;
-      tile_base[s] = (uint32_t)tiles.size();
-      for (uint32_t bt = 0; bt < l.nbt; bt++) tiles.push_back({s, bt, 0, 0, 0, 0});
-      // windows per tile (plan_fw): at most ceil(m / kPlanFW) + size * 32 / (31 S) + 2
-      const uint32_t gpt = (m + kPlanFW - 1) / kPlanFW + 2;
-      piece_seg_base[s] = (uint32_t)piece_tot;
-      piece_tot += 3 * (g.len / TC::S) + uint64_t(l.nbt) * (1 + gpt) + 1;
-      // columns: fc full ones of m keys, then at most one ragged one
-      const uint32_t fc = (uint32_t)std::min<uint64_t>(m, g.len / m);
-      const uint32_t rem = fc < m ? (uint32_t)(g.len - uint64_t(fc) * m) : 0u;
-      if (m > cap) {
-        generic = true;
-        for (uint32_t c = 0; c < fc + (rem ? 1u : 0u); c++)
-          allcols.push_back({uint32_t(g.off + uint64_t(c) * m), c < fc ? m : rem, child_key(g.node, 0, c)});
-      } else {
-        std::vector<ColDesc>& full = colcls[std::max<uint32_t>(64, tile_for(m))];
-        full.reserve(full.size() + fc);
-        for (uint32_t c = 0; c < fc; c++) full.push_back({uint32_t(g.off + uint64_t(c) * m), m, s, c});
-        if (rem) colcls[std::max<uint32_t>(64, tile_for(rem))].push_back({uint32_t(g.off + uint64_t(fc) * m), rem, s, fc});
-      }
-      for (uint32_t c0 = 0; c0 < m; c0 += 64) mtasks.push_back({s, c0, std::min(m, c0 + 64)});
-    }
-    if (maxnp > key_max_tile<K>()) throw Error(SQ_ERR_INVALID_ARGUMENT, "pivot sample too large for one CTA");
-    const uint32_t ntiles = (uint32_t)tiles.size();
-
-    // every descriptor of the level in one transfer; the column descriptors too:
-    // nothing but kernels may sit between the sampler, the round selection and the
-    // column sort (programmatic dependent launch)
-    std::vector<std::pair<const void*, size_t>> parts = {Arena::part(L), Arena::part(tiles),
-                                                        Arena::part(tile_base), Arena::part(piece_seg_base),
-                                                        Arena::part(mtasks)};
-    if (!generic)
-      for (auto& kv : colcls) parts.push_back(Arena::part(kv.second));
-    const std::vector<void*> up = ar.upload_all(parts);
-    LevelSeg* dL = (LevelSeg*)up[0];
-    TileInfo* dTiles = (TileInfo*)up[1];
-    uint32_t* dTileBase = (uint32_t*)up[2];
-    uint32_t* dPieceBase = (uint32_t*)up[3];
-    TaskDesc* dM = (TaskDesc*)up[4];
-    K* cand = (K*)ar.alloc(std::max<uint64_t>(cand_tot, 1) * sizeof(K));
-    uint8_t* flags = (uint8_t*)ar.alloc(uint64_t(ns) * kCap);
-    K* p0s = (K*)ar.alloc(uint64_t(ns) * kCap * sizeof(K));
-    K* piv = (K*)ar.alloc(std::max<uint64_t>(piv_tot, 1) * sizeof(K));
-    uint32_t* info = (uint32_t*)ar.alloc(ns * 4);
-    uint32_t* fix = (uint32_t*)ar.alloc((ns + 1) * 4);
-    K* segmin = (K*)ar.alloc(ns * sizeof(K));
-    uint32_t* segmat = (uint32_t*)ar.alloc(segmat_tot * 4);
-    uint32_t* pout = (uint32_t*)ar.alloc(piece_tot * 4);
-    uint16_t* ppre = (uint16_t*)ar.alloc(piece_tot * kPP * 2);
-    BucketRec* recs = (BucketRec*)ar.alloc(buck_tot * sizeof(BucketRec));
-    SQ_CUDA(cudaMemsetAsync(fix, 0, (ns + 1) * 4, st));
-    SQ_CUDA(cudaMemsetAsync(segmin, 0xff, ns * sizeof(K), st));
-    SQ_CUDA(cudaMemsetAsync(segmat, 0, segmat_tot * 4, st));
-
-    std::vector<std::pair<uint32_t, const ColDesc*>> coldesc;
-    if (!generic) {
-      size_t q = 5;
-      for (auto& kv : colcls) coldesc.push_back({kv.first, (const ColDesc*)up[q++]});
-    }
-    // 1. pivots: all rounds in parallel from the level input (L9)
-    with_tile<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
-      constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
-      using BS = BlockSort<K, NT, V>;
-      static bool init = false;
-      if (!init) { set_smem(k_sample_all<K, NT, V>, BS::SMEM_BYTES); init = true; }
-      ProfScope ps("sample", st);
-      k_sample_all<K, NT, V><<<ns * kCap, NT, BS::SMEM_BYTES, st>>>(dL, kb[X], cand, flags, p0s);
-      check_launch("k_sample_all");
-    });
-    {
-      ProfScope ps("select", st);
-      launch_pdl(k_select_round<K>, ns, 256, 0, st, dL, ns, (const K*)cand, (const uint8_t*)flags, (const K*)p0s,
-                 (const K*)segmin, piv, info, fix, 0);
-    }
-    // 2. sort every column in place + tile boundaries + min(D).  The first
-    // class launches as a programmatic dependent: its CTAs load and sort while the
-    // sampler and the round selection still run, and wait for them (griddepcontrol)
-    // before writing keys back (the sampler reads the unsorted level input) and
-    // before reading the pivots.
-    if (!generic) {
-      bool first = true;
-      for (auto& cd : coldesc) {
-        const uint32_t ncol = (uint32_t)colcls[cd.first].size();
-        with_tile<SK>(cd.first, [&](auto nt, auto v) {
-          constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
-          using BS = BlockSort<SK, NT, V>;
-          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
-          static bool init = false;
-          if (!init) { set_smem(k_colsort<K, NT, V, PAIRS>, smem); init = true; }
-          ProfScope ps("colsort", st);
-          auto f = k_colsort<K, NT, V, PAIRS>;
-          if (first && !g_prof.load())
-            launch_pdl(f, ncol, NT, smem, st, cd.second, (const LevelSeg*)dL, kb[X], PAIRS ? vb[X] : nullptr,
-                       (const K*)piv, segmat, segmin);
-          else
-            f<<<ncol, NT, smem, st>>>(cd.second, dL, kb[X], PAIRS ? vb[X] : nullptr, piv, segmat, segmin);
-          check_launch("k_colsort");
-          first = false;
-        });
-      }
-    } else {  // columns longer than a CTA holds: a recursive level sorts them
-      sort_batch(allcols, X, X, depth + 1, "colsort");
-      {
-        ProfScope ps("colmin", st);
-        k_colmin<K><<<ns, 256, 0, st>>>(dL, kb[X], segmin);
-        check_launch("k_colmin");
-      }
-      {
-        ProfScope ps("segmat", st);
-        k_segmat<K><<<(uint32_t)mtasks.size(), 256, 0, st>>>(dL, dM, kb[X], piv, segmat, fix, 0);
-        check_launch("k_segmat");
-      }
-    }
-    // 3. min-exclusion: final round; repair the boundaries if it changed
-    {
-      ProfScope ps("select", st);
-      k_select_round<K><<<ns, 256, 0, st>>>(dL, ns, cand, flags, p0s, segmin, piv, info, fix, 1);
-      check_launch("k_select_round");
-    }
-    {
-      ProfScope ps("segmat", st);
-      k_segmat<K><<<(uint32_t)mtasks.size(), 256, 0, st>>>(dL, dM, kb[X], piv, segmat, fix, 1);
-      check_launch("k_segmat");
-    }
-    ar.release(cand);
-    // 4. tile sizes and offsets, then the SkewTranspose X -> T; the
-    // transpose also accumulates the bucket sizes
-    uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
-    SQ_CUDA(cudaMemsetAsync(bsize, 0, buck_tot * 4, st));
-    {
-      ProfScope ps("tiles", st);
-      k_tile_sizes<<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat);
-      check_launch("k_tile_sizes");
-      k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, kPlanFW, dPieceBase);
-      check_launch("k_tile_scan");
-    }
-    {
-      PieceDesc* pieces = (PieceDesc*)ar.alloc(piece_tot * sizeof(PieceDesc));
-      uint32_t* pcount = (uint32_t*)ar.alloc(16);  // [0] pieces, [1] tile tickets
-      SQ_CUDA(cudaMemsetAsync(pcount, 0, 8, st));
-      unsigned long long* pstatus = (unsigned long long*)ar.alloc(uint64_t(ntiles) * 8);
-      SQ_CUDA(cudaMemsetAsync(pstatus, 0, uint64_t(ntiles) * 8, st));
-      {
-        ProfScope ps("tiles", st);
-        k_piece_plan2<1024, TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout, pstatus);
-        check_launch("k_piece_plan2");
-      }
-      ar.release(pstatus);
-      using XC = WsCfg<K, PAIRS, TC::S, TC::F>;
-      auto f = k_transpose_ws<K, PAIRS, TC::S, TC::F>;
-      static int grid = 0;
-      if (!grid) {
-        set_smem(f, XC::SMEM);
-        grid = wave_grid(f, XC::NT, XC::SMEM);
-      }
-      ProfScope ps("transpose", st);
-      f<<<(uint32_t)std::min<uint64_t>(grid, piece_tot), XC::NT, XC::SMEM, st>>>(
-          pieces, pcount, kb[X], kb[T], PAIRS ? vb[X] : nullptr, PAIRS ? vb[T] : nullptr, piv, segmat, ppre, bsize);
-      check_launch("k_transpose_ws");
-      ar.release(pcount);
-      ar.release(pieces);
-    }
-    // 5. bucket plan: sizes, final offsets, work lists
-    PlanOut po{};
-    po.ncls = 0;
-    int cls_cl[20] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
-    {
-      const uint32_t one = g_big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
-      // smallest bucket-sort class 1K keys: smaller chunks share it (their padding is
-      // skipped), instead of a latency-bound launch per tiny class
-      const uint32_t lower = std::min<uint32_t>(1024u, one);
-      for (uint32_t t : kTiles)
-        if (t >= lower && t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
-      po.max_tile = one;
-      if (g_big_mode == 2) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
-        const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
-        for (int cl : {4, 8, 16}) {
-          if (cl * ct <= po.max_tile) continue;
-          cls_cl[po.ncls] = cl;
-          po.cls_tile[po.ncls++] = cl * ct;
-          po.max_tile = cl * ct;
-        }
-        if (!g_max_tile && 16u * ClusterBig<SK>::TILE > po.max_tile) {
-          cls_cl[po.ncls] = -16;
-          po.cls_tile[po.ncls++] = 16u * ClusterBig<SK>::TILE;
-          po.max_tile = 16u * ClusterBig<SK>::TILE;
-        }
-      }
-    }
-    uint64_t level_keys = 0;
-    for (const Seg& g : segs) level_keys += g.len;
-    po.msort_max = po.max_tile;
-    po.mtile = MergeCfg<K, PAIRS>::NT * MergeCfg<K, PAIRS>::VM;
-    po.mcap = 1;
-    // pair sort: 32-bit keys only, with the default one-CTA cap (not under test hooks)
-    po.pair = 0;  // (a two-CTA cluster pair sort over DSMEM measured slower)
-    po.units = (Unit*)ar.alloc(buck_tot * sizeof(Unit));
-    po.unit_max = 0;
-    for (uint32_t c = 0; c < po.ncls; c++)
-      if (!cls_cl[c]) po.unit_max = std::max(po.unit_max, po.cls_tile[c]);
-    po.nunits = (uint32_t*)ar.alloc(16);
-    SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
-    if (g_big_mode == 1) {  // multi-CTA merge sort for buckets of up to 16 chunks
-      po.msort_max = 16u * (po.pair ? 2u : 1u) * po.max_tile;
-      po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
-      ensure_third();
-    }
-    po.mlist = (MTile*)ar.alloc(uint64_t(kMaxPasses) * po.mcap * sizeof(MTile));
-    po.mcount = (uint32_t*)ar.alloc(kMaxPasses * 4);
-    SQ_CUDA(cudaMemsetAsync(po.mcount, 0, kMaxPasses * 4, st));
-    po.cap_per_list = (uint32_t)(buck_tot + level_keys / std::max<uint32_t>(po.max_tile, 1) + 16);
-    // lists: [0, ncls) classes, ncls copy, ncls+1 oversize, ncls+2 pair, then the
-    // chunks of merge-sorted buckets per class at ncls+3+c (sorted first, so that
-    // the merge passes can overlap the other classes)
-    const uint32_t nlists = 2 * po.ncls + 3;
-    po.list = (uint32_t*)ar.alloc(uint64_t(nlists) * po.cap_per_list * 4);
-    po.count = (uint32_t*)ar.alloc(nlists * 4);
-    SQ_CUDA(cudaMemsetAsync(po.count, 0, nlists * 4, st));
-    {
-      ProfScope ps("plan", st);
-      k_tile_bucket_plan<K><<<(ntiles * 32 + 127) / 128, 128, 0, st>>>(dL, dTiles, ntiles, bsize, piv, recs, po);
-      check_launch("k_tile_bucket_plan");
-    }
-    if (dbg) {
-      k_bucket_gather<K, 256><<<1024, 256, 0, st>>>(recs, dTiles, nullptr, nullptr, (uint32_t)buck_tot, kb[T],
-                                                    (K*)dbg->dst, nullptr, nullptr, pout, ppre);
-      check_launch("k_bucket_gather");
-      std::vector<BucketRec> hr(buck_tot);
-      std::vector<uint32_t> hinfo(ns);
-      SQ_CUDA(cudaMemcpyAsync(hr.data(), recs, buck_tot * sizeof(BucketRec), cudaMemcpyDeviceToHost, st));
-      SQ_CUDA(cudaMemcpyAsync(hinfo.data(), info, ns * 4, cudaMemcpyDeviceToHost, st));
-      SQ_CUDA(cudaMemcpyAsync(dbg->pivots, piv, piv_tot * sizeof(K), cudaMemcpyDeviceToDevice, st));
-      SQ_CUDA(cudaStreamSynchronize(st));
-      std::vector<uint32_t> be(buck_tot), inf = {hinfo[0] & 0x7fffffffu, hinfo[0] >> 31};
-      for (uint64_t i = 0; i < buck_tot; i++) be[i] = hr[i].out + hr[i].size;
-      uint32_t* dbe = ar.upload(be);
-      uint32_t* dinf = ar.upload(inf);
-      SQ_CUDA(cudaMemcpyAsync(dbg->bucend, dbe, buck_tot * 4, cudaMemcpyDeviceToDevice, st));
-      SQ_CUDA(cudaMemcpyAsync(dbg->info, dinf, 8, cudaMemcpyDeviceToDevice, st));
-      return;
-    }
-    // 6. bucket sorts: gather from T, sort on chip, write to X.  The
-    // size classes are independent: their kernels run concurrently on side streams.
-    SideStreams& ss = side_streams();
-    // profiling: concurrent classes overlap, so the role is timed as one span on
-    // the caller's stream (fork to join); serial classes are timed per launch
-    std::optional<ProfScope> span;
-    if (g_concurrent_classes) span.emplace("bucketsort", st);
-    const bool merge = g_big_mode == 1;
-    // allocated on st before the fork, released on st after the join
-    uint32_t* splits = merge ? (uint32_t*)ar.alloc(uint64_t(po.mcap) * 4) : nullptr;
-    cudaEvent_t fork = pool_event();
-    SQ_CUDA(cudaEventRecord(fork, st));
-    for (int i = 0; i < SideStreams::N; i++) SQ_CUDA(cudaStreamWaitEvent(ss.s[i], fork, 0));
-    auto launch_class = [&](int c, uint32_t li, cudaStream_t cs) {
-      const uint32_t* lst = po.list + uint64_t(li) * po.cap_per_list;
-      if (cls_cl[c]) {
-        launch_cluster(cls_cl[c], cs, lst, po.count + li, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
-        return;
-      }
-      with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
-        constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
-        using BS = BlockSort<SK, NT, V>;
-        const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4;
-        auto f = k_bucketsort<K, NT, V, PAIRS>;
-        static int grid = 0;
-        if (!grid) {
-          set_smem(f, smem);
-          grid = wave_grid(f, NT, smem);
-        }
-        std::optional<ProfScope> ps;
-        if (!g_concurrent_classes) ps.emplace("bucketsort", cs);
-        f<<<(uint32_t)std::min<uint64_t>(grid, po.cap_per_list), NT, smem, cs>>>(
-            recs, dTiles, lst, po.count + li, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
-            ppre, kb[2], PAIRS ? vb[2] : nullptr, po.units);
-        check_launch("k_bucketsort");
-      });
-    };
-    auto launch_merges = [&](cudaStream_t ms) {  // merge passes of the multi-CTA base case (X <-> U)
-      using MC = MergeCfg<K, PAIRS>;
-      using BS = BlockSort<K, MC::NT, MC::VM>;
-      const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
-      auto f = k_merge_pass<K, PAIRS, MC::NT, MC::VM>;
-      static int grid = 0;
-      if (!grid) {
-        set_smem(f, smem);
-        grid = wave_grid(f, MC::NT, smem);
-      }
-      for (uint32_t p = 0; p < (uint32_t)kMaxPasses; p++) {
-        ProfScope ps("merge", ms);
-        const MTile* items = po.mlist + uint64_t(p) * po.mcap;
-        k_merge_split<K><<<2 * num_sms(), 256, 0, ms>>>(recs, items, po.mcount + p, p, po.mtile, kb[X], kb[2], splits);
-        check_launch("k_merge_split");
-        f<<<grid, MC::NT, smem, ms>>>(recs, items, po.mcount + p, p, kb[X], kb[2], PAIRS ? vb[X] : nullptr,
-                                      PAIRS ? vb[2] : nullptr, splits);
-        check_launch("k_merge_pass");
-      }
-    };
-
-    if (!g_concurrent_classes) {
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, st);
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, st);
-      if (merge) launch_merges(st);
-    } else {
-      // streams 0-1: the chunks of merge-sorted buckets, then (stream 0) the merge
-      // passes; streams 2-3: whole buckets and units, which the merges overlap
-      int rc = 0, rw = 0;
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, ss.s[rc++ % 2]);
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, ss.s[2 + rw++ % 2]);
-      if (merge) {
-        cudaEvent_t e = pool_event();
-        SQ_CUDA(cudaEventRecord(e, ss.s[1]));
-        SQ_CUDA(cudaStreamWaitEvent(ss.s[0], e, 0));
-        g_event_pool.push_back(e);
-        launch_merges(ss.s[0]);
-      }
-    }
-    for (int i = 0; i < SideStreams::N && g_concurrent_classes; i++) {
-      cudaEvent_t j = pool_event();
-      SQ_CUDA(cudaEventRecord(j, ss.s[i]));
-      SQ_CUDA(cudaStreamWaitEvent(st, j, 0));
-      g_event_pool.push_back(j);
-    }
-    span.reset();
-    g_event_pool.push_back(fork);
-    if (splits) ar.release(splits);
-    {  // single-value buckets (copied) and oversize buckets (made contiguous),
-       // in units of kGatherKeys keys so that huge buckets are copied by many CTAs
-      ProfScope ps("gather", st);
-      const uint64_t ucap = buck_tot + level_keys / kGatherKeys + 16;
-      uint2* units = (uint2*)ar.alloc(ucap * sizeof(uint2));
-      uint32_t* nun = (uint32_t*)ar.alloc(16);
-      for (uint32_t c = po.ncls; c < po.ncls + 2; c++) {
-        const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
-        k_gather_units<<<1, 1024, 0, st>>>(recs, lst, po.count + c, units, nun);
-        check_launch("k_gather_units");
-        k_bucket_gather_units<K, 256><<<4 * num_sms(), 256, 0, st>>>(
-            recs, dTiles, lst, units, nun, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
-            ppre);
-        check_launch("k_bucket_gather_units");
-      }
-      ar.release(nun);
-      ar.release(units);
-    }
-    // 7. one host read per level: the oversize list (and the round, for stats)
-    uint32_t* hcnt = (uint32_t*)ar.pinned((po.ncls + 2) * 4);
-    uint32_t* hinfo = (uint32_t*)ar.pinned(4);
-    xfer(hcnt, po.count, (po.ncls + 2) * 4, st);
-    xfer(hinfo, info, 4, st);
-    SQ_CUDA(cudaStreamSynchronize(st));
-    g_stats.host_syncs++;
-    if (depth == 0) {
-      g_stats.top_round = hinfo[0] & 0x7fffffffu;
-      g_stats.top_degenerate = hinfo[0] >> 31;
-      g_stats.top_m = L[0].k;
-    }
-    const uint32_t nos = hcnt[po.ncls + 1];
-    std::vector<Seg> over;
-    if (nos) {
-      uint32_t* hl = (uint32_t*)ar.pinned(nos * 4);
-      xfer(hl, po.list + uint64_t(po.ncls + 1) * po.cap_per_list, nos * 4, st);
-      BucketRec* hr = (BucketRec*)ar.pinned(buck_tot * sizeof(BucketRec));
-      xfer(hr, recs, buck_tot * sizeof(BucketRec), st);
-      SQ_CUDA(cudaStreamSynchronize(st));
-      g_stats.host_syncs++;
-      for (uint32_t q = 0; q < nos; q++) {
-        const uint32_t e = hl[q];
-        const uint32_t i = item_bucket(e);
-        over.push_back({hr[i].out, hr[i].size, hr[i].node});
-        g_stats.oversize_keys += hr[i].size;
-      }
-    }
-    for (void* p : {(void*)po.units, (void*)po.nunits}) ar.release(p);
-    for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)po.mlist, (void*)piv,
-                    (void*)flags, (void*)p0s, (void*)info, (void*)fix, (void*)segmin})
-      ar.release(p);
-    if (!over.empty()) sort_batch(over, X, X, depth + 1, "bucketsort");
-  }
-};
-
-// ------------------------------------------------------------------ ABI helpers
-static int fail(const Error& e) {
-  g_errmsg = e.what();
-  return e.code;
-}
-
-template <typename Fn>
-static int guarded(Fn&& fn) {
-  g_stats = sq_stats{};
-  try {
-    fn();
-    prof_collect();
-    return SQ_OK;
-  } catch (const Error& e) {
-    return fail(e);
-  } catch (const std::exception& e) {
-    g_errmsg = e.what();
-    return SQ_ERR_CUDA;
-  }
-}
-
-static void need(bool cond, const char* msg) {
-  if (!cond) throw Error(SQ_ERR_INVALID_ARGUMENT, msg);
-}
-
-static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
-  const char* x = (const char*)a;
-  const char* y = (const char*)b;
-  return x < y + nb && y < x + na;
-}
-
-template <typename K, bool PAIRS>
-static void sort_device(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
-  Arena ar(st);
-  Engine<K, PAIRS> eng(st, ar, keys, vals, n);
-  std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
-  eng.sort_batch(top, 0, 0, 0, "smallsort");
-  SQ_CUDA(cudaGetLastError());
-}
-
-template <typename K, bool PAIRS>
-static int sort_entry(K* keys, uint32_t* vals, size_t n, uint64_t seed, void* stream, bool host) {
-  return guarded([&] {
-    if (n <= 1) return;
-    need(keys != nullptr, "keys is NULL");
-    if (PAIRS) {
-      need(vals != nullptr, "vals is NULL");
-      need(!overlap(keys, n * sizeof(K), vals, n * 4), "keys and vals overlap");
-    }
-    need(n <= (sizeof(K) == 4 ? (size_t(1) << 30) : (size_t(1) << 28)), "n exceeds the supported maximum");
-    check_device();
-    cudaStream_t st = (cudaStream_t)stream;
-    if (!host) {
-      sort_device<K, PAIRS>(keys, vals, n, seed, st);
-      SQ_CUDA(cudaStreamSynchronize(st));
-      return;
-    }
-    Arena ar(st);
-    K* dk = (K*)ar.alloc(n * sizeof(K));
-    uint32_t* dv = PAIRS ? (uint32_t*)ar.alloc(n * 4) : nullptr;
-    SQ_CUDA(cudaMemcpyAsync(dk, keys, n * sizeof(K), cudaMemcpyHostToDevice, st));
-    if (PAIRS) SQ_CUDA(cudaMemcpyAsync(dv, vals, n * 4, cudaMemcpyHostToDevice, st));
-    sort_device<K, PAIRS>(dk, dv, n, seed, st);
-    SQ_CUDA(cudaMemcpyAsync(keys, dk, n * sizeof(K), cudaMemcpyDeviceToHost, st));
-    if (PAIRS) SQ_CUDA(cudaMemcpyAsync(vals, dv, n * 4, cudaMemcpyDeviceToHost, st));
-    SQ_CUDA(cudaStreamSynchronize(st));
-  });
-}
-
-// Signed and floating-point keys: an order-preserving bijection
-// onto unsigned keys of the same width, applied in place before the unsigned sort
-// and inverted after it (reading L25).  Signed: flip the sign bit.
-// IEEE-754 binary32/64: flip every bit of a negative value, only the sign bit of a
-// non-negative one -- the totalOrder of IEEE 754-2008 5.10 (-NaN < -inf < ... < -0
-// < +0 < ... < +inf < +NaN).
-template <typename U>
-__global__ void k_key_map(U* __restrict__ k, size_t n, int kind, bool inverse) {
-  constexpr U SIGN = U(1) << (sizeof(U) * 8 - 1);
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-    const U x = k[i];
-    U y;
-    if (kind == 0) y = x ^ SIGN;                                    // two's complement
-    else if (!inverse) y = (x & SIGN) ? U(~x) : U(x | SIGN);         // float -> ordered
-    else y = (x & SIGN) ? U(x ^ SIGN) : U(~x);                      // ordered -> float
-    k[i] = y;
-  }
-}
-
-template <typename U>
-static int mapped_entry(U* keys, size_t n, uint64_t seed, void* stream, int kind) {
-  return guarded([&] {
-    if (n <= 1) return;
-    need(keys != nullptr, "keys is NULL");
-    need(n <= (sizeof(U) == 4 ? (size_t(1) << 30) : (size_t(1) << 28)), "n exceeds the supported maximum");
-    check_device();
-    cudaStream_t st = (cudaStream_t)stream;
-    const uint32_t g = (uint32_t)std::min<size_t>((n + 1023) / 1024, size_t(num_sms()) * 8);
-    k_key_map<U><<<g, 256, 0, st>>>(keys, n, kind, false);
-    check_launch("k_key_map");
-    sort_device<U, false>(keys, nullptr, n, seed, st);
-    k_key_map<U><<<g, 256, 0, st>>>(keys, n, kind, true);
-    check_launch("k_key_map");
-    SQ_CUDA(cudaStreamSynchronize(st));
-  });
-}
-
-// Pipelined batch of host sorts (sq_sort_*_host_batch): item i's sort on `st`
-// overlaps the H2D copy of item i+1 and the D2H copy of item i-1, each on a
-// library-owned non-blocking copy stream.  Three device buffers rotate, so a
-// buffer's copy-in -> sort -> copy-out cycle (~2 copies + 1 sort) spans three
-// items and the steady state is bound by the copies alone.
-template <typename K>
-static int batch_entry(const K* const* in, K* const* out, size_t n, size_t count, uint64_t seed, void* stream) {
-  struct Res {
-    cudaStream_t st = nullptr, cs[2] = {nullptr, nullptr};
-    cudaEvent_t ev[10] = {};
-    K* buf[3] = {nullptr, nullptr, nullptr};
-    ~Res() {
-      for (auto s : cs)
-        if (s) cudaStreamSynchronize(s);
-      cudaStreamSynchronize(st);
-      for (auto b : buf)  // back to the pool (kept, release threshold = max)
-        if (b) cudaFreeAsync(b, st);
-      cudaStreamSynchronize(st);
-      for (auto e : ev)
-        if (e) cudaEventDestroy(e);
-      for (auto s : cs)
-        if (s) cudaStreamDestroy(s);
-    }
-  };
-  return guarded([&] {
-    if (count == 0) return;
-    need(in != nullptr && out != nullptr, "in/out is NULL");
-    need(n <= (sizeof(K) == 4 ? (size_t(1) << 30) : (size_t(1) << 28)), "n exceeds the supported maximum");
-    const size_t bytes = n * sizeof(K);
-    for (size_t i = 0; i < count; ++i) {
-      need(in[i] != nullptr && out[i] != nullptr, "in[i]/out[i] is NULL");
-      for (size_t j = i + 1; j < count && count <= 4096; ++j)
-        need(!overlap(out[i], bytes, in[j], bytes), "out[i] overlaps in[j] with j > i");
-    }
-    if (n <= 1) {
-      for (size_t i = 0; i < count; ++i)
-        if (n == 1 && out[i] != in[i]) out[i][0] = in[i][0];
-      return;
-    }
-    check_device();
-    cudaStream_t st = (cudaStream_t)stream;
-    Res r;
-    r.st = st;
-    for (auto& s : r.cs) SQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    for (auto& e : r.ev) SQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (int b = 0; b < int(std::min<size_t>(count, 3)); b++) SQ_CUDA(cudaMallocAsync((void**)&r.buf[b], bytes, st));
-    cudaStream_t h2d = r.cs[0], d2h = r.cs[1];
-    SQ_CUDA(cudaEventRecord(r.ev[9], st));  // the buffers exist
-    SQ_CUDA(cudaStreamWaitEvent(h2d, r.ev[9], 0));
-    cudaEvent_t* in_done = r.ev;        // [3]: buffer b holds item i's input
-    cudaEvent_t* sorted = r.ev + 3;     // [3]: item in buffer b is sorted
-    cudaEvent_t* out_done = r.ev + 6;   // [3]: buffer b has been copied out
-    auto copy_in = [&](size_t i) {
-      const int b = int(i % 3);
-      if (i >= 3) SQ_CUDA(cudaStreamWaitEvent(h2d, out_done[b], 0));
-      SQ_CUDA(cudaMemcpyAsync(r.buf[b], in[i], bytes, cudaMemcpyHostToDevice, h2d));
-      SQ_CUDA(cudaEventRecord(in_done[b], h2d));
-    };
-    copy_in(0);
-    for (size_t i = 0; i < count; ++i) {
-      const int b = int(i % 3);
-      if (i + 1 < count) copy_in(i + 1);  // enqueued before the sort's host waits
-      SQ_CUDA(cudaStreamWaitEvent(st, in_done[b], 0));
-      sort_device<K, false>(r.buf[b], nullptr, n, seed, st);
-      SQ_CUDA(cudaEventRecord(sorted[b], st));
-      SQ_CUDA(cudaStreamWaitEvent(d2h, sorted[b], 0));
-      SQ_CUDA(cudaMemcpyAsync(out[i], r.buf[b], bytes, cudaMemcpyDeviceToHost, d2h));
-      SQ_CUDA(cudaEventRecord(out_done[b], d2h));
-    }
-    SQ_CUDA(cudaStreamSynchronize(d2h));
-    SQ_CUDA(cudaStreamSynchronize(h2d));
-    SQ_CUDA(cudaStreamSynchronize(st));
-  });
-}
-
+SQ_ENGINE_INSTANCES(extern)
 }  // namespace sq
+
 
 using namespace sq;
 
@@ -1298,6 +168,13 @@ const char* sq_status_string(int s) {
 
 const char* sq_last_error_message(void) { return g_errmsg.c_str(); }
 
+int sq_trim_memory(void) {
+  return guarded([&] {
+    check_device();
+    SQ_CUDA(cudaMemPoolTrimTo(lib_pool(), 0));
+  });
+}
+
 void sq_get_stats(sq_stats* out) {
   if (out) *out = g_stats;
 }
@@ -1349,15 +226,7 @@ int sq_debug_level_u32(const uint32_t* src, uint32_t* dst, size_t n, uint64_t se
     need(src && dst && pivots_out && bucend_out && info_out, "NULL pointer");
     need(!overlap(src, n * 4, dst, n * 4), "src and dst overlap");
     check_device();
-    cudaStream_t st = (cudaStream_t)stream;
-    Arena ar(st);
-    uint32_t* work = (uint32_t*)ar.alloc(n * 4);
-    SQ_CUDA(cudaMemcpyAsync(work, src, n * 4, cudaMemcpyDeviceToDevice, st));
-    Engine<uint32_t, false> eng(st, ar, work, nullptr, n);
-    DebugOut dbg{dst, pivots_out, bucend_out, info_out};
-    std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
-    eng.run_level(top, 0, 0, &dbg);
-    SQ_CUDA(cudaStreamSynchronize(st));
+    debug_level_u32(src, dst, n, seed, pivots_out, bucend_out, info_out, (cudaStream_t)stream);
   });
 }
 

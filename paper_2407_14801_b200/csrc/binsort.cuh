@@ -1,0 +1,204 @@
+// binsort.cuh -- the B200 base case for 32-bit keys: one CTA sorts a tile held
+// in shared memory by a counting sort on a monotone bin of the key, then fixes
+// the order inside the (short) bins with two sorting-network passes.
+//
+// The paper's base case is any direct sort of a small array ("simple_sort",
+// P:259-261; std::sort below 1000 items in the experiments).  On B200 the
+// comparison merge sort of blocksort.cuh costs ~180 instructions per key and is
+// bound by the integer ALU pipe; shared-memory atomics, random stores and random
+// loads all issue at ~1.4 clk per warp instruction per SM (tools/ubench/ubench2,
+// profiles/r02_ubench2.txt), so a counting sort is cheaper:
+//   1. min and max of the tile; bin(x) = floor((x - min) * f / 2^32) with
+//      f = floor(NB * 2^32 / (max - min + 1)) spreads [min, max] over NB = TILE/2
+//      bins (two keys per bin on average; one multiply-high on the FMA pipe).
+//      bin is monotone: bin(x) < bin(y) implies x < y.  When max - min < NB the
+//      bin is x - min itself (exact).
+//   2. histogram of the bins (shared-memory atomics), exclusive scan -> the start
+//      of every bin, and the largest bin.
+//   3. scatter: each key takes the next slot of its bin (atomic increment).  The
+//      tile is now ordered by bin; only keys of one bin can be out of order.
+//   4. if the bins are exact (single values): done.  Otherwise, when no bin holds
+//      more than V/2 keys, pass 1 sorts every thread's block of V consecutive keys
+//      in registers (Batcher's network), and pass 2 merges the upper half of block
+//      t with the lower half of block t+1: a bin of at most V/2 keys lies inside
+//      one block, where pass 1 sorts it, or straddles one block boundary and lies
+//      inside the window pass 2 merges.  A larger bin (skewed input) falls back to
+//      the merge sort of blocksort.cuh on the bin-ordered tile.
+// The result is the sorted tile; keys are unique values, so the unstable scatter
+// does not matter (pairs keep the stable merge sort).
+#pragma once
+#include "blocksort.cuh"
+
+namespace sq {
+
+template <int NT_, int V_>
+struct BinSort {
+  static constexpr int NT = NT_;
+  static constexpr int V = V_;
+  static constexpr int NW = NT / 32;
+  static constexpr int TILE = NT * V;
+  static_assert(V == 16 || V == 32, "fix-up networks for 16 or 32 keys per thread");
+  static_assert(NT % 32 == 0, "whole warps");
+  // V = 32: TILE/2 bins (mean 2 keys); V = 16 handles bins of <= 8 keys: 2*TILE bins
+  static constexpr int E = V == 32 ? 16 : 32;  // counters per thread in the scan
+  static constexpr int NB = NT * E;
+  static constexpr int RUNMAX = V / 2;
+  // shared memory for the counters and the block reductions (bytes), besides the tile
+  static constexpr size_t CNT_WORDS = NB + 2 * 32 + 4;
+  static constexpr size_t CNT_BYTES = CNT_WORDS * 4;
+
+  __device__ __forceinline__ static uint32_t pad(uint32_t i) { return pad32(i); }
+
+  template <bool SCATTER>
+  __device__ __forceinline__ static void bin_op(uint32_t* s, uint32_t* cnt, uint32_t x, uint32_t b) {
+    if constexpr (SCATTER) {
+      const uint32_t d = atomicAdd(&cnt[b], 1u);
+      s[pad(d)] = x;
+    } else {
+      atomicAdd(&cnt[b], 1u);
+    }
+  }
+  // Histogram (SCATTER = false) or scatter (true) of the thread's keys; the branch on
+  // `exact` and `full` is uniform across the CTA.
+  template <bool SCATTER>
+  __device__ __forceinline__ static void hist_or_scatter(uint32_t* s, uint32_t* cnt, const uint32_t (&r)[V],
+                                                         uint32_t mn, uint32_t f, bool exact, bool full,
+                                                         uint32_t b0, uint32_t len) {
+    if (full) {
+      if (exact) {
+#pragma unroll
+        for (int j = 0; j < V; j++) bin_op<SCATTER>(s, cnt, r[j], r[j] - mn);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; j++) bin_op<SCATTER>(s, cnt, r[j], __umulhi(r[j] - mn, f));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; j++)
+        if (b0 + j < len) bin_op<SCATTER>(s, cnt, r[j], exact ? r[j] - mn : __umulhi(r[j] - mn, f));
+    }
+  }
+
+  // Sort the TILE keys at s[pad(0..TILE-1)]; positions >= len hold 0xFFFFFFFF
+  // padding (left in place).  cnt: CNT_WORDS words of shared memory.  On return
+  // the sorted tile is in s and a __syncthreads() has been executed.
+  __device__ static void sort_smem(uint32_t* s, uint32_t* cnt, uint32_t len = TILE) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint32_t* red = cnt + NB;  // [0, 32): warp minima, [32, 64): warp maxima, [64, 68): misc
+    const uint32_t b0 = uint32_t(t) * V;
+    const bool full = b0 + V <= len;
+    uint32_t r[V];
+#pragma unroll
+    for (int j = 0; j < V; j++) r[j] = s[pad(b0 + j)];
+    // ---- 1. min and max of the real keys; counters cleared
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < V; j++) {
+        mn = min(mn, r[j]);
+        mx = max(mx, r[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; j++)
+        if (b0 + j < len) {
+          mn = min(mn, r[j]);
+          mx = max(mx, r[j]);
+        }
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+      red[w] = mn;
+      red[32 + w] = mx;
+    }
+#pragma unroll
+    for (int q = 0; q < E; q++) cnt[q * NT + t] = 0u;
+    __syncthreads();
+    mn = red[0];
+    mx = red[32];
+#pragma unroll
+    for (int q = 1; q < NW; q++) {
+      mn = min(mn, red[q]);
+      mx = max(mx, red[32 + q]);
+    }
+    const uint32_t range = mx - mn;
+    const bool exact = range < uint32_t(NB);
+    // f = floor(NB * 2^32 / (range + 1)) < 2^32 when range >= NB
+    const uint32_t f = exact ? 0u : (uint32_t)((uint64_t(NB) << 32) / (uint64_t(range) + 1));
+    // ---- 2. histogram of the bins
+    hist_or_scatter<false>(s, cnt, r, mn, f, exact, full, b0, len);
+    __syncthreads();
+    // ---- exclusive scan of the NB counters (thread t owns [t*E, t*E+E)) and the largest bin
+    uint32_t c[E], sum = 0, big = 0;
+#pragma unroll
+    for (int q = 0; q < E; q++) {
+      c[q] = cnt[t * E + q];
+      big = max(big, c[q]);
+      const uint32_t x = c[q];
+      c[q] = sum;
+      sum += x;
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    big = __reduce_max_sync(0xffffffffu, big);
+    if (lane == 31) red[w] = incl;
+    if (lane == 0) red[32 + w] = big;
+    __syncthreads();
+    uint32_t wbase = 0;
+#pragma unroll
+    for (int q = 0; q < NW; q++) wbase += q < w ? red[q] : 0u;
+    uint32_t gbig = 0;
+#pragma unroll
+    for (int q = 0; q < NW; q++) gbig = max(gbig, red[32 + q]);
+    const uint32_t tbase = wbase + incl - sum;
+#pragma unroll
+    for (int q = 0; q < E; q++) cnt[t * E + q] = tbase + c[q];
+    __syncthreads();
+    // ---- 3. scatter: each key to the next free slot of its bin
+    hist_or_scatter<true>(s, cnt, r, mn, f, exact, full, b0, len);
+    __syncthreads();
+    if (exact) return;  // every bin is one value
+    if (gbig > RUNMAX) {  // a bin too long for the fix-up (skewed input): merge sort
+      BlockSort<uint32_t, NT, V>::sort_smem(s, len);
+      return;
+    }
+    // ---- 4a. fix-up pass 1: every thread sorts its block of V consecutive keys
+    const bool live = (uint32_t(t) & ~31u) * V < len;  // warp-uniform: padding-only warps skip
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < V; j++) r[j] = s[pad(b0 + j)];
+      thread_sort<uint32_t, V>(r);
+#pragma unroll
+      for (int j = 0; j < V; j++) s[pad(b0 + j)] = r[j];
+    }
+    __syncthreads();
+    // ---- 4b. fix-up pass 2: merge [b0 + V/2, b0 + V) with [b0 + V, b0 + 3V/2)
+    constexpr int H = V / 2;
+    if (t < NT - 1 && b0 + H < len) {
+#pragma unroll
+      for (int j = 0; j < H; j++) {
+        r[j] = s[pad(b0 + H + j)];
+        r[H + j] = s[pad(b0 + V + H - 1 - j)];  // descending: a bitonic sequence
+      }
+      const uint32_t one = (uint32_t)c_one, mone = (uint32_t)c_mone;
+#pragma unroll
+      for (int d = H; d >= 1; d >>= 1)
+#pragma unroll
+        for (int i = 0; i < V; i++)
+          if ((i & d) == 0) {
+            if (i & 1) cas_fma(r[i], r[i + d], one, mone);
+            else cas(r[i], r[i + d]);
+          }
+#pragma unroll
+      for (int j = 0; j < V; j++) s[pad(b0 + H + j)] = r[j];
+    }
+    __syncthreads();
+  }
+};
+
+}  // namespace sq

@@ -58,7 +58,7 @@ struct OddEvenNet {
 // is nearly idle; alternating the two forms balances the pipes.
 // The multiplier is read from constant memory so that ptxas cannot fold the
 // multiply-adds into ALU adds.
-__constant__ int32_t c_one = 1, c_mone = -1, c_mtwo = -2;
+static __constant__ int32_t c_one = 1, c_mone = -1, c_mtwo = -2;
 __device__ __forceinline__ void cas_fma(uint32_t& a, uint32_t& b, uint32_t one, uint32_t mone) {
   const uint32_t lo = min(a, b);
   uint32_t sum, hi;
@@ -255,7 +255,7 @@ struct BlockSort {
       const uint32_t tv = t * V;
       const uint32_t a0 = tv & ~(2 * w - 1);
       const uint32_t b0 = min(a0 + w, (uint32_t)TILE), bend = min(a0 + 2 * w, (uint32_t)TILE);
-      const uint32_t la = b0 - a0, lb = bend - b0;
+      const uint32_t la = b0 - a0;
       {
         // this thread's V keys belong to run tv / w; odd runs are stored reversed: the
         // thread's block [tv, tv+V) of run [r0, r0+rlen) lands, reversed, on the block
@@ -304,7 +304,7 @@ template <typename K, int NT, int V>
 __global__ void __launch_bounds__(NT)
 k_blocksort(const SegDesc* __restrict__ segs, const K* __restrict__ src, K* __restrict__ dst) {
   using BS = BlockSort<K, NT, V>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
   const SegDesc d = segs[blockIdx.x];
   const K* in = src + d.off;
@@ -322,7 +322,7 @@ k_blocksort_pairs(const SegDesc* __restrict__ segs, const uint32_t* __restrict__
                   const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ kdst,
                   uint32_t* __restrict__ vdst) {
   using BS = BlockSort<uint64_t, NT, V>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* s = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
   const SegDesc d = segs[blockIdx.x];

@@ -60,70 +60,6 @@ __global__ void k_colmin(const LevelSeg* __restrict__ segs, const K* __restrict_
 }
 
 // ------------------------------------------------------------------------------
-// Pivot sampling.  Round r draws positions
-// t_i = floor(draw(node, r, i) * len / 2^64), i = 0..m-2, from the level array
-// after its columns are sorted (the paper's D), sorts the candidates on
-// chip, and accepts iff they are strictly increasing (L7) and the
-// smallest exceeds min(D).  CTA (seg, slot j) evaluates rounds
-// j, j+R, j+2R, ... and stops at its first accepted round, so the first
-// accepted round overall is found by k_select.  Round cap-1's sample is kept
-// for the degenerate mode.
-template <typename K, int NT, int V>
-__global__ void __launch_bounds__(NT)
-k_sample(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tasks, const K* __restrict__ data,
-         const K* __restrict__ segmin, K* __restrict__ cand, uint8_t* __restrict__ flags, uint32_t R) {
-  using BS = BlockSort<K, NT, V>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* s = reinterpret_cast<K*>(smem_raw);
-  const TaskDesc tk = tasks[blockIdx.x];
-  const LevelSeg sg = segs[tk.seg];
-  const uint32_t np = sg.k - 1;
-  const K mn = segmin[tk.seg];
-  const K* lvl = data + sg.off;
-  for (uint32_t r = tk.a; r < kCap; r += R) {
-    for (int i = threadIdx.x; i < BS::TILE; i += NT) {
-      K x = KeyTraits<K>::kMax;
-      if (i < (int)np) x = lvl[draw_index(draw(sg.node, r, (uint32_t)i), sg.len)];
-      s[BS::pad(i)] = x;
-    }
-    __syncthreads();
-    BS::sort_smem(s);
-    int viol = 0;
-    for (int i = threadIdx.x + 1; i < (int)np; i += NT)
-      if (!(s[BS::pad(i - 1)] < s[BS::pad(i)])) viol = 1;
-    const bool ok = !__syncthreads_or(viol) && (np == 0 || s[BS::pad(0)] > mn);
-    if (ok || r == kCap - 1) {
-      K* out = cand + sg.cand_base + uint64_t(ok ? tk.a : R) * np;
-      for (int i = threadIdx.x; i < (int)np; i += NT) out[i] = s[BS::pad(i)];
-    }
-    if (threadIdx.x == 0) flags[uint64_t(tk.seg) * kCap + r] = ok ? 1 : 2;
-    if (ok) break;
-    __syncthreads();
-  }
-}
-
-// First accepted round per segment -> pivots arena; info = round | (degenerate << 31).
-template <typename K>
-__global__ void k_select(const LevelSeg* __restrict__ segs, const K* __restrict__ cand,
-                         const uint8_t* __restrict__ flags, K* __restrict__ piv,
-                         uint32_t* __restrict__ info, uint32_t R) {
-  const LevelSeg sg = segs[blockIdx.x];
-  __shared__ uint32_t sel;
-  if (threadIdx.x == 0) {
-    uint32_t r = kCap;
-    for (uint32_t q = 0; q < kCap; q++)
-      if (flags[uint64_t(blockIdx.x) * kCap + q] == 1) { r = q; break; }
-    sel = r;
-    info[blockIdx.x] = r < kCap ? r : ((kCap - 1) | 0x80000000u);
-  }
-  __syncthreads();
-  const uint32_t np = sg.k - 1;
-  const uint32_t slot = sel < kCap ? sel % R : R;
-  const K* in = cand + sg.cand_base + uint64_t(slot) * np;
-  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) piv[sg.piv_base + i] = in[i];
-}
-
-// ------------------------------------------------------------------------------
 // Bucket count: for each sorted column, a simultaneous scan
 // of the column and the pivots gives the position of every bucket boundary;
 // bucket sizes accumulate per CTA in shared memory (flushed with one atomic
@@ -135,7 +71,7 @@ template <typename K, int NT, int STAGE, int KSMEM>
 __global__ void __launch_bounds__(NT)
 k_count(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tasks, const K* __restrict__ data,
         const K* __restrict__ piv, uint32_t* __restrict__ segmat, uint32_t* __restrict__ gcnt) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K* col = reinterpret_cast<K*>(smem_raw);                                   // STAGE keys
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw + STAGE * sizeof(K));  // KSMEM counters
   const TaskDesc tk = tasks[blockIdx.x];
@@ -287,7 +223,7 @@ k_transpose(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tile
   static_assert(G <= 256, "fragment index is a byte");
   static_assert(S % NT == 0 && NT % 32 == 0 && NT >= G, "shape");
   static_assert(S <= 65535, "u16 table");
-  extern __shared__ __align__(16) unsigned char sm[];
+  extern __shared__ __align__(128) unsigned char sm[];
   K* stage = reinterpret_cast<K*>(sm + C::off_stage);
   K* outb = reinterpret_cast<K*>(sm + C::off_out);
   uint32_t* vstage = reinterpret_cast<uint32_t*>(sm + C::off_vstage);
@@ -473,7 +409,7 @@ __global__ void k_copy_ranges(const SegDesc* __restrict__ r, const K* __restrict
 
 // Precondition check for the standalone SkewTranspose (SQ_FLAG_VALIDATE):
 // columns sorted and pivots non-decreasing.
-__global__ void k_validate(const uint32_t* __restrict__ src, uint64_t rows, uint64_t n,
+static __global__ void k_validate(const uint32_t* __restrict__ src, uint64_t rows, uint64_t n,
                            const uint32_t* __restrict__ piv, uint32_t np, uint32_t* __restrict__ bad) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride)

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(NT)
 k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* __restrict__ cand,
              uint8_t* __restrict__ flags, K* __restrict__ p0s) {
   using BS = BlockSort<K, NT, V>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the selection may launch now
   const uint32_t seg = blockIdx.x / kCap, r = blockIdx.x % kCap;
@@ -160,7 +160,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
           K* __restrict__ segmin) {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   using BS = BlockSort<SK, NT, V, 32>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   SK* s = reinterpret_cast<SK*>(smem_raw);
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
   const ColDesc d = cols[blockIdx.x];
@@ -275,7 +275,7 @@ __global__ void k_segmat(const LevelSeg* __restrict__ segs, const TaskDesc* __re
 }
 
 // Keys per bucket tile (sum of the tile's run in every column).  CTA per tile.
-__global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
+static __global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
                              const uint32_t* __restrict__ segmat) {
   TileInfo ti = tiles[blockIdx.x];
   const LevelSeg sg = segs[ti.seg];
@@ -308,7 +308,7 @@ __host__ __device__ __forceinline__ uint32_t plan_fw(uint32_t size, uint32_t nco
   return (uint32_t)max((uint64_t)min(32u, FWMAX), min((uint64_t)FWMAX, fw));
 }
 
-__global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
+static __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
                             TileInfo* __restrict__ tiles, uint32_t S, uint32_t G,
                             const uint32_t* __restrict__ piece_seg_base) {
   const LevelSeg sg = segs[blockIdx.x];
@@ -367,10 +367,6 @@ __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* _
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_addr(bar)) : "memory");
 }
@@ -383,14 +379,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-// global -> shared bulk copy, completion counted on `bar` (16-byte aligned, size % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_addr(sdst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
 // shared -> global bulk copy (bulk-group completion)
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_addr(ssrc)),
@@ -632,9 +620,6 @@ struct PlanOut {
   MTile* mlist;           // [kMaxPasses][mcap]
   uint32_t* mcount;       // [kMaxPasses]
   uint32_t mcap;
-  // pair mode (a two-CTA cluster sort, removed): 0; else buckets and chunks of max_tile < len <=
-  // 2*max_tile keys go to list ncls + 2, and merge-sort chunks are 2*max_tile keys
-  uint32_t pair;
   // units: consecutive buckets of one tile, each of at most max_tile keys, packed
   // into work items of at most max_tile keys (their keys are value-ordered ranges,
   // so sorting the concatenation sorts every bucket); items are kUnitFlag | index
@@ -677,7 +662,7 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
     rc.passes = 0;
     const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
     uint32_t q = 1;  // chunks
-    const uint32_t chunk_len = po.pair ? 2 * po.max_tile : po.max_tile;
+    const uint32_t chunk_len = po.max_tile;
     if (size && !single && size > po.max_tile && size <= po.msort_max) {
       q = (size + chunk_len - 1) / chunk_len;
       rc.chunk = chunk_len;  // full chunks; the last one takes the remainder
@@ -708,11 +693,8 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
         for (uint32_t k = 0; k < q; k++) {
           const uint32_t len = min(rc.chunk, size - k * rc.chunk);
           uint32_t cls = 0;
-          if (po.pair && len > po.max_tile) cls = po.ncls + 2;
-          else {
-            while (po.cls_tile[cls] < len) cls++;
-            cls += lbase;
-          }
+          while (po.cls_tile[cls] < len) cls++;
+          cls += lbase;
           const uint32_t slot = atomicAdd(&po.count[cls], 1u);
           po.list[uint64_t(cls) * po.cap_per_list + slot] = gi * 16 + k;
         }
@@ -802,7 +784,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
              const Unit* __restrict__ units) {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   using BS = BlockSort<SK, NT, V>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   SK* s = reinterpret_cast<SK*>(smem_raw);
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
   uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES + (PAIRS ? BS::TILE * 4 : 0));
@@ -888,28 +870,6 @@ struct GSeq {  // sorted run in global memory
   __device__ __forceinline__ K at(uint32_t i) const { return p[i]; }
 };
 
-template <typename SEQ, typename K>
-__device__ __forceinline__ uint32_t warp_split(const SEQ& A, const SEQ& B, uint32_t d) {
-  const int lane = threadIdx.x & 31;
-  uint32_t lo = d > B.len ? d - B.len : 0, hi = min(d, A.len);
-  while (hi > lo) {
-    const uint32_t step = (hi - lo + 31) / 32;
-    const uint32_t p = lo + lane * step;
-    bool gt = true;
-    if (p < hi) gt = A.template at<1>(p) > B.template at<1>(d - 1 - p);
-    const uint32_t m = __ballot_sync(0xffffffffu, gt);
-    const uint32_t first = m ? (uint32_t)(__ffs(m) - 1) : 32u;
-    if (first == 0) {
-      hi = lo;
-    } else {
-      const uint32_t lo_old = lo;
-      lo = lo_old + (first - 1) * step + 1;
-      hi = (uint32_t)min((uint64_t)hi, (uint64_t)lo_old + (uint64_t)first * step);
-    }
-  }
-  return lo;
-}
-
 // Merge-path split of every merge item of a pass, one thread per item (a binary
 // search in global memory; all items in flight at once instead of one latency-bound
 // search per CTA inside the merge kernel).  splits[it] = A keys before output tile it.
@@ -947,7 +907,7 @@ k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   constexpr int TM = NT * VM;
   using BS = BlockSort<K, NT, VM>;  // padding helper only
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K* sk = reinterpret_cast<K*>(smem_raw);                        // TM (+pad) keys: A part then B part
   uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);  // TM vals (pairs)
   __shared__ uint32_t split[2];
@@ -1115,7 +1075,7 @@ k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__
 // units[u] = (list position, part).
 constexpr uint32_t kGatherKeys = 65536;
 
-__global__ void __launch_bounds__(1024)
+static __global__ void __launch_bounds__(1024)
 k_gather_units(const BucketRec* __restrict__ recs, const uint32_t* __restrict__ list,
                const uint32_t* __restrict__ count, uint2* __restrict__ units, uint32_t* __restrict__ nunits) {
   __shared__ uint32_t misc[64];
@@ -1225,7 +1185,7 @@ k_clustersort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ t
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
   using BS = BlockSort<SK, NT, V>;
   constexpr int PER = BS::PER;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   SK* bufA = reinterpret_cast<SK*>(smem_raw);                     // my part of the current sequence
   SK* bufB = reinterpret_cast<SK*>(smem_raw + BS::SMEM_BYTES);   // staged merge inputs
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + 2 * BS::SMEM_BYTES);
