@@ -196,6 +196,14 @@ int sq_set_max_tile(uint32_t max_tile);
  * memory.  Process-wide; SQ_ERR_INVALID_ARGUMENT for other values. */
 int sq_set_big_bucket_mode(int mode);
 
+/* Tuning/test knob: the on-chip base case of keys-only 32-bit sorts (the GPU's
+ * simple_sort).  1 (default): counting sort on a monotone bin of the
+ * key followed by a sorting-network fix-up inside the bins;
+ * 0: merge sort (Batcher network, warp bitonic merges, merge-path passes).
+ * Both give the same (unique) result.  Process-wide; SQ_ERR_INVALID_ARGUMENT
+ * for other values. */
+int sq_set_base_case(int which);
+
 /* Per-kernel device timing: when enabled, every kernel the library launches is
  * bracketed by CUDA events on its stream and the elapsed times accumulate per
  * kernel role (colsort, bucketsort, smallsort, sample, count, transpose, ...).

@@ -25,7 +25,7 @@ EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_h
            "sq_sort_u64_host_batch", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode",
-           "sq_trim_memory"]
+           "sq_trim_memory", "sq_set_base_case"]
 
 
 class SqError(RuntimeError):
@@ -87,6 +87,8 @@ def lib():
         L.sq_profile_read.restype = ctypes.c_int
         L.sq_debug_level_u32.argtypes = [vp, vp, sz, u64, vp, vp, vp, vp]
         L.sq_debug_level_u32.restype = ctypes.c_int
+        L.sq_set_base_case.argtypes = [ctypes.c_int]
+        L.sq_set_base_case.restype = ctypes.c_int
         L.sq_trim_memory.argtypes = []
         L.sq_trim_memory.restype = ctypes.c_int
         _lib = L
@@ -276,6 +278,14 @@ BIG_LEVEL, BIG_MERGE, BIG_CLUSTER = 0, 1, 2
 def set_big_bucket_mode(mode: int):
     """0: recurse into a SquareSort level, 1: multi-CTA merge sort (default), 2: clusters."""
     _check(lib().sq_set_big_bucket_mode(mode))
+
+
+BASE_MERGE, BASE_BIN = 0, 1
+
+
+def set_base_case(which: int):
+    """On-chip base case of keys-only u32 sorts: 1 counting sort + fix-up (default), 0 merge sort."""
+    _check(lib().sq_set_base_case(which))
 
 
 def trim_memory():

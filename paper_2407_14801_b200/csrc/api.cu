@@ -209,6 +209,12 @@ int sq_set_big_bucket_mode(int mode) {
   return SQ_OK;
 }
 
+int sq_set_base_case(int which) {
+  if (which < 0 || which > 1) return SQ_ERR_INVALID_ARGUMENT;
+  g_base_case = which;
+  return SQ_OK;
+}
+
 int sq_set_max_tile(uint32_t t) {
   if (t == 0) {
     g_max_tile = 0;

@@ -44,8 +44,12 @@ struct BinSort {
   static constexpr int NB = NT * E;
   static constexpr int RUNMAX = V / 2;
   // shared memory for the counters and the block reductions (bytes), besides the tile
+  // (+16 bytes: the counters are aligned up to 16 bytes for vector access)
   static constexpr size_t CNT_WORDS = NB + 2 * 32 + 4;
-  static constexpr size_t CNT_BYTES = CNT_WORDS * 4;
+  static constexpr size_t CNT_BYTES = CNT_WORDS * 4 + 16;
+  __device__ __forceinline__ static uint32_t* align_cnt(uint32_t* p) {
+    return reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  }
 
   __device__ __forceinline__ static uint32_t pad(uint32_t i) { return pad32(i); }
 
@@ -60,22 +64,31 @@ struct BinSort {
   }
   // Histogram (SCATTER = false) or scatter (true) of the thread's keys; the branch on
   // `exact` and `full` is uniform across the CTA.
-  template <bool SCATTER>
+  template <bool SCATTER, typename POS>
   __device__ __forceinline__ static void hist_or_scatter(uint32_t* s, uint32_t* cnt, const uint32_t (&r)[V],
                                                          uint32_t mn, uint32_t f, bool exact, bool full,
-                                                         uint32_t b0, uint32_t len) {
+                                                         uint32_t len, POS pos) {
+    // groups of G keys: a scatter's returned slots stay live until the store, so the
+    // compiler may not hoist all V atomics (register pressure, spills)
+    constexpr int G = SCATTER ? 8 : V;
     if (full) {
       if (exact) {
 #pragma unroll
-        for (int j = 0; j < V; j++) bin_op<SCATTER>(s, cnt, r[j], r[j] - mn);
+        for (int j = 0; j < V; j++) {
+          bin_op<SCATTER>(s, cnt, r[j], r[j] - mn);
+          if (j % G == G - 1) asm volatile("" ::: "memory");
+        }
       } else {
 #pragma unroll
-        for (int j = 0; j < V; j++) bin_op<SCATTER>(s, cnt, r[j], __umulhi(r[j] - mn, f));
+        for (int j = 0; j < V; j++) {
+          bin_op<SCATTER>(s, cnt, r[j], __umulhi(r[j] - mn, f));
+          if (j % G == G - 1) asm volatile("" ::: "memory");
+        }
       }
     } else {
 #pragma unroll
       for (int j = 0; j < V; j++)
-        if (b0 + j < len) bin_op<SCATTER>(s, cnt, r[j], exact ? r[j] - mn : __umulhi(r[j] - mn, f));
+        if (pos(j) < len) bin_op<SCATTER>(s, cnt, r[j], exact ? r[j] - mn : __umulhi(r[j] - mn, f));
     }
   }
 
@@ -83,13 +96,25 @@ struct BinSort {
   // padding (left in place).  cnt: CNT_WORDS words of shared memory.  On return
   // the sorted tile is in s and a __syncthreads() has been executed.
   __device__ static void sort_smem(uint32_t* s, uint32_t* cnt, uint32_t len = TILE) {
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    uint32_t* red = cnt + NB;  // [0, 32): warp minima, [32, 64): warp maxima, [64, 68): misc
-    const uint32_t b0 = uint32_t(t) * V;
-    const bool full = b0 + V <= len;
+    const uint32_t b0 = uint32_t(threadIdx.x) * V;
     uint32_t r[V];
 #pragma unroll
     for (int j = 0; j < V; j++) r[j] = s[pad(b0 + j)];
+    sort_regs(r, s, cnt, len, [&](int j) { return b0 + j; });
+  }
+
+  // Same, with the tile's keys already in registers: r[j] holds the key at tile
+  // position pos(j) (any arrangement; positions >= len are ignored).  s receives the
+  // sorted tile (padded layout, positions >= len set to 0xFFFFFFFF).
+  template <typename POS>
+  __device__ static void sort_regs(uint32_t (&r)[V], uint32_t* s, uint32_t* cnt, uint32_t len, POS pos) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    cnt = align_cnt(cnt);
+    uint32_t* red = cnt + NB;  // [0, 32): warp minima, [32, 64): warp maxima, [64, 68): misc
+    const uint32_t b0 = uint32_t(t) * V;
+    bool full = true;
+#pragma unroll
+    for (int j = 0; j < V; j++) full = full && pos(j) < len;
     // ---- 1. min and max of the real keys; counters cleared
     uint32_t mn = 0xffffffffu, mx = 0u;
     if (full) {
@@ -101,10 +126,12 @@ struct BinSort {
     } else {
 #pragma unroll
       for (int j = 0; j < V; j++)
-        if (b0 + j < len) {
+        if (pos(j) < len) {
           mn = min(mn, r[j]);
           mx = max(mx, r[j]);
         }
+      // padding positions of the sorted tile (the scatter fills [0, len))
+      for (uint32_t i = t; i < uint32_t(TILE) - len; i += NT) s[pad(len + i)] = 0xffffffffu;
     }
     mn = __reduce_min_sync(0xffffffffu, mn);
     mx = __reduce_max_sync(0xffffffffu, mx);
@@ -115,29 +142,39 @@ struct BinSort {
 #pragma unroll
     for (int q = 0; q < E; q++) cnt[q * NT + t] = 0u;
     __syncthreads();
-    mn = red[0];
-    mx = red[32];
-#pragma unroll
-    for (int q = 1; q < NW; q++) {
-      mn = min(mn, red[q]);
-      mx = max(mx, red[32 + q]);
+    if (t == 0) {  // tile minimum, bin factor, exactness
+      mn = red[0];
+      mx = red[32];
+      for (int q = 1; q < NW; q++) {
+        mn = min(mn, red[q]);
+        mx = max(mx, red[32 + q]);
+      }
+      const uint32_t range = mx - mn;
+      // f = floor(NB * 2^32 / (range + 1)) < 2^32 when range >= NB
+      red[64] = mn;
+      red[65] = range < uint32_t(NB) ? 0u : (uint32_t)((uint64_t(NB) << 32) / (uint64_t(range) + 1));
     }
-    const uint32_t range = mx - mn;
-    const bool exact = range < uint32_t(NB);
-    // f = floor(NB * 2^32 / (range + 1)) < 2^32 when range >= NB
-    const uint32_t f = exact ? 0u : (uint32_t)((uint64_t(NB) << 32) / (uint64_t(range) + 1));
-    // ---- 2. histogram of the bins
-    hist_or_scatter<false>(s, cnt, r, mn, f, exact, full, b0, len);
     __syncthreads();
-    // ---- exclusive scan of the NB counters (thread t owns [t*E, t*E+E)) and the largest bin
-    uint32_t c[E], sum = 0, big = 0;
+    mn = red[64];
+    uint32_t f = red[65];
+    const bool exact = f == 0u;
+    // ---- 2. histogram of the bins
+    hist_or_scatter<false>(s, cnt, r, mn, f, exact, full, len, pos);
+    __syncthreads();
+    // ---- exclusive scan of the NB counters (thread t owns [t*E, t*E+E)) and the largest
+    // bin.  16-byte chunks are read and written in a per-thread rotated order so the
+    // 8 threads of a shared-memory phase hit 8 different bank groups.
+    constexpr int NQ = E / 4;
+    const int rot = E == 16 ? ((t >> 1) & 3) : (t & 7);
+    uint4* c4 = reinterpret_cast<uint4*>(cnt + t * E);
+    uint4 v[NQ];
+    uint32_t cs[NQ], sum = 0, big = 0;
 #pragma unroll
-    for (int q = 0; q < E; q++) {
-      c[q] = cnt[t * E + q];
-      big = max(big, c[q]);
-      const uint32_t x = c[q];
-      c[q] = sum;
-      sum += x;
+    for (int q = 0; q < NQ; q++) {
+      v[q] = c4[(q + rot) % NQ];
+      cs[q] = v[q].x + v[q].y + v[q].z + v[q].w;
+      big = max(big, max(max(v[q].x, v[q].y), max(v[q].z, v[q].w)));
+      sum += cs[q];
     }
     uint32_t incl = sum;
 #pragma unroll
@@ -149,18 +186,32 @@ struct BinSort {
     if (lane == 31) red[w] = incl;
     if (lane == 0) red[32 + w] = big;
     __syncthreads();
-    uint32_t wbase = 0;
+    uint32_t tb = incl - sum;
 #pragma unroll
-    for (int q = 0; q < NW; q++) wbase += q < w ? red[q] : 0u;
+    for (int q = 0; q < NW; q++) tb += q < w ? red[q] : 0u;
     uint32_t gbig = 0;
 #pragma unroll
     for (int q = 0; q < NW; q++) gbig = max(gbig, red[32 + q]);
-    const uint32_t tbase = wbase + incl - sum;
 #pragma unroll
-    for (int q = 0; q < E; q++) cnt[t * E + q] = tbase + c[q];
+    for (int q = 0; q < NQ; q++) {
+      const int cq = (q + rot) % NQ;  // logical chunk of v[q]
+      uint32_t pre = tb;
+#pragma unroll
+      for (int q2 = 0; q2 < NQ; q2++) pre += ((q2 + rot) % NQ < cq) ? cs[q2] : 0u;
+      uint4 o;
+      o.x = pre;
+      o.y = pre + v[q].x;
+      o.z = o.y + v[q].y;
+      o.w = o.z + v[q].z;
+      c4[cq] = o;
+    }
     __syncthreads();
-    // ---- 3. scatter: each key to the next free slot of its bin
-    hist_or_scatter<true>(s, cnt, r, mn, f, exact, full, b0, len);
+    // ---- 3. scatter: each key to the next free slot of its bin.  The bins are
+    // recomputed (mn and f laundered through asm) rather than kept live across the
+    // scan: V extra registers would spill.
+    asm volatile("mov.b32 %0, %0;" : "+r"(mn));
+    asm volatile("mov.b32 %0, %0;" : "+r"(f));
+    hist_or_scatter<true>(s, cnt, r, mn, f, exact, full, len, pos);
     __syncthreads();
     if (exact) return;  // every bin is one value
     if (gbig > RUNMAX) {  // a bin too long for the fix-up (skewed input): merge sort

@@ -168,6 +168,17 @@ inline int g_big_mode = 1;
 // serialises them on the caller's stream; measured 6.47 vs 6.61 ms at cfg5)
 inline int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv("SQ_CONCURRENT_CLASSES")) : 1;
 
+// on-chip base case for keys-only 32-bit sorts: 1 = counting sort + network
+// fix-up (binsort.cuh, default), 0 = merge sort (blocksort.cuh)
+inline int g_base_case = getenv("SQ_BASE_CASE") ? atoi(getenv("SQ_BASE_CASE")) : 1;
+template <bool ENABLE, typename F>
+void with_base_case(F&& f) {
+  if constexpr (ENABLE) {
+    if (g_base_case) return f(std::true_type{});
+  }
+  f(std::false_type{});
+}
+
 // ------------------------------------------------------------------ device check
 // The device must be an sm_100 part.  Scratch comes from a pool the library owns
 // (the device's default pool and other users' allocations are left alone); freed
@@ -376,13 +387,13 @@ void with_tile(uint32_t tile, F&& f) {
       case 64: return f(IC<32>{}, IC<2>{});
       case 128: return f(IC<32>{}, IC<4>{});
       case 256: return f(IC<32>{}, IC<8>{});
-      case 512: return f(IC<64>{}, IC<8>{});
-      case 1024: return f(IC<128>{}, IC<8>{});
-      case 2048: return f(IC<128>{}, IC<16>{});
+      case 512: return f(IC<32>{}, IC<16>{});
+      case 1024: return f(IC<32>{}, IC<32>{});
+      case 2048: return f(IC<64>{}, IC<32>{});
       case 3072: return f(IC<96>{}, IC<32>{});
-      case 4096: return f(IC<256>{}, IC<16>{});
+      case 4096: return f(IC<128>{}, IC<32>{});
       case 6144: return f(IC<192>{}, IC<32>{});
-      case 8192: return f(IC<512>{}, IC<16>{});
+      case 8192: return f(IC<256>{}, IC<32>{});
       case 12288: return f(IC<384>{}, IC<32>{});
       case 16384: return f(IC<512>{}, IC<32>{});
       case 24576: return f(IC<768>{}, IC<32>{});
@@ -796,10 +807,12 @@ struct Engine {
         with_tile<SK>(cd.first, [&](auto nt, auto v) {
           constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
           using BS = BlockSort<SK, NT, V>;
-          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
-          set_smem(k_colsort<K, NT, V, PAIRS>, smem);
+          with_base_case<std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
+          constexpr bool BIN = decltype(bin)::value;
+          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + bin_smem<K, NT, V, PAIRS, BIN>();
+          set_smem(k_colsort<K, NT, V, PAIRS, BIN>, smem);
           ProfScope ps("colsort", st);
-          auto f = k_colsort<K, NT, V, PAIRS>;
+          auto f = k_colsort<K, NT, V, PAIRS, BIN>;
           if (first && !g_prof.load())
             launch_pdl(f, ncol, NT, smem, st, cd.second, (const LevelSeg*)dL, kb[X], PAIRS ? vb[X] : nullptr,
                        (const K*)piv, segmat, segmin);
@@ -807,6 +820,7 @@ struct Engine {
             f<<<ncol, NT, smem, st>>>(cd.second, dL, kb[X], PAIRS ? vb[X] : nullptr, piv, segmat, segmin);
           check_launch("k_colsort");
           first = false;
+          });
         });
       }
     } else {  // columns longer than a CTA holds: a recursive level sorts them
@@ -964,8 +978,11 @@ struct Engine {
       with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
         constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
         using BS = BlockSort<SK, NT, V>;
-        const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4;
-        auto f = k_bucketsort<K, NT, V, PAIRS>;
+        with_base_case<std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
+        constexpr bool BIN = decltype(bin)::value;
+        const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4 +
+                            bin_smem<K, NT, V, PAIRS, BIN>();
+        auto f = k_bucketsort<K, NT, V, PAIRS, BIN>;
         const int grid = wave_grid(f, NT, smem);
         std::optional<ProfScope> ps;
         if (!g_concurrent_classes) ps.emplace("bucketsort", cs);
@@ -973,6 +990,7 @@ struct Engine {
             recs, dTiles, lst, po.count + li, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
             ppre, kb[2], PAIRS ? vb[2] : nullptr, po.units);
         check_launch("k_bucketsort");
+        });
       });
     };
     auto launch_merges = [&](cudaStream_t ms) {  // merge passes of the multi-CTA base case (X <-> U)

@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 #include <type_traits>
 #include "level.cuh"
+#include "binsort.cuh"
 
 namespace sq {
 
@@ -67,6 +68,25 @@ struct MTile {
 constexpr int kMaxPasses = 4;  // 16 chunks
 
 constexpr int kPP = kTB + 1;  // prefix entries per piece
+
+// The counting-sort base case (binsort.cuh) serves keys-only 32-bit sorts with 16
+// or 32 keys per thread; everything else uses the merge sort (blocksort.cuh).
+template <typename K, int V, bool PAIRS>
+__host__ __device__ constexpr bool bin_ok() {
+  return std::is_same<K, uint32_t>::value && !PAIRS && (V == 16 || V == 32);
+}
+// shared memory of the counting sort's counters (0 when the merge sort runs)
+template <typename K, int NT, int V, bool PAIRS, bool BIN>
+__host__ __device__ constexpr size_t bin_smem() {
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) return BinSort<NT, V>::CNT_BYTES;
+  else return 0;
+}
+// Sort the tile in shared memory with the selected base case.
+template <typename K, int NT, int V, bool PAIRS, bool BIN, typename SK>
+__device__ __forceinline__ void tile_sort(SK* s, uint32_t* cnt, uint32_t len) {
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) BinSort<NT, V>::sort_smem(reinterpret_cast<uint32_t*>(s), cnt, len);
+  else BlockSort<SK, NT, V>::sort_smem(s, len);
+}
 
 // ------------------------------------------------------------------------------
 // All kCap sampling rounds of every segment in parallel (CTA = (segment, round)),
@@ -153,8 +173,14 @@ struct ColDesc {
   uint32_t off, len, seg, col;
 };
 
-template <typename K, int NT, int V, bool PAIRS>
-__global__ void __launch_bounds__(NT)
+// resident CTAs per SM the counting-sort kernels are compiled for (64 registers)
+template <typename K, int NT, int V, bool PAIRS, bool BIN>
+__host__ __device__ constexpr int bin_min_blocks() {
+  return (BIN && bin_ok<K, V, PAIRS>()) ? (NT >= 1024 ? 1 : 1024 / NT) : 1;
+}
+
+template <typename K, int NT, int V, bool PAIRS, bool BIN>
+__global__ void __launch_bounds__(NT, (bin_min_blocks<K, NT, V, PAIRS, BIN>()))
 k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K* __restrict__ keys,
           uint32_t* __restrict__ vals, const K* __restrict__ piv, uint32_t* __restrict__ segmat,
           K* __restrict__ segmin) {
@@ -167,35 +193,57 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   const LevelSeg sg = segs[d.seg];
   constexpr int VW = 16 / sizeof(K), NV = BS::TILE / (NT * VW);  // 16-byte vectors per thread
   constexpr bool VEC = !PAIRS && NV >= 1 && NV * NT * VW == BS::TILE;
-  if (VEC && d.len == BS::TILE && (reinterpret_cast<uintptr_t>(keys + d.off) & 15) == 0) {
-    // full, aligned column: every vector load in flight before the first store
-    const uint4* g = reinterpret_cast<const uint4*>(keys + d.off);
-    uint4 v[NV > 0 ? NV : 1];
+  const bool vec_ok = VEC && d.len == BS::TILE && (reinterpret_cast<uintptr_t>(keys + d.off) & 15) == 0;
+  bool sorted = false;
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) {
+    if (vec_ok) {  // full, aligned column: straight from 16-byte loads into the sort's registers
+      static_assert(NV * VW == V, "vector loads fill the thread's keys");
+      uint32_t r[V];
+      const uint4* g = reinterpret_cast<const uint4*>(keys + d.off);
 #pragma unroll
-    for (int q = 0; q < NV; q++) v[q] = g[threadIdx.x + q * NT];
-#pragma unroll
-    for (int q = 0; q < NV; q++) {
-      const uint32_t i0 = (threadIdx.x + q * NT) * VW;
-      const K* e = reinterpret_cast<const K*>(&v[q]);
-#pragma unroll
-      for (int j = 0; j < VW; j++) s[BS::pad(i0 + j)] = SK(e[j]);
-    }
-  } else {
-    for (int i = threadIdx.x; i < BS::TILE; i += NT) {
-      SK x = KeyTraits<SK>::kMax;
-      if (i < (int)d.len) {
-        if constexpr (PAIRS) {
-          x = (uint64_t(keys[d.off + i]) << 32) | uint32_t(i);
-          vs[i] = vals[d.off + i];
-        } else {
-          x = keys[d.off + i];
-        }
+      for (int q = 0; q < NV; q++) {
+        const uint4 x = g[threadIdx.x + q * NT];
+        r[4 * q] = x.x;
+        r[4 * q + 1] = x.y;
+        r[4 * q + 2] = x.z;
+        r[4 * q + 3] = x.w;
       }
-      s[BS::pad(i)] = x;
+      BinSort<NT, V>::sort_regs(r, reinterpret_cast<uint32_t*>(s), reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES),
+                                d.len, [&](int j) { return (threadIdx.x + (j / 4) * NT) * 4 + (j % 4); });
+      sorted = true;
     }
   }
-  __syncthreads();
-  BS::sort_smem(s, d.len);
+  if (!sorted) {
+    if (vec_ok) {
+      // full, aligned column: every vector load in flight before the first store
+      const uint4* g = reinterpret_cast<const uint4*>(keys + d.off);
+      uint4 v[NV > 0 ? NV : 1];
+#pragma unroll
+      for (int q = 0; q < NV; q++) v[q] = g[threadIdx.x + q * NT];
+#pragma unroll
+      for (int q = 0; q < NV; q++) {
+        const uint32_t i0 = (threadIdx.x + q * NT) * VW;
+        const K* e = reinterpret_cast<const K*>(&v[q]);
+#pragma unroll
+        for (int j = 0; j < VW; j++) s[BS::pad(i0 + j)] = SK(e[j]);
+      }
+    } else {
+      for (int i = threadIdx.x; i < BS::TILE; i += NT) {
+        SK x = KeyTraits<SK>::kMax;
+        if (i < (int)d.len) {
+          if constexpr (PAIRS) {
+            x = (uint64_t(keys[d.off + i]) << 32) | uint32_t(i);
+            vs[i] = vals[d.off + i];
+          } else {
+            x = keys[d.off + i];
+          }
+        }
+        s[BS::pad(i)] = x;
+      }
+    }
+    __syncthreads();
+    tile_sort<K, NT, V, PAIRS, BIN>(s, reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES), d.len);
+  }
   // (programmatic dependent launch) the sampler must be done reading the unsorted
   // input, and the pivots must be selected, before this CTA writes or reads them
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -775,8 +823,8 @@ __device__ __forceinline__ void gather_bucket(const TileInfo& ti, uint32_t lane_
 // Bucket sort with gather: CTA loops over its class list.  An item is a
 // whole bucket or one chunk of a merge-sorted bucket; chunks of a bucket with an
 // odd number of merge passes go to `dst_odd`, so the last pass ends in `dst`.
-template <typename K, int NT, int V, bool PAIRS>
-__global__ void __launch_bounds__(NT)
+template <typename K, int NT, int V, bool PAIRS, bool BIN>
+__global__ void __launch_bounds__(NT, (bin_min_blocks<K, NT, V, PAIRS, BIN>()))
 k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
              const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
              const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst, const uint32_t* __restrict__ pout,
@@ -791,6 +839,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
   uint32_t* s_len = s_off + NT;
   uint32_t* s_dst = s_len + NT;
   uint32_t* misc = s_dst + NT;
+  uint32_t* cnt = misc + 64;  // counting-sort counters (BIN)
   const uint32_t total = *count;
   for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
     const uint32_t e = list[it];
@@ -841,7 +890,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
       }
       __syncthreads();
     }
-    BS::sort_smem(s, len);
+    tile_sort<K, NT, V, PAIRS, BIN>(s, cnt, len);
     for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
       if constexpr (PAIRS) {

@@ -1,0 +1,99 @@
+// Base-case microbenchmark: one CTA sorts each 16K-key tile of a 2^28-key
+// array (the column-sort shape of cfg5) with the counting sort (binsort.cuh)
+// or the merge sort (blocksort.cuh); checks every tile is a sorted permutation
+// (sum and xor of keys kept, non-decreasing).  Not part of the product.
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../paper_2407_14801_b200/csrc/binsort.cuh"
+
+using namespace sq;
+
+template <int NT, int V, int MINB, bool BIN>
+__global__ void __launch_bounds__(NT, MINB) k_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                    uint32_t len) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  constexpr int TILE = NT * V;
+  uint32_t* s = (uint32_t*)sm;
+  uint32_t* cnt = s + TILE + TILE / 32 + 1;
+  const uint32_t* g = in + size_t(blockIdx.x) * TILE;
+  for (int i = threadIdx.x; i < TILE; i += NT) s[pad32(i)] = i < (int)len ? g[i] : 0xffffffffu;
+  __syncthreads();
+  if constexpr (BIN) BinSort<NT, V>::sort_smem(s, cnt, len);
+  else BlockSort<uint32_t, NT, V>::sort_smem(s, len);
+  uint32_t* o = out + size_t(blockIdx.x) * TILE;
+  for (int i = threadIdx.x; i < (int)len; i += NT) o[i] = s[pad32(i)];
+}
+
+static uint64_t splitmix(uint64_t& x) {
+  uint64_t z = (x += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+template <int NT, int V, int MINB, bool BIN>
+void run(const char* name, const std::vector<uint32_t>& h, uint32_t len) {
+  constexpr int TILE = NT * V;
+  const size_t n = h.size(), ntiles = n / TILE;
+  uint32_t *din, *dout;
+  cudaMalloc(&din, n * 4);
+  cudaMalloc(&dout, n * 4);
+  cudaMemcpy(din, h.data(), n * 4, cudaMemcpyHostToDevice);
+  const size_t smem = (TILE + TILE / 32 + 1) * 4 + (BIN ? BinSort<NT, V>::CNT_BYTES : 0);
+  cudaFuncSetAttribute(k_tiles<NT, V, MINB, BIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9f;
+  for (int it = 0; it < 8; it++) {
+    cudaEventRecord(a);
+    k_tiles<NT, V, MINB, BIN><<<(unsigned)ntiles, NT, smem>>>(din, dout, len);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (it >= 2 && ms < best) best = ms;
+  }
+  cudaError_t e = cudaGetLastError();
+  std::vector<uint32_t> o(n);
+  cudaMemcpy(o.data(), dout, n * 4, cudaMemcpyDeviceToHost);
+  size_t bad = 0;
+  for (size_t t = 0; t < ntiles; t++) {
+    uint64_t s1 = 0, s2 = 0, x1 = 0, x2 = 0;
+    for (uint32_t i = 0; i < len; i++) {
+      const uint32_t u = h[t * TILE + i], v = o[t * TILE + i];
+      s1 += u; s2 += v; x1 ^= u * 0x9e3779b1u; x2 ^= v * 0x9e3779b1u;
+      if (i && o[t * TILE + i - 1] > v) { bad++; break; }
+    }
+    if (s1 != s2 || x1 != x2) bad++;
+  }
+  const double keys = double(ntiles) * len;
+  printf("%-36s tile %5d len %5u: %7.3f ms  %6.1f Gkeys/s  bad tiles %zu  %s\n", name, TILE, len, best,
+         keys / best * 1e-6, bad, cudaGetErrorString(e));
+  cudaFree(din);
+  cudaFree(dout);
+}
+
+int main() {
+  const size_t n = size_t(1) << 28;
+  std::vector<uint32_t> h(n);
+  uint64_t st = 5;
+  for (auto& x : h) x = uint32_t(splitmix(st) >> 32);
+  run<512, 32, 2, true>("binsort uniform", h, 16384);
+  run<512, 32, 1, false>("mergesort uniform", h, 16384);
+  run<512, 32, 2, true>("binsort uniform ragged", h, 16000);
+  run<256, 32, 2, true>("binsort uniform 8K", h, 8192);
+  run<1024, 32, 1, true>("binsort uniform 32K", h, 32768);
+  // narrow-range tiles (a bucket of cfg5: range ~2^18)
+  for (auto& x : h) x = uint32_t(splitmix(st) >> 46);
+  run<512, 32, 2, true>("binsort range 2^18", h, 16384);
+  // low cardinality (exact bins)
+  for (auto& x : h) x = uint32_t(splitmix(st) % 1000);
+  run<512, 32, 2, true>("binsort 1000 values", h, 16384);
+  // skewed: mostly one value plus outliers (fallback)
+  for (size_t i = 0; i < n; i++) h[i] = (i % 97 == 0) ? uint32_t(splitmix(st) >> 32) : 12345u;
+  run<512, 32, 2, true>("binsort skewed (fallback)", h, 16384);
+  return 0;
+}
