@@ -6,10 +6,6 @@
 // exception crosses the ABI.
 #include "engine.cuh"
 
-namespace sq {
-SQ_ENGINE_INSTANCES(extern)
-}  // namespace sq
-
 
 using namespace sq;
 

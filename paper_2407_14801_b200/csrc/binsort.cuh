@@ -47,8 +47,10 @@ struct BinSort {
   // (+16 bytes: the counters are aligned up to 16 bytes for vector access)
   static constexpr size_t CNT_WORDS = NB + 2 * 32 + 4;
   static constexpr size_t CNT_BYTES = CNT_WORDS * 4 + 16;
+  // (pointer arithmetic on p, so the compiler keeps it in the shared window)
   __device__ __forceinline__ static uint32_t* align_cnt(uint32_t* p) {
-    return reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(p)) & 15u;
+    return p + ((16u - mis) & 15u) / 4u;
   }
 
   __device__ __forceinline__ static uint32_t pad(uint32_t i) { return pad32(i); }

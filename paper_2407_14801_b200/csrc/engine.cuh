@@ -171,12 +171,9 @@ inline int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv(
 // on-chip base case for keys-only 32-bit sorts: 1 = counting sort + network
 // fix-up (binsort.cuh, default), 0 = merge sort (blocksort.cuh)
 inline int g_base_case = getenv("SQ_BASE_CASE") ? atoi(getenv("SQ_BASE_CASE")) : 1;
-template <bool ENABLE, typename F>
-void with_base_case(F&& f) {
-  if constexpr (ENABLE) {
-    if (g_base_case) return f(std::true_type{});
-  }
-  f(std::false_type{});
+template <bool B, typename F>
+void with_bin(F&& f) {
+  f(std::integral_constant<bool, B>{});
 }
 
 // ------------------------------------------------------------------ device check
@@ -473,7 +470,10 @@ template <typename SK> struct ClusterBig;
 template <> struct ClusterBig<uint32_t> { static constexpr int NT = 512, V = 32, TILE = 16384; };
 template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16, TILE = 8192; };
 // largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
-template <typename SK> constexpr uint32_t single_cap() { return sizeof(SK) == 4 ? 16384u : 8192u; }
+// (the counting-sort base case sorts up to 32K 32-bit keys per CTA at full rate;
+// SQ_ONE_CAP overrides it for experiments)
+inline uint32_t g_one_cap = getenv("SQ_ONE_CAP") ? (uint32_t)atoi(getenv("SQ_ONE_CAP")) : 32768u;
+template <typename SK> uint32_t single_cap() { return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : 8192u; }
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
 template <typename K, bool PAIRS> struct MergeCfg {
@@ -561,7 +561,9 @@ struct DebugOut {  // sq_debug_level_u32
   uint32_t* info;
 };
 
-template <typename K, bool PAIRS>
+// BIN: the counting-sort base case (keys-only u32); each (K, PAIRS, BIN) is
+// compiled in its own translation unit (inst_*.cu).
+template <typename K, bool PAIRS, bool BIN = false>
 struct Engine {
   using SK = typename std::conditional<PAIRS, uint64_t, K>::type;  // on-chip sort key
   cudaStream_t st;
@@ -807,12 +809,12 @@ struct Engine {
         with_tile<SK>(cd.first, [&](auto nt, auto v) {
           constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
           using BS = BlockSort<SK, NT, V>;
-          with_base_case<std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
-          constexpr bool BIN = decltype(bin)::value;
-          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + bin_smem<K, NT, V, PAIRS, BIN>();
-          set_smem(k_colsort<K, NT, V, PAIRS, BIN>, smem);
+          with_bin<BIN && std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
+          constexpr bool UB = decltype(bin)::value;
+          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + bin_smem<K, NT, V, PAIRS, UB>();
+          set_smem(k_colsort<K, NT, V, PAIRS, UB>, smem);
           ProfScope ps("colsort", st);
-          auto f = k_colsort<K, NT, V, PAIRS, BIN>;
+          auto f = k_colsort<K, NT, V, PAIRS, UB>;
           if (first && !g_prof.load())
             launch_pdl(f, ncol, NT, smem, st, cd.second, (const LevelSeg*)dL, kb[X], PAIRS ? vb[X] : nullptr,
                        (const K*)piv, segmat, segmin);
@@ -978,11 +980,11 @@ struct Engine {
       with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
         constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
         using BS = BlockSort<SK, NT, V>;
-        with_base_case<std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
-        constexpr bool BIN = decltype(bin)::value;
+        with_bin<BIN && std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
+        constexpr bool UB = decltype(bin)::value;
         const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4 +
-                            bin_smem<K, NT, V, PAIRS, BIN>();
-        auto f = k_bucketsort<K, NT, V, PAIRS, BIN>;
+                            bin_smem<K, NT, V, PAIRS, UB>();
+        auto f = k_bucketsort<K, NT, V, PAIRS, UB>;
         const int grid = wave_grid(f, NT, smem);
         std::optional<ProfScope> ps;
         if (!g_concurrent_classes) ps.emplace("bucketsort", cs);
@@ -1113,13 +1115,55 @@ inline bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
-template <typename K, bool PAIRS>
-void sort_device(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
+template <typename K, bool PAIRS, bool BIN>
+void sort_engine(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
   Arena ar(st);
-  Engine<K, PAIRS> eng(st, ar, keys, vals, n);
+  Engine<K, PAIRS, BIN> eng(st, ar, keys, vals, n);
   std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
   eng.sort_batch(top, 0, 0, 0, "smallsort");
   SQ_CUDA(cudaGetLastError());
+}
+
+template <bool BIN>
+void debug_level_engine(const uint32_t* src, uint32_t* dst, size_t n, uint64_t seed, uint32_t* pivots_out,
+                        uint32_t* bucend_out, uint32_t* info_out, cudaStream_t st) {
+  Arena ar(st);
+  uint32_t* work = (uint32_t*)ar.alloc(n * 4);
+  SQ_CUDA(cudaMemcpyAsync(work, src, n * 4, cudaMemcpyDeviceToDevice, st));
+  Engine<uint32_t, false, BIN> eng(st, ar, work, nullptr, n);
+  DebugOut dbg{dst, pivots_out, bucend_out, info_out};
+  std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
+  eng.run_level(top, 0, 0, &dbg);
+  SQ_CUDA(cudaStreamSynchronize(st));
+}
+
+// The engine is compiled once per (key type, pairs, base case) in its own
+// translation unit (inst_*.cu, built in parallel); every other unit sees only
+// these declarations.
+#define SQ_ENGINE_INSTANCES(X)                                                                        \
+  X template void sort_engine<uint32_t, false, true>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void sort_engine<uint32_t, false, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void sort_engine<uint64_t, false, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void sort_engine<uint32_t, true, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void debug_level_engine<true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*,  \
+                                           uint32_t*, cudaStream_t);                            \
+  X template void debug_level_engine<false>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*, \
+                                            uint32_t*, cudaStream_t);
+SQ_ENGINE_INSTANCES(extern)
+
+// Sort on the device with the selected base case (sq_set_base_case).
+template <typename K, bool PAIRS>
+void sort_device(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
+  if constexpr (std::is_same<K, uint32_t>::value && !PAIRS) {
+    if (g_base_case) return sort_engine<K, PAIRS, true>(keys, vals, n, seed, st);
+  }
+  sort_engine<K, PAIRS, false>(keys, vals, n, seed, st);
+}
+
+inline void debug_level_u32(const uint32_t* src, uint32_t* dst, size_t n, uint64_t seed, uint32_t* pivots_out,
+                            uint32_t* bucend_out, uint32_t* info_out, cudaStream_t st) {
+  if (g_base_case) debug_level_engine<true>(src, dst, n, seed, pivots_out, bucend_out, info_out, st);
+  else debug_level_engine<false>(src, dst, n, seed, pivots_out, bucend_out, info_out, st);
 }
 
 template <typename K, bool PAIRS>
@@ -1262,16 +1306,5 @@ int batch_entry(const K* const* in, K* const* out, size_t n, size_t count, uint6
     SQ_CUDA(cudaStreamSynchronize(st));
   });
 }
-
-// The engine is compiled once per (key type, pairs) in its own translation unit
-// (inst_*.cu, built in parallel); every other unit sees only these declarations.
-#define SQ_ENGINE_INSTANCES(X)                                                        \
-  X template void sort_device<uint32_t, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
-  X template void sort_device<uint64_t, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
-  X template void sort_device<uint32_t, true>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t);
-
-// sq_debug_level_u32: one level of the u32 engine with intermediate outputs (inst_u32.cu)
-void debug_level_u32(const uint32_t* src, uint32_t* dst, size_t n, uint64_t seed, uint32_t* pivots_out,
-                     uint32_t* bucend_out, uint32_t* info_out, cudaStream_t st);
 
 }  // namespace sq

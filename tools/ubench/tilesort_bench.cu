@@ -18,10 +18,20 @@ __global__ void __launch_bounds__(NT, MINB) k_tiles(const uint32_t* __restrict__
   uint32_t* s = (uint32_t*)sm;
   uint32_t* cnt = s + TILE + TILE / 32 + 1;
   const uint32_t* g = in + size_t(blockIdx.x) * TILE;
-  for (int i = threadIdx.x; i < TILE; i += NT) s[pad32(i)] = i < (int)len ? g[i] : 0xffffffffu;
-  __syncthreads();
-  if constexpr (BIN) BinSort<NT, V>::sort_smem(s, cnt, len);
-  else BlockSort<uint32_t, NT, V>::sort_smem(s, len);
+  if (BIN && len == TILE) {  // the column sort's path: 16-byte loads straight into registers
+    uint32_t r[V];
+#pragma unroll
+    for (int q = 0; q < V / 4; q++) {
+      const uint4 x = reinterpret_cast<const uint4*>(g)[threadIdx.x + q * NT];
+      r[4 * q] = x.x; r[4 * q + 1] = x.y; r[4 * q + 2] = x.z; r[4 * q + 3] = x.w;
+    }
+    BinSort<NT, V>::sort_regs(r, s, cnt, len, [&](int j) { return (threadIdx.x + (j / 4) * NT) * 4 + (j % 4); });
+  } else {
+    for (int i = threadIdx.x; i < TILE; i += NT) s[pad32(i)] = i < (int)len ? g[i] : 0xffffffffu;
+    __syncthreads();
+    if constexpr (BIN) BinSort<NT, V>::sort_smem(s, cnt, len);
+    else BlockSort<uint32_t, NT, V>::sort_smem(s, len);
+  }
   uint32_t* o = out + size_t(blockIdx.x) * TILE;
   for (int i = threadIdx.x; i < (int)len; i += NT) o[i] = s[pad32(i)];
 }
