@@ -299,6 +299,29 @@ def test_sample_pivots_invariants_and_round_rule():
                 assert (cand == P).all()
 
 
+@pytest.mark.parametrize("cap", [32, 5, 1])
+def test_sample_pivots_degenerate_keeps_last_round(cap):
+    # S:94 / L8: after `cap` failed rounds the pivots are degenerate and round cap-1's
+    # sorted candidates are kept.  Low cardinality (400 keys over 3 values) makes every
+    # round fail (m-1 = 19 draws cannot be strictly increasing); the kept set must be
+    # round cap-1's draw, recomputed from the RNG spec (a different round's draw differs).
+    rng = np.random.default_rng(21)
+    n = 400
+    x = rng.integers(0, 3, n).astype(np.uint64) + 5
+    m = O.ceil_sqrt(n)
+    D = x.copy()
+    for a in range(0, n, m):
+        D[a:a + m] = np.sort(D[a:a + m])
+    for s in range(10):
+        node = O.root_key(s)
+        P, r, deg = O.sample_pivots(node, x, D, cap=cap)
+        assert deg == 1 and r == cap - 1
+        rounds = [np.sort([x[O.index(O.draw(node, rr, i), n)] for i in range(m - 1)]) for rr in range(cap)]
+        assert (P == rounds[cap - 1]).all()
+        if cap > 1:  # the rounds differ, so keeping another round would be caught
+            assert any((rounds[rr] != rounds[cap - 1]).any() for rr in range(cap - 1))
+
+
 def test_mean_rounds_closed_form():
     # Distinct keys: a round succeeds iff the m-1 positions are distinct and avoid the
     # minimum: p = prod_{i=0}^{m-2} (n-1-i)/n; E[rounds] = 1/p  (<= e^2).
@@ -326,14 +349,14 @@ def test_square_sort_spec(golden):
     assert d.tolist() == list(range(1, 101))
 
 
-@pytest.mark.parametrize("n", range(0, 9))
+@pytest.mark.parametrize("n", range(0, 10))
 def test_square_sort_all_permutations(n):
     for perm in itertools.permutations(range(n)):
         d, _, _ = O.square_sort(np.array(perm, np.uint64), cutoff=4, seed=n)
         assert d.tolist() == list(range(n))
 
 
-@pytest.mark.parametrize("n", range(5, 9))
+@pytest.mark.parametrize("n", range(5, 10))
 def test_square_sort_all_ternary(n):
     for t in itertools.product(range(3), repeat=n):
         d, _, _ = O.square_sort(np.array(t, np.uint64), cutoff=4, seed=1)
