@@ -226,6 +226,11 @@ int sq_debug_level_u32(const uint32_t *src, uint32_t *dst, size_t n, uint64_t se
                        uint32_t *pivots_out, uint32_t *bucend_out, uint32_t *info_out,
                        void *stream);
 
+/* The same for u64 keys (the pivots are u64; n in [5, 2^28]). */
+int sq_debug_level_u64(const uint64_t *src, uint64_t *dst, size_t n, uint64_t seed,
+                       uint64_t *pivots_out, uint32_t *bucend_out, uint32_t *info_out,
+                       void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_h
            "sq_sort_u64_host_batch", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode",
-           "sq_trim_memory", "sq_set_base_case"]
+           "sq_trim_memory", "sq_set_base_case", "sq_debug_level_u64"]
 
 
 class SqError(RuntimeError):
@@ -87,6 +87,8 @@ def lib():
         L.sq_profile_read.restype = ctypes.c_int
         L.sq_debug_level_u32.argtypes = [vp, vp, sz, u64, vp, vp, vp, vp]
         L.sq_debug_level_u32.restype = ctypes.c_int
+        L.sq_debug_level_u64.argtypes = [vp, vp, sz, u64, vp, vp, vp, vp]
+        L.sq_debug_level_u64.restype = ctypes.c_int
         L.sq_set_base_case.argtypes = [ctypes.c_int]
         L.sq_set_base_case.restype = ctypes.c_int
         L.sq_trim_memory.argtypes = []
@@ -204,6 +206,15 @@ def debug_level_u32(src, dst, seed: int, pivots_out, bucend_out, info_out, strea
     with _on(src):
         _check(lib().sq_debug_level_u32(_dev(src, "torch.uint32"), _dev(dst, "torch.uint32", d),
                                         src.numel(), _seed(seed), _dev(pivots_out, "torch.uint32", d),
+                                        _dev(bucend_out, "torch.uint32", d), _dev(info_out, "torch.uint32", d),
+                                        _stream(stream)))
+
+
+def debug_level_u64(src, dst, seed: int, pivots_out, bucend_out, info_out, stream=None):
+    d = src.device
+    with _on(src):
+        _check(lib().sq_debug_level_u64(_dev(src, "torch.uint64"), _dev(dst, "torch.uint64", d),
+                                        src.numel(), _seed(seed), _dev(pivots_out, "torch.uint64", d),
                                         _dev(bucend_out, "torch.uint32", d), _dev(info_out, "torch.uint32", d),
                                         _stream(stream)))
 

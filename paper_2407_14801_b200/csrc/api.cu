@@ -232,4 +232,15 @@ int sq_debug_level_u32(const uint32_t* src, uint32_t* dst, size_t n, uint64_t se
   });
 }
 
+int sq_debug_level_u64(const uint64_t* src, uint64_t* dst, size_t n, uint64_t seed, uint64_t* pivots_out,
+                       uint32_t* bucend_out, uint32_t* info_out, void* stream) {
+  return guarded([&] {
+    need(n >= 5 && n <= (size_t(1) << 28), "n must be in [5, 2^28]");
+    need(src && dst && pivots_out && bucend_out && info_out, "NULL pointer");
+    need(!overlap(src, n * 8, dst, n * 8), "src and dst overlap");
+    check_device();
+    debug_level_engine<uint64_t, false>(src, dst, n, seed, pivots_out, bucend_out, info_out, (cudaStream_t)stream);
+  });
+}
+
 }  // extern "C"

@@ -554,9 +554,9 @@ struct Seg {
   uint64_t node;
 };
 
-struct DebugOut {  // sq_debug_level_u32
-  uint32_t* dst;
-  uint32_t* pivots;
+struct DebugOut {  // sq_debug_level_u32 / _u64
+  void* dst;       // n keys (K)
+  void* pivots;    // m-1 keys (K)
   uint32_t* bucend;
   uint32_t* info;
 };
@@ -1124,13 +1124,13 @@ void sort_engine(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t 
   SQ_CUDA(cudaGetLastError());
 }
 
-template <bool BIN>
-void debug_level_engine(const uint32_t* src, uint32_t* dst, size_t n, uint64_t seed, uint32_t* pivots_out,
-                        uint32_t* bucend_out, uint32_t* info_out, cudaStream_t st) {
+template <typename K, bool BIN>
+void debug_level_engine(const K* src, K* dst, size_t n, uint64_t seed, K* pivots_out, uint32_t* bucend_out,
+                        uint32_t* info_out, cudaStream_t st) {
   Arena ar(st);
-  uint32_t* work = (uint32_t*)ar.alloc(n * 4);
-  SQ_CUDA(cudaMemcpyAsync(work, src, n * 4, cudaMemcpyDeviceToDevice, st));
-  Engine<uint32_t, false, BIN> eng(st, ar, work, nullptr, n);
+  K* work = (K*)ar.alloc(n * sizeof(K));
+  SQ_CUDA(cudaMemcpyAsync(work, src, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+  Engine<K, false, BIN> eng(st, ar, work, nullptr, n);
   DebugOut dbg{dst, pivots_out, bucend_out, info_out};
   std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};
   eng.run_level(top, 0, 0, &dbg);
@@ -1145,10 +1145,12 @@ void debug_level_engine(const uint32_t* src, uint32_t* dst, size_t n, uint64_t s
   X template void sort_engine<uint32_t, false, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint64_t, false, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint32_t, true, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
-  X template void debug_level_engine<true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*,  \
-                                           uint32_t*, cudaStream_t);                            \
-  X template void debug_level_engine<false>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*, \
-                                            uint32_t*, cudaStream_t);
+  X template void debug_level_engine<uint32_t, true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*,   \
+                                                     uint32_t*, uint32_t*, cudaStream_t);                     \
+  X template void debug_level_engine<uint32_t, false>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*,  \
+                                                      uint32_t*, uint32_t*, cudaStream_t);                    \
+  X template void debug_level_engine<uint64_t, false>(const uint64_t*, uint64_t*, size_t, uint64_t, uint64_t*,  \
+                                                      uint32_t*, uint32_t*, cudaStream_t);
 SQ_ENGINE_INSTANCES(extern)
 
 // Sort on the device with the selected base case (sq_set_base_case).
@@ -1162,8 +1164,8 @@ void sort_device(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t 
 
 inline void debug_level_u32(const uint32_t* src, uint32_t* dst, size_t n, uint64_t seed, uint32_t* pivots_out,
                             uint32_t* bucend_out, uint32_t* info_out, cudaStream_t st) {
-  if (g_base_case) debug_level_engine<true>(src, dst, n, seed, pivots_out, bucend_out, info_out, st);
-  else debug_level_engine<false>(src, dst, n, seed, pivots_out, bucend_out, info_out, st);
+  if (g_base_case) debug_level_engine<uint32_t, true>(src, dst, n, seed, pivots_out, bucend_out, info_out, st);
+  else debug_level_engine<uint32_t, false>(src, dst, n, seed, pivots_out, bucend_out, info_out, st);
 }
 
 template <typename K, bool PAIRS>

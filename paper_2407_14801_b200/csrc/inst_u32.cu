@@ -4,6 +4,6 @@
 
 namespace sq {
 template void sort_engine<uint32_t, false, true>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t);
-template void debug_level_engine<true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*, uint32_t*,
-                                       cudaStream_t);
+template void debug_level_engine<uint32_t, true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*,
+                                                 uint32_t*, cudaStream_t);
 }  // namespace sq

@@ -4,6 +4,6 @@
 
 namespace sq {
 template void sort_engine<uint32_t, false, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t);
-template void debug_level_engine<false>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*, uint32_t*,
-                                        cudaStream_t);
+template void debug_level_engine<uint32_t, false>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*, uint32_t*,
+                                                  uint32_t*, cudaStream_t);
 }  // namespace sq

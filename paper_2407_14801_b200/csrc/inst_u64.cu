@@ -4,4 +4,6 @@
 
 namespace sq {
 template void sort_engine<uint64_t, false, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t);
+template void debug_level_engine<uint64_t, false>(const uint64_t*, uint64_t*, size_t, uint64_t, uint64_t*, uint32_t*,
+                                                  uint32_t*, cudaStream_t);
 }  // namespace sq
