@@ -267,52 +267,46 @@ def main():
 
     hbm, hbm_src, sm_mhz_max = peaks()
     b_alg = 6 * W * n  # column pass + SkewTranspose + bucket pass, read + write
-    # Dominant kernel role and its roofline.  HBM-bound roles: algorithmic bytes per
-    # launch / mean launch duration.  Sort roles are bound by integer ALU issue: their
-    # work is key comparisons (n*log2(m) per level pass: m-key columns, and the
-    # bucket sizes' sum n_i log n_i <= n log sqrt(n) + 4e n), each a
-    # compare + select on the ALU pipe: peak = SMs * 64 ALU lanes/clk * clock / 2.
+    # Roofline of the dominant role: every pass of the level is bound by
+    # HBM bandwidth in the model -- its algorithmic bytes are one read and one write of
+    # the n keys (2*w*n) -- so `achieved` = 2*w*n / the role's device time per step and
+    # `frac` = achieved / the measured copy bandwidth.  The bucket phase is timed as one
+    # span (its size classes and the merge passes of big buckets run concurrently on
+    # side streams); its ncu traffic includes the merge passes.  The on-chip sorts'
+    # ALU view (comparisons/s) is kept beside it.
     m = int(math.isqrt(n - 1)) + 1
     comps = n * math.log2(m)
     alu_peak = 148 * 64 * sm_mhz_max * 1e6 / 2 / 1e12  # T comparisons/s
-    hbm_roles = {"transpose": 2 * W * n, "count": W * n}
-    alu_roles = {"colsort": comps, "bucketsort": comps, "smallsort": n * math.log2(max(n, 2)),
-                 "clustersort": comps}
-    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
-    dname, (dlaunch, dms) = dom
-    per_step_launch = dlaunch / args.steps
-    traffic = None
+    role_bytes = {"colsort": 2 * W * n, "transpose": 2 * W * n, "bucketsort": 2 * W * n,
+                  "smallsort": 2 * W * n, "count": W * n}
+    per_step = {k: (v[0] / args.steps, v[1] / args.steps) for k, v in prof.items()}  # role -> (launches, ms)
+    cand = {k: v for k, v in per_step.items() if k in role_bytes}
+    dname, (dlaunch, dms) = max(cand.items(), key=lambda kv: kv[1][1]) if cand else ("none", (1.0, 0.0))
+    traffic_step = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            traffic = tj["bytes_per_launch"].get(dname)
-            # the library may time a role as one span over several kernel launches
-            # (concurrent bucket-sort classes): traffic per timed unit, like `achieved`
-            lpc = tj.get("launches_per_call", {}).get(dname)
-            if traffic is not None and lpc and per_step_launch:
-                traffic = traffic * lpc / per_step_launch
+            bpl, lpc = tj["bytes_per_launch"], tj.get("launches_per_call", {})
+            parts = [dname] + (["merge"] if dname == "bucketsort" else [])
+            traffic_step = sum(bpl[r] * lpc.get(r, 1) for r in parts if r in bpl) or None
         except Exception:
-            traffic = None
-    mean_launch_s = dms / dlaunch / 1e3 if dlaunch else 0.0
-    if dname in alu_roles:
-        work = alu_roles[dname] / max(per_step_launch, 1)
-        achieved = work / mean_launch_s / 1e12 if mean_launch_s else 0.0
-        hbm_view = 2 * W * n / max(per_step_launch, 1) / mean_launch_s / 1e9 if mean_launch_s else 0.0
-        roofline = {"bound": "alu", "kernel": dname, "achieved": achieved, "peak": alu_peak,
-                    "unit": "T comparisons/s", "frac": achieved / alu_peak, "traffic": traffic,
-                    "peak_source": f"derived: 148 SMs x 64 ALU lanes/clk x {sm_mhz_max:.0f} MHz / 2 ops "
-                                   "per comparison (DESIGN.md 8)",
-                    "algorithmic_work_per_launch": work, "launches_per_step": per_step_launch,
-                    "share_of_step": dms / total_ms if total_ms > 0 else None,
-                    "hbm_view": {"achieved_gbs": hbm_view, "frac_of_measured": hbm_view / hbm}}
-    else:
-        bytes_per_launch = hbm_roles.get(dname, 0) / max(per_step_launch, 1)
-        achieved = bytes_per_launch / mean_launch_s / 1e9 if mean_launch_s else 0.0
-        roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-                    "algorithmic_bytes_per_launch": bytes_per_launch, "launches_per_step": per_step_launch,
-                    "share_of_step": dms / total_ms if total_ms > 0 else None}
+            traffic_step = None
+    sec = dms / 1e3
+    achieved = role_bytes.get(dname, 0) / sec / 1e9 if sec else 0.0
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic_step, "peak_source": hbm_src,
+                "algorithmic_bytes_per_launch": role_bytes.get(dname, 0),
+                "launch": "one timed unit per step (the bucket phase: one fork-to-join span)",
+                "launches_per_step": 1, "share_of_step": dms / ms if ms > 0 else None,
+                "traffic_note": "ncu dram__bytes_read+write summed over the role's kernels per sort call "
+                                "(profiles/ncu_traffic.json; bucket phase incl. merge passes)",
+                "alu_view": {"work": "n*log2(m) comparisons", "achieved_tcomp_s": comps / sec / 1e12 if sec else 0.0,
+                             "peak_tcomp_s": alu_peak,
+                             "frac": (comps / sec / 1e12) / alu_peak if sec else 0.0,
+                             "peak_source": f"derived: 148 SMs x 64 ALU lanes/clk x {sm_mhz_max:.0f} MHz / 2"}}
+    roles = {k: {"ms": v[1], "hbm_frac": role_bytes[k] / (v[1] / 1e3) / 1e9 / hbm}
+             for k, v in per_step.items() if k in role_bytes and v[1] > 0}
     step_gbs = b_alg / (ms / 1e3) / 1e9
 
     out = {
@@ -326,6 +320,8 @@ def main():
         "hbm_roofline_step": {"b_alg_bytes": b_alg, "achieved_gbs": step_gbs,
                               "frac_of_8TBs": step_gbs / NOMINAL_HBM_GBS, "frac_of_measured": step_gbs / hbm},
         "roofline": roofline,
+        "roles_hbm_frac_of_measured": roles,
+        "ms_per_step_median": statistics.median(step_ms), "ms_per_step_min": min(step_ms),
         "kernels_ms_per_step": {k: v[1] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "kernel_timing": "library per-launch CUDA events (on the sort's stream) over a second pass of the same K steps "
                          "run right after the timed steps (events inside the timed steps would add ~2 % of API overhead)",

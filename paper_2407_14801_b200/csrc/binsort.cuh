@@ -59,6 +59,7 @@ struct BinSort {
   __device__ __forceinline__ static void bin_op(uint32_t* s, uint32_t* cnt, uint32_t x, uint32_t b) {
     if constexpr (SCATTER) {
       const uint32_t d = atomicAdd(&cnt[b], 1u);
+      SQ_CHECK(d < uint32_t(TILE) && b < uint32_t(NB));
       s[pad(d)] = x;
     } else {
       atomicAdd(&cnt[b], 1u);

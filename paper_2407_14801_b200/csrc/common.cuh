@@ -11,6 +11,25 @@
 
 namespace sq {
 
+// Device-side consistency checks for debug builds (-DSQ_DEBUG_CHECKS, e.g.
+// SQ_NVCC_EXTRA=-DSQ_DEBUG_CHECKS python -m paper_2407_14801_b200.build --force):
+// an index outside the range its producer promised traps the kernel.  This is
+// the memory check of this pool (compute-sanitizer is closed).
+#ifdef SQ_DEBUG_CHECKS
+#define SQ_CHECK(cond)                                                                        \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("SQ_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                              \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define SQ_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- RNG (L10)
 // mix = SplitMix64's output function applied to z + golden-ratio increment.
 __host__ __device__ __forceinline__ uint64_t mix(uint64_t z) {

@@ -872,6 +872,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     for (int i = threadIdx.x + len; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
     gather_bucket<NT>(ti, lane0, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        SQ_CHECK(d + l <= uint32_t(BS::TILE) && o >= ti.out && o + l <= ti.out + ti.size);
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
                             // key into the low half of the composite slot, fixed up below
@@ -892,6 +893,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
       }
       __syncthreads();
     }
+    SQ_CHECK(len <= uint32_t(BS::TILE));
     tile_sort<K, NT, V, PAIRS, BIN>(s, cnt, len);
     for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
@@ -1088,6 +1090,7 @@ k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items
         }
     }
     __syncthreads();
+    SQ_CHECK(a0 + d0 + m <= rc.size && m <= uint32_t(TM));
     for (uint32_t i = threadIdx.x; i < m; i += NT) {
       dst[rc.out + a0 + d0 + i] = sk[BS::pad(i)];
       if (PAIRS) vdst[rc.out + a0 + d0 + i] = sv[i];
@@ -1111,6 +1114,7 @@ k_bucket_gather(const BucketRec* __restrict__ recs, const TileInfo* __restrict__
     const TileInfo ti = tiles[rc.tile];
     gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, 0u, rc.size,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        SQ_CHECK(d + l <= rc.size && o >= ti.out && o + l <= ti.out + ti.size);
                         for (uint32_t q = ln; q < l; q += 32) {
                           dst[rc.out + d + q] = src[o + q];
                           if (vsrc) vdst[rc.out + d + q] = vsrc[o + q];
@@ -1164,6 +1168,7 @@ k_bucket_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __rest
     uint32_t* vout = vdst ? vdst + rc.out + lo : nullptr;
     gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
+                        SQ_CHECK(lo + d + l <= rc.size && o >= ti.out && o + l <= ti.out + ti.size);
                         uint32_t q = ln;
                         for (; q + 96 < l; q += 128) {  // four independent loads in flight per lane
                           const K x0 = src[o + q], x1 = src[o + q + 32], x2 = src[o + q + 64], x3 = src[o + q + 96];

@@ -370,6 +370,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
       const uint32_t bk = c & 63;
       if (bk < 32) {
         const uint32_t dpos = cnt[bk * NC + tsw] + (c >> 6);
+        SQ_CHECK(dpos < Pn);
         outb[dpos] = xs[j];
         if (PAIRS) vout[dpos] = vslot[w0 + j];
       }
