@@ -74,6 +74,11 @@ int sq_sort_u64(uint64_t *keys, size_t n, uint64_t seed, void *stream);
  * keys and vals must not overlap. */
 int sq_sort_pairs_u32_u32(uint32_t *keys, uint32_t *vals, size_t n, uint64_t seed, void *stream);
 
+/* Sort n (u64 key, u32 value) pairs by key, stably (the paper's external-sort
+ * workload is 64-bit integers); n <= 2^28.  keys and vals must not
+ * overlap.  On chip the sorts order (key << 32 | position) 128-bit composites. */
+int sq_sort_pairs_u64_u32(uint64_t *keys, uint32_t *vals, size_t n, uint64_t seed, void *stream);
+
 /* Signed and IEEE-754 keys (the paper's workloads are signed
  * integers): an order-preserving bit map onto unsigned keys of the
  * same width (signed: flip the sign bit; float/double: flip all bits of a
@@ -91,6 +96,7 @@ int sq_sort_f64(double *keys, size_t n, uint64_t seed, void *stream);
  * synchronize.  The end-to-end path the bench's `e2e` figure measures. */
 int sq_sort_u32_host(uint32_t *keys, size_t n, uint64_t seed, void *stream);
 int sq_sort_u64_host(uint64_t *keys, size_t n, uint64_t seed, void *stream);
+int sq_sort_pairs_u64_u32_host(uint64_t *keys, uint32_t *vals, size_t n, uint64_t seed, void *stream);
 int sq_sort_pairs_u32_u32_host(uint32_t *keys, uint32_t *vals, size_t n, uint64_t seed,
                                void *stream);
 

@@ -25,7 +25,8 @@ EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_h
            "sq_sort_u64_host_batch", "sq_skew_transpose",
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode",
-           "sq_trim_memory", "sq_set_base_case", "sq_debug_level_u64"]
+           "sq_trim_memory", "sq_set_base_case", "sq_debug_level_u64", "sq_sort_pairs_u64_u32",
+           "sq_sort_pairs_u64_u32_host"]
 
 
 class SqError(RuntimeError):
@@ -63,7 +64,8 @@ def lib():
                   "sq_sort_i64", "sq_sort_f32", "sq_sort_f64"):
             getattr(L, f).argtypes = [vp, sz, u64, vp]
             getattr(L, f).restype = ctypes.c_int
-        for f in ("sq_sort_pairs_u32_u32", "sq_sort_pairs_u32_u32_host"):
+        for f in ("sq_sort_pairs_u32_u32", "sq_sort_pairs_u32_u32_host", "sq_sort_pairs_u64_u32",
+                  "sq_sort_pairs_u64_u32_host"):
             getattr(L, f).argtypes = [vp, vp, sz, u64, vp]
             getattr(L, f).restype = ctypes.c_int
         for f in ("sq_sort_u32_host_batch", "sq_sort_u64_host_batch"):
@@ -185,6 +187,16 @@ def sort_pairs_u32_u32(keys, vals, seed: int = 0, stream=None):
     return keys, vals
 
 
+def sort_pairs_u64_u32(keys, vals, seed: int = 0, stream=None):
+    """Stable sort of (torch.uint64 keys, torch.uint32 vals) CUDA tensors by key, in place."""
+    if vals.numel() != keys.numel():
+        raise ValueError("keys and vals differ in length")
+    with _on(keys):
+        _check(lib().sq_sort_pairs_u64_u32(_dev(keys, "torch.uint64"), _dev(vals, "torch.uint32", keys.device),
+                                           keys.numel(), _seed(seed), _stream(stream)))
+    return keys, vals
+
+
 def skew_transpose(src, dst, rows: int, cols: int, pivots=None, k: int | None = None,
                    n: int = 0, buc_in=None, buc_out=None, naive_threshold: int = 4,
                    flags: int = 0, stream=None):
@@ -242,6 +254,13 @@ def sort_u64_host(keys, seed: int = 0, stream=None):
 def sort_pairs_u32_u32_host(keys, vals, seed: int = 0, stream=None):
     import numpy as np
     _check(lib().sq_sort_pairs_u32_u32_host(_host_ptr(keys, np.uint32), _host_ptr(vals, np.uint32),
+                                            keys.size, _seed(seed), _stream(stream)))
+    return keys, vals
+
+
+def sort_pairs_u64_u32_host(keys, vals, seed: int = 0, stream=None):
+    import numpy as np
+    _check(lib().sq_sort_pairs_u64_u32_host(_host_ptr(keys, np.uint64), _host_ptr(vals, np.uint32),
                                             keys.size, _seed(seed), _stream(stream)))
     return keys, vals
 

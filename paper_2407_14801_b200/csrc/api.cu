@@ -20,6 +20,12 @@ int sq_sort_u64(uint64_t* keys, size_t n, uint64_t seed, void* stream) {
 int sq_sort_pairs_u32_u32(uint32_t* keys, uint32_t* vals, size_t n, uint64_t seed, void* stream) {
   return sort_entry<uint32_t, true>(keys, vals, n, seed, stream, false);
 }
+int sq_sort_pairs_u64_u32(uint64_t* keys, uint32_t* vals, size_t n, uint64_t seed, void* stream) {
+  return sort_entry<uint64_t, true>(keys, vals, n, seed, stream, false);
+}
+int sq_sort_pairs_u64_u32_host(uint64_t* keys, uint32_t* vals, size_t n, uint64_t seed, void* stream) {
+  return sort_entry<uint64_t, true>(keys, vals, n, seed, stream, true);
+}
 int sq_sort_u32_host(uint32_t* keys, size_t n, uint64_t seed, void* stream) {
   return sort_entry<uint32_t, false>(keys, nullptr, n, seed, stream, true);
 }

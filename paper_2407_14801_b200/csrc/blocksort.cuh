@@ -121,7 +121,7 @@ __device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
   {
     K p[V];
 #pragma unroll
-    for (int i = 0; i < V; i++) p[i] = __shfl_xor_sync(0xffffffffu, r[V - 1 - i], G - 1);
+    for (int i = 0; i < V; i++) p[i] = shfl_xor_k(r[V - 1 - i], G - 1);
 #pragma unroll
     for (int i = 0; i < V; i++) r[i] = dir_minmax<K>(false, r[i], p[i], upper, upper ? 1u : 0u, one, mtwo);
   }
@@ -131,7 +131,7 @@ __device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
     const uint32_t u = hi ? 1u : 0u;
 #pragma unroll
     for (int i = 0; i < V; i++) {
-      const K q = __shfl_xor_sync(0xffffffffu, r[i], d);
+      const K q = shfl_xor_k(r[i], d);
       r[i] = dir_minmax<K>(false, r[i], q, hi, u, one, mtwo);
     }
   }
@@ -148,7 +148,7 @@ struct BlockSort {
   static constexpr int V = V_;
   static constexpr int TILE = NT * V;
   static constexpr int PER = 128 / sizeof(K);  // elements per 128-byte pad period
-  static constexpr int PSH = sizeof(K) == 4 ? 5 : 4;
+  static constexpr int PSH = sizeof(K) == 4 ? 5 : (sizeof(K) == 8 ? 4 : 3);
   static constexpr int SMEM_ELEMS = TILE + TILE / PER + 1;
   static constexpr size_t SMEM_BYTES = size_t(SMEM_ELEMS) * sizeof(K);
 
@@ -315,21 +315,22 @@ k_blocksort(const SegDesc* __restrict__ segs, const K* __restrict__ src, K* __re
   for (int i = threadIdx.x; i < (int)d.len; i += NT) out[i] = s[BS::pad(i)];
 }
 
-// Pairs batched sort (u32 keys, u32 payload), stable: composites key<<32 | pos.
-template <int NT, int V>
+// Pairs batched sort (u32 or u64 keys, u32 payload), stable: composites key<<32 | pos.
+template <typename K, int NT, int V>
 __global__ void __launch_bounds__(NT)
-k_blocksort_pairs(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ ksrc,
-                  const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ kdst,
+k_blocksort_pairs(const SegDesc* __restrict__ segs, const K* __restrict__ ksrc,
+                  const uint32_t* __restrict__ vsrc, K* __restrict__ kdst,
                   uint32_t* __restrict__ vdst) {
-  using BS = BlockSort<uint64_t, NT, V>;
+  using SK = sortkey_t<K, true>;
+  using BS = BlockSort<SK, NT, V>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* s = reinterpret_cast<uint64_t*>(smem_raw);
+  SK* s = reinterpret_cast<SK*>(smem_raw);
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
   const SegDesc d = segs[blockIdx.x];
   for (int i = threadIdx.x; i < BS::TILE; i += NT) {
-    uint64_t c = KeyTraits<uint64_t>::kMax;
+    SK c = KeyTraits<SK>::kMax;
     if (i < (int)d.len) {
-      c = (uint64_t(ksrc[d.off + i]) << 32) | uint32_t(i);
+      c = (SK(ksrc[d.off + i]) << 32) | SK(uint32_t(i));
       vs[i] = vsrc[d.off + i];
     }
     s[BS::pad(i)] = c;
@@ -337,8 +338,8 @@ k_blocksort_pairs(const SegDesc* __restrict__ segs, const uint32_t* __restrict__
   __syncthreads();
   BS::sort_smem(s, d.len);
   for (int i = threadIdx.x; i < (int)d.len; i += NT) {
-    uint64_t c = s[BS::pad(i)];
-    kdst[d.off + i] = uint32_t(c >> 32);
+    const SK c = s[BS::pad(i)];
+    kdst[d.off + i] = K(c >> 32);
     vdst[d.off + i] = vs[uint32_t(c)];
   }
 }

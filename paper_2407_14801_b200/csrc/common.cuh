@@ -65,6 +65,29 @@ template <> struct KeyTraits<uint32_t> {
 template <> struct KeyTraits<uint64_t> {
   static constexpr uint64_t kMax = 0xffffffffffffffffull;
 };
+typedef unsigned __int128 u128;
+template <> struct KeyTraits<u128> {
+  static constexpr u128 kMax = ~u128(0);
+};
+
+// The on-chip sort key: the key itself, or for pairs the stable composite
+// (key << 32 | position in the tile), L16: 64-bit for u32 keys, 128-bit for u64 keys.
+template <typename K, bool PAIRS> struct SortKey { using type = K; };
+template <> struct SortKey<uint32_t, true> { using type = uint64_t; };
+template <> struct SortKey<uint64_t, true> { using type = u128; };
+template <typename K, bool PAIRS> using sortkey_t = typename SortKey<K, PAIRS>::type;
+
+// __shfl_xor_sync for 4-, 8- and 16-byte keys
+template <typename K>
+__device__ __forceinline__ K shfl_xor_k(K v, int m) {
+  if constexpr (sizeof(K) == 16) {
+    const uint64_t lo = __shfl_xor_sync(0xffffffffu, uint64_t(v), m);
+    const uint64_t hi = __shfl_xor_sync(0xffffffffu, uint64_t(v >> 64), m);
+    return (K(hi) << 64) | K(lo);
+  } else {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+  }
+}
 
 // ---------------------------------------------------------------- bucket membership
 // Boundary j (1 <= j <= k-1) separates bucket j-1 from bucket j.  A key x lies

@@ -335,7 +335,9 @@ struct Arena {
 // 64-bit sort keys (u64 keys, pair composites).
 inline constexpr uint32_t kTiles[] = {64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 12288, 16384, 24576, 32768};
 
-template <typename SK> constexpr uint32_t key_max_tile() { return sizeof(SK) == 4 ? 32768u : 16384u; }
+template <typename SK> constexpr uint32_t key_max_tile() {
+  return sizeof(SK) == 4 ? 32768u : (sizeof(SK) == 8 ? 16384u : 8192u);
+}
 
 inline uint32_t tile_for(uint32_t len) {
   for (uint32_t t : kTiles)
@@ -395,6 +397,19 @@ void with_tile(uint32_t tile, F&& f) {
       case 16384: return f(IC<512>{}, IC<32>{});
       case 24576: return f(IC<768>{}, IC<32>{});
       case 32768: return f(IC<1024>{}, IC<32>{});
+    }
+  } else if constexpr (sizeof(SK) == 16) {  // u64-key pair composites: 8 keys (32 registers) per thread
+    switch (tile) {
+      case 64: return f(IC<32>{}, IC<2>{});
+      case 128: return f(IC<32>{}, IC<4>{});
+      case 256: return f(IC<32>{}, IC<8>{});
+      case 512: return f(IC<64>{}, IC<8>{});
+      case 1024: return f(IC<128>{}, IC<8>{});
+      case 2048: return f(IC<256>{}, IC<8>{});
+      case 3072: return f(IC<384>{}, IC<8>{});
+      case 4096: return f(IC<512>{}, IC<8>{});
+      case 6144: return f(IC<768>{}, IC<8>{});
+      case 8192: return f(IC<1024>{}, IC<8>{});
     }
   } else {
     switch (tile) {
@@ -459,6 +474,7 @@ template <typename K, bool PAIRS> struct PmTr;
 template <> struct PmTr<uint32_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
 template <> struct PmTr<uint32_t, true> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
 template <> struct PmTr<uint64_t, false> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
+template <> struct PmTr<uint64_t, true> { static constexpr int NT = 256, S = 4096, F = 128, XNT = 256; };
 
 // cluster bucket sort: per-CTA tile (threads x keys) for 32-bit / 64-bit sort keys
 // (small per-CTA tiles keep 3 CTAs per SM resident; the big one serves the
@@ -473,7 +489,9 @@ template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16,
 // (the counting-sort base case sorts up to 32K 32-bit keys per CTA at full rate;
 // SQ_ONE_CAP overrides it for experiments)
 inline uint32_t g_one_cap = getenv("SQ_ONE_CAP") ? (uint32_t)atoi(getenv("SQ_ONE_CAP")) : 32768u;
-template <typename SK> uint32_t single_cap() { return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : 8192u; }
+template <typename SK> uint32_t single_cap() {
+  return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : (sizeof(SK) == 8 ? 8192u : 4096u);
+}
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
 template <typename K, bool PAIRS> struct MergeCfg {
@@ -565,7 +583,7 @@ struct DebugOut {  // sq_debug_level_u32 / _u64
 // compiled in its own translation unit (inst_*.cu).
 template <typename K, bool PAIRS, bool BIN = false>
 struct Engine {
-  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;  // on-chip sort key
+  using SK = sortkey_t<K, PAIRS>;  // on-chip sort key
   cudaStream_t st;
   Arena& ar;
   K* kb[3];        // [0] caller's buffer, [1] scratch, [2] merge-sort scratch
@@ -610,8 +628,8 @@ struct Engine {
       ProfScope ps(role, st);
       if constexpr (PAIRS) {
         const size_t smem = BS::SMEM_BYTES + size_t(BS::TILE) * 4;
-        set_smem(k_blocksort_pairs<NT, V>, smem);
-        k_blocksort_pairs<NT, V><<<nseg, NT, smem, st>>>(dd, kb[src], vb[src], kb[dst], vb[dst]);
+        set_smem(k_blocksort_pairs<K, NT, V>, smem);
+        k_blocksort_pairs<K, NT, V><<<nseg, NT, smem, st>>>(dd, kb[src], vb[src], kb[dst], vb[dst]);
       } else {
         set_smem(k_blocksort<K, NT, V>, BS::SMEM_BYTES);
         k_blocksort<K, NT, V><<<nseg, NT, BS::SMEM_BYTES, st>>>(dd, kb[src], kb[dst]);
@@ -680,12 +698,16 @@ struct Engine {
   void launch_cluster(int cl, cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
                       const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
                       uint32_t nbuck) {
+    if constexpr (sizeof(SK) == 16) {
+      throw Error(SQ_ERR_CUDA, "cluster bucket sort is not built for u64 pairs");
+    } else {
     using CS = ClusterCfg<SK>;
     using CB = ClusterBig<SK>;
     if (cl == 4) launch_cluster_t<4, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
     else if (cl == 8) launch_cluster_t<8, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
     else if (cl == 16) launch_cluster_t<16, CS>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
     else launch_cluster_t<16, CB>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, nbuck);
+    }
   }
 
   // One SquareSort level (Alg 1) for a batch of segments that live in buffer X,
@@ -895,7 +917,7 @@ struct Engine {
       for (uint32_t t : kTiles)
         if (t >= lower && t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
       po.max_tile = one;
-      if (g_big_mode == 2) {  // buckets beyond one CTA: thread-block clusters of 4, 8, 16 CTAs
+      if constexpr (sizeof(SK) <= 8) if (g_big_mode == 2) {  // beyond one CTA: clusters of 4, 8, 16 CTAs
         const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
         for (int cl : {4, 8, 16}) {
           if (cl * ct <= po.max_tile) continue;
@@ -921,7 +943,9 @@ struct Engine {
       if (!cls_cl[c]) po.unit_max = std::max(po.unit_max, po.cls_tile[c]);
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
-    if (g_big_mode == 1) {  // multi-CTA merge sort for buckets of up to 16 chunks
+    // (u64 pairs have no cluster kernel: mode 2 runs the merge base case for them)
+    const bool merge = g_big_mode == 1 || (g_big_mode == 2 && sizeof(SK) == 16);
+    if (merge) {  // multi-CTA merge sort for buckets of up to 16 chunks
       po.msort_max = 16u * po.max_tile;
       po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
       ensure_third();
@@ -967,7 +991,6 @@ struct Engine {
     // the caller's stream (fork to join); serial classes are timed per launch
     std::optional<ProfScope> span;
     if (g_concurrent_classes) span.emplace("bucketsort", st);
-    const bool merge = g_big_mode == 1;
     // allocated on st before the fork, released on st after the join
     uint32_t* splits = merge ? (uint32_t*)ar.alloc(uint64_t(po.mcap) * 4) : nullptr;
     ForkJoin fj(st, ss);
@@ -1145,6 +1168,7 @@ void debug_level_engine(const K* src, K* dst, size_t n, uint64_t seed, K* pivots
   X template void sort_engine<uint32_t, false, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint64_t, false, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint32_t, true, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void sort_engine<uint64_t, true, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void debug_level_engine<uint32_t, true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*,   \
                                                      uint32_t*, uint32_t*, cudaStream_t);                     \
   X template void debug_level_engine<uint32_t, false>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*,  \

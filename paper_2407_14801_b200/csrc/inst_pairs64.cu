@@ -1,0 +1,7 @@
+// inst_pairs64.cu -- explicit instantiation of the SquareSort engine for uint64_t keys
+// with uint32_t values (its own translation unit, so the library builds in parallel).
+#include "engine.cuh"
+
+namespace sq {
+template void sort_engine<uint64_t, true, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t);
+}  // namespace sq

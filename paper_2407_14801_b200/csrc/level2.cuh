@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<K, NT, V, PAIRS, BIN>()))
 k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K* __restrict__ keys,
           uint32_t* __restrict__ vals, const K* __restrict__ piv, uint32_t* __restrict__ segmat,
           K* __restrict__ segmin) {
-  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using SK = sortkey_t<K, PAIRS>;
   using BS = BlockSort<SK, NT, V, 32>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SK* s = reinterpret_cast<SK*>(smem_raw);
@@ -232,7 +232,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
         SK x = KeyTraits<SK>::kMax;
         if (i < (int)d.len) {
           if constexpr (PAIRS) {
-            x = (uint64_t(keys[d.off + i]) << 32) | uint32_t(i);
+            x = (SK(keys[d.off + i]) << 32) | SK(uint32_t(i));
             vs[i] = vals[d.off + i];
           } else {
             x = keys[d.off + i];
@@ -254,7 +254,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   for (int i = threadIdx.x; i < (int)d.len; i += NT) {
     const SK x = s[BS::pad(i)];
     if constexpr (PAIRS) {
-      keys[d.off + i] = uint32_t(x >> 32);
+      keys[d.off + i] = K(x >> 32);
       vals[d.off + i] = vs[uint32_t(x)];
     } else {
       keys[d.off + i] = x;
@@ -832,7 +832,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
              const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst, const uint32_t* __restrict__ pout,
              const uint16_t* __restrict__ ppre, K* __restrict__ dst_odd, uint32_t* __restrict__ vdst_odd,
              const Unit* __restrict__ units) {
-  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using SK = sortkey_t<K, PAIRS>;
   using BS = BlockSort<SK, NT, V>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SK* s = reinterpret_cast<SK*>(smem_raw);
@@ -876,7 +876,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
                             // key into the low half of the composite slot, fixed up below
-                            cp_async_elem(reinterpret_cast<uint32_t*>(&s[BS::pad(d + q)]), &src[o + q]);
+                            cp_async_elem(reinterpret_cast<K*>(&s[BS::pad(d + q)]), &src[o + q]);
                             cp_async_elem(&vs[d + q], &vsrc[o + q]);
                           } else {
                             cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
@@ -888,8 +888,8 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     __syncthreads();
     if constexpr (PAIRS) {  // composite = key << 32 | position (stable order)
       for (int i = threadIdx.x; i < (int)len; i += NT) {
-        const uint32_t key = *reinterpret_cast<uint32_t*>(&s[BS::pad(i)]);
-        s[BS::pad(i)] = (uint64_t(key) << 32) | uint32_t(i);
+        const K key = *reinterpret_cast<K*>(&s[BS::pad(i)]);
+        s[BS::pad(i)] = (SK(key) << 32) | SK(uint32_t(i));
       }
       __syncthreads();
     }
@@ -898,7 +898,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     for (int i = threadIdx.x; i < (int)len; i += NT) {
       const SK x = s[BS::pad(i)];
       if constexpr (PAIRS) {
-        out[outpos + lo + i] = uint32_t(x >> 32);
+        out[outpos + lo + i] = K(x >> 32);
         vout[outpos + lo + i] = vs[uint32_t(x)];
       } else {
         out[outpos + lo + i] = x;
@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(NT, PAIRS ? 1 : (sizeof(K) == 8 ? 512 : 1024) 
 k_merge_pass(const BucketRec* __restrict__ recs, const MTile* __restrict__ items, const uint32_t* __restrict__ count,
              uint32_t pass, K* __restrict__ bufX, K* __restrict__ bufU, uint32_t* __restrict__ vX,
              uint32_t* __restrict__ vU, const uint32_t* __restrict__ splits) {
-  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using SK = sortkey_t<K, PAIRS>;
   constexpr int TM = NT * VM;
   using BS = BlockSort<K, NT, VM>;  // padding helper only
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1238,7 +1238,7 @@ k_clustersort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ t
               K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
               const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
   namespace cg = cooperative_groups;
-  using SK = typename std::conditional<PAIRS, uint64_t, K>::type;
+  using SK = sortkey_t<K, PAIRS>;
   using BS = BlockSort<SK, NT, V>;
   constexpr int PER = BS::PER;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1275,7 +1275,7 @@ k_clustersort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ t
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
-                            bufA[BS::pad(d + q)] = (uint64_t(src[o + q]) << 32) | (lo + d + q);
+                            bufA[BS::pad(d + q)] = (SK(src[o + q]) << 32) | SK(lo + d + q);
                             vs[d + q] = vsrc[o + q];
                           } else {
                             cp_async_elem(&bufA[BS::pad(d + q)], &src[o + q]);
@@ -1345,7 +1345,7 @@ k_clustersort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ t
           if (d0 + k < mlen) {
             if constexpr (PAIRS) {
               const uint32_t src_pos = uint32_t(r[k]);  // position in the bucket's gathered order
-              dst[rc.out + pos] = uint32_t(r[k] >> 32);
+              dst[rc.out + pos] = K(r[k] >> 32);
               vdst[rc.out + pos] = partsV[src_pos / chunk][src_pos % chunk];
             } else {
               dst[rc.out + pos] = r[k];

@@ -115,6 +115,41 @@ def test_cfg5p_pairs_full_size():
     assert np.array_equal(gv, inv)
 
 
+@pytest.mark.parametrize("n,card", [(1 << 18, 2**64), (200003, 1000), (70000, 3), (1 << 20, 2**40)])
+def test_pairs_u64_vs_oracle(n, card):
+    """u64 keys with a u32 payload (f1; P:1048's 64-bit workload): stable, against the oracle."""
+    rng = np.random.default_rng(n ^ 77)
+    if card == 2**64:
+        keys = rng.integers(0, 2**63, n, dtype=np.uint64) * 2 + rng.integers(0, 2, n, dtype=np.uint64)
+    else:
+        keys = rng.integers(0, card, n, dtype=np.uint64)
+    vals = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    want_k, want_v = O.square_sort(keys, vals, seed=3)[:2]
+    k, v = to_dev(keys), to_dev(vals)
+    sq.sort_pairs_u64_u32(k, v, 3)
+    assert np.array_equal(to_host(k), want_k) and np.array_equal(to_host(v), want_v)
+    ek, ev = CF.stable_pairs_sort(keys, vals)
+    assert np.array_equal(want_k, ek) and np.array_equal(want_v, ev)
+
+
+def test_pairs_u64_modes_and_host():
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 5000, 300001, dtype=np.uint64) << np.uint64(33)
+    vals = np.arange(len(keys), dtype=np.uint32)
+    ek, ev = CF.stable_pairs_sort(keys, vals)
+    for mode in (sq.BIG_LEVEL, sq.BIG_MERGE, sq.BIG_CLUSTER):
+        sq.set_max_tile(1024)
+        sq.set_big_bucket_mode(mode)
+        k, v = to_dev(keys), to_dev(vals)
+        sq.sort_pairs_u64_u32(k, v, 1)
+        assert np.array_equal(to_host(k), ek) and np.array_equal(to_host(v), ev), mode
+    sq.set_max_tile(0)
+    sq.set_big_bucket_mode(sq.BIG_MERGE)
+    hk, hv = keys.copy(), vals.copy()
+    sq.sort_pairs_u64_u32_host(hk, hv, 2)
+    assert np.array_equal(hk, ek) and np.array_equal(hv, ev)
+
+
 def test_pairs_scaled_vs_oracle():
     keys, vals = S.config("cfg5p", n=1 << 18)
     want_k, want_v = oracle_sort(keys, 5, vals)
