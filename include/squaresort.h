@@ -163,6 +163,22 @@ typedef struct {
 int sq_skew_transpose(const uint32_t *src, uint32_t *dst, size_t rows, size_t cols,
                       const sq_skew_params *params, void *stream);
 
+/* The same for 64-bit keys (the paper's external-sort workload): the
+ * pivots are u64; cursors, sizes and every rule as above.  The call blocks the
+ * host once, at its end (twice with SQ_FLAG_VALIDATE); the cursors are scanned
+ * and checked on the device. */
+typedef struct {
+  const uint64_t *pivots;   /* device, k-1 non-decreasing u64 pivots (NULL when k = 1) */
+  uint32_t k;
+  uint64_t n;
+  const uint32_t *buc_in;
+  uint32_t *buc_out;
+  uint32_t naive_threshold;
+  uint32_t flags;
+} sq_skew_params_u64;
+int sq_skew_transpose_u64(const uint64_t *src, uint64_t *dst, size_t rows, size_t cols,
+                          const sq_skew_params_u64 *params, void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* Introspection and test hooks.                                             */
 /* ------------------------------------------------------------------------- */

@@ -26,7 +26,7 @@ EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_h
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode",
            "sq_trim_memory", "sq_set_base_case", "sq_debug_level_u64", "sq_sort_pairs_u64_u32",
-           "sq_sort_pairs_u64_u32_host"]
+           "sq_sort_pairs_u64_u32_host", "sq_skew_transpose_u64"]
 
 
 class SqError(RuntimeError):
@@ -36,6 +36,12 @@ class SqError(RuntimeError):
 
 
 class SkewParams(ctypes.Structure):
+    _fields_ = [("pivots", ctypes.c_void_p), ("k", ctypes.c_uint32), ("n", ctypes.c_uint64),
+                ("buc_in", ctypes.c_void_p), ("buc_out", ctypes.c_void_p),
+                ("naive_threshold", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
+
+
+class SkewParamsU64(ctypes.Structure):
     _fields_ = [("pivots", ctypes.c_void_p), ("k", ctypes.c_uint32), ("n", ctypes.c_uint64),
                 ("buc_in", ctypes.c_void_p), ("buc_out", ctypes.c_void_p),
                 ("naive_threshold", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
@@ -73,6 +79,8 @@ def lib():
             getattr(L, f).restype = ctypes.c_int
         L.sq_skew_transpose.argtypes = [vp, vp, sz, sz, ctypes.POINTER(SkewParams), vp]
         L.sq_skew_transpose.restype = ctypes.c_int
+        L.sq_skew_transpose_u64.argtypes = [vp, vp, sz, sz, ctypes.POINTER(SkewParamsU64), vp]
+        L.sq_skew_transpose_u64.restype = ctypes.c_int
         L.sq_status_string.argtypes = [ctypes.c_int]
         L.sq_status_string.restype = ctypes.c_char_p
         L.sq_last_error_message.argtypes = []
@@ -200,16 +208,22 @@ def sort_pairs_u64_u32(keys, vals, seed: int = 0, stream=None):
 def skew_transpose(src, dst, rows: int, cols: int, pivots=None, k: int | None = None,
                    n: int = 0, buc_in=None, buc_out=None, naive_threshold: int = 4,
                    flags: int = 0, stream=None):
-    """sq_skew_transpose on torch.uint32 CUDA tensors (all on src's device).  Returns buc_out."""
+    """sq_skew_transpose (torch.uint32) or sq_skew_transpose_u64 (torch.uint64) on CUDA
+    tensors, all on src's device.  Returns buc_out."""
     import torch
+    wide = src.dtype == torch.uint64
+    kdt = "torch.uint64" if wide else "torch.uint32"
     k = (pivots.numel() + 1 if pivots is not None else 1) if k is None else k
     dev = src.device
     with _on(src):
         if buc_out is None:
             buc_out = torch.empty(k, dtype=torch.uint32, device=dev)
-        ptr = lambda t: _dev(t, "torch.uint32", dev) if t is not None and t.numel() else None
-        p = SkewParams(ptr(pivots), k, n, ptr(buc_in), ptr(buc_out), naive_threshold, flags)
-        _check(lib().sq_skew_transpose(ptr(src), ptr(dst), rows, cols, ctypes.byref(p), _stream(stream)))
+        kptr = lambda t: _dev(t, kdt, dev) if t is not None and t.numel() else None
+        cptr = lambda t: _dev(t, "torch.uint32", dev) if t is not None and t.numel() else None
+        P = SkewParamsU64 if wide else SkewParams
+        p = P(kptr(pivots), k, n, cptr(buc_in), cptr(buc_out), naive_threshold, flags)
+        fn = lib().sq_skew_transpose_u64 if wide else lib().sq_skew_transpose
+        _check(fn(kptr(src), kptr(dst), rows, cols, ctypes.byref(p), _stream(stream)))
     return buc_out
 
 

@@ -7,6 +7,97 @@
 #include "engine.cuh"
 
 
+namespace sq {
+
+// The standalone SkewTranspose (sq_skew_transpose / _u64): count -> cursors (device
+// scan, or the caller's cursors checked on the device) -> transpose -> final cursors.
+// The host blocks once, at the end (and once after the optional validation).
+template <typename K>
+void skew_entry(const K* src, K* dst, size_t rows, size_t cols, const K* pivots, uint32_t k, uint64_t pn,
+                const uint32_t* buc_in, uint32_t* buc_out, uint32_t threshold, uint32_t flags, cudaStream_t st) {
+  need(k >= 1, "k must be >= 1");
+  need(threshold >= 2, "naive_threshold must be >= 2");
+  need(rows == 0 || cols <= SIZE_MAX / rows, "rows*cols overflows");
+  const size_t cap = rows * cols;
+  const size_t n = pn ? pn : cap;
+  need(n <= cap, "n > rows*cols");
+  need(n < (size_t(1) << 32), "n must be < 2^32");
+  need(k == 1 || pivots != nullptr, "pivots is NULL");
+  need(buc_out != nullptr, "buc_out is NULL");
+  need(cols <= 0xffffffffu && rows <= 0xffffffffu, "rows/cols too large");
+  if (n > 0) {
+    need(src != nullptr && dst != nullptr, "src/dst is NULL");
+    need(!overlap(src, n * sizeof(K), dst, n * sizeof(K)), "src and dst overlap");
+  }
+  check_device();
+  Arena ar(st);
+  uint32_t* bad = (uint32_t*)ar.alloc(4);
+  SQ_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  if (flags & SQ_FLAG_VALIDATE) {
+    if (n > 0 || k > 2) {
+      k_validate<K><<<592, 256, 0, st>>>(src, std::max<size_t>(rows, 1), n, pivots, k - 1, bad);
+      check_launch("k_validate");
+    }
+    uint32_t hb = 0;
+    SQ_CUDA(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, st));
+    SQ_CUDA(cudaStreamSynchronize(st));
+    g_stats.host_syncs++;
+    if (hb) throw Error(SQ_ERR_PRECONDITION, hb & 1 ? "a column is not sorted" : "pivots decrease");
+  }
+  const uint32_t nbt = (k + kTB - 1) / kTB;
+  LevelSeg l{};
+  l.off = 0;
+  l.len = (uint32_t)n;
+  l.rows = (uint32_t)rows;
+  l.ncols = (uint32_t)cols;
+  l.k = k;
+  l.nbt = nbt;
+  // pivots: the user's array (k-1 entries); an empty list gets a dummy buffer
+  const K* piv = pivots;
+  if (k == 1) piv = (const K*)ar.alloc(sizeof(K));
+  uint32_t* segmat = (uint32_t*)ar.alloc(std::max<uint64_t>(uint64_t(cols) * (nbt + 1), 1) * 4);
+  uint32_t* cnt = (uint32_t*)ar.alloc(uint64_t(k) * 4);
+  uint32_t* start = (uint32_t*)ar.alloc(uint64_t(k) * 4);
+  SQ_CUDA(cudaMemsetAsync(cnt, 0, uint64_t(k) * 4, st));
+  std::vector<TaskDesc> ct, tt;
+  const uint64_t cg = std::max<uint64_t>(1, (cols + 295) / 296);
+  for (uint64_t c0 = 0; c0 < cols; c0 += cg) ct.push_back({0, (uint32_t)c0, (uint32_t)std::min<uint64_t>(cols, c0 + cg)});
+  for (uint32_t bt = 0; bt < nbt; bt++) tt.push_back({0, bt, 0});
+  const std::vector<void*> up = ar.upload_all({Arena::part(std::vector<LevelSeg>{l}), Arena::part(ct), Arena::part(tt)});
+  const LevelSeg* dL = (const LevelSeg*)up[0];
+  if (!ct.empty()) {
+    using CC = CountCfg<K>;
+    const size_t smem = CC::STAGE * sizeof(K) + CC::KSMEM * 4;
+    set_smem(k_count<K, CC::NT, CC::STAGE, CC::KSMEM>, smem);
+    ProfScope ps("count", st);
+    k_count<K, CC::NT, CC::STAGE, CC::KSMEM><<<(uint32_t)ct.size(), CC::NT, smem, st>>>(
+        dL, (const TaskDesc*)up[1], src, piv, segmat, cnt);
+    check_launch("k_count");
+  }
+  k_skew_cursors<<<1, 1024, 0, st>>>(cnt, k, n, buc_in, start, bad);
+  check_launch("k_skew_cursors");
+  if (n > 0) {
+    using TC = TrCfg<K, false>;
+    using CF = TransposeCfg<K, false, TC::NT, TC::S, TC::G>;
+    auto f = k_transpose<K, false, TC::NT, TC::S, TC::G>;
+    set_smem(f, CF::SMEM);
+    ProfScope ps("transpose", st);
+    f<<<(uint32_t)tt.size(), TC::NT, CF::SMEM, st>>>(dL, (const TaskDesc*)up[2], src, dst, nullptr, nullptr, piv,
+                                                       segmat, start, bad);
+    check_launch("k_transpose");
+  }
+  k_skew_finish<<<std::max<uint32_t>(1, std::min<uint32_t>((k + 255) / 256, 1184)), 256, 0, st>>>(start, cnt, k,
+                                                                                                  buc_out);
+  check_launch("k_skew_finish");
+  uint32_t* hb = (uint32_t*)ar.pinned(4);
+  xfer(hb, bad, 4, st);
+  SQ_CUDA(cudaStreamSynchronize(st));
+  g_stats.host_syncs++;
+  if (*hb & 4) throw Error(SQ_ERR_INVALID_ARGUMENT, "buc_in[j] + size_j exceeds n");
+}
+
+}  // namespace sq
+
 using namespace sq;
 
 extern "C" {
@@ -60,99 +151,17 @@ int sq_skew_transpose(const uint32_t* src, uint32_t* dst, size_t rows, size_t co
                       void* stream) {
   return guarded([&] {
     need(p != nullptr, "params is NULL");
-    need(p->k >= 1, "k must be >= 1");
-    need(p->naive_threshold >= 2, "naive_threshold must be >= 2");
-    need(rows == 0 || cols <= SIZE_MAX / rows, "rows*cols overflows");
-    const size_t cap = rows * cols;
-    const size_t n = p->n ? p->n : cap;
-    need(n <= cap, "n > rows*cols");
-    need(n < (size_t(1) << 32), "n must be < 2^32");
-    need(p->k == 1 || p->pivots != nullptr, "pivots is NULL");
-    need(p->buc_out != nullptr, "buc_out is NULL");
-    need(cols <= 0xffffffffu && rows <= 0xffffffffu, "rows/cols too large");
-    need(p->k - 1 <= 0xffffffffu, "k too large");
-    if (n > 0) {
-      need(src != nullptr && dst != nullptr, "src/dst is NULL");
-      need(!overlap(src, n * 4, dst, n * 4), "src and dst overlap");
-    }
-    check_device();
-    cudaStream_t st = (cudaStream_t)stream;
-    Arena ar(st);
-    if (p->flags & SQ_FLAG_VALIDATE) {
-      uint32_t* bad = (uint32_t*)ar.alloc(4);
-      SQ_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-      if (n > 0 || p->k > 2) {
-        k_validate<<<592, 256, 0, st>>>(src, std::max<size_t>(rows, 1), n, p->pivots, p->k - 1, bad);
-        check_launch("k_validate");
-      }
-      uint32_t hb = 0;
-      SQ_CUDA(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, st));
-      SQ_CUDA(cudaStreamSynchronize(st));
-      if (hb) throw Error(SQ_ERR_PRECONDITION, hb & 1 ? "a column is not sorted" : "pivots decrease");
-    }
-    const uint32_t k = p->k;
-    const uint32_t nbt = (k + kTB - 1) / kTB;
-    LevelSeg l{};
-    l.off = 0;
-    l.len = (uint32_t)n;
-    l.rows = (uint32_t)rows;
-    l.ncols = (uint32_t)cols;
-    l.k = k;
-    l.nbt = nbt;
-    LevelSeg* dL = ar.upload(std::vector<LevelSeg>{l});
-    // pivots: the user's array (k-1 entries); an empty list gets a dummy buffer
-    const uint32_t* piv = p->pivots;
-    if (k == 1) piv = (uint32_t*)ar.alloc(4);
-    uint32_t* segmat = (uint32_t*)ar.alloc(std::max<uint64_t>(uint64_t(cols) * (nbt + 1), 1) * 4);
-    uint32_t* cnt = (uint32_t*)ar.alloc(uint64_t(k) * 4);
-    SQ_CUDA(cudaMemsetAsync(cnt, 0, uint64_t(k) * 4, st));
-    std::vector<TaskDesc> ct, tt;
-    const uint64_t cg = std::max<uint64_t>(1, (cols + 295) / 296);
-    for (uint64_t c0 = 0; c0 < cols; c0 += cg) ct.push_back({0, (uint32_t)c0, (uint32_t)std::min<uint64_t>(cols, c0 + cg)});
-    for (uint32_t bt = 0; bt < nbt; bt++) tt.push_back({0, bt, 0});
-    if (!ct.empty()) {
-      using CC = CountCfg<uint32_t>;
-      const size_t smem = CC::STAGE * 4 + CC::KSMEM * 4;
-      static bool init = false;
-      if (!init) { set_smem(k_count<uint32_t, CC::NT, CC::STAGE, CC::KSMEM>, smem); init = true; }
-      TaskDesc* dC = ar.upload(ct);
-      ProfScope ps("count", st);
-      k_count<uint32_t, CC::NT, CC::STAGE, CC::KSMEM><<<(uint32_t)ct.size(), CC::NT, smem, st>>>(dL, dC, src, piv,
-                                                                                                 segmat, cnt);
-      check_launch("k_count");
-    }
-    std::vector<uint32_t> hcnt(k), start(k);
-    SQ_CUDA(cudaMemcpyAsync(hcnt.data(), cnt, uint64_t(k) * 4, cudaMemcpyDeviceToHost, st));
-    if (p->buc_in) SQ_CUDA(cudaMemcpyAsync(start.data(), p->buc_in, uint64_t(k) * 4, cudaMemcpyDeviceToHost, st));
-    SQ_CUDA(cudaStreamSynchronize(st));
-    g_stats.host_syncs++;
-    if (!p->buc_in) {
-      uint64_t pre = 0;
-      for (uint32_t b = 0; b < k; b++) {
-        start[b] = (uint32_t)pre;
-        pre += hcnt[b];
-      }
-    } else {
-      for (uint32_t b = 0; b < k; b++)
-        need(uint64_t(start[b]) + hcnt[b] <= n, "buc_in[j] + size_j exceeds n");
-    }
-    uint32_t* dstart = ar.upload(start);
-    if (n > 0) {
-      using TC = TrCfg<uint32_t, false>;
-      using CF = TransposeCfg<uint32_t, false, TC::NT, TC::S, TC::G>;
-      auto f = k_transpose<uint32_t, false, TC::NT, TC::S, TC::G>;
-      static bool init = false;
-      if (!init) { set_smem(f, CF::SMEM); init = true; }
-      TaskDesc* dT = ar.upload(tt);
-      ProfScope ps("transpose", st);
-      f<<<(uint32_t)tt.size(), TC::NT, CF::SMEM, st>>>(dL, dT, src, dst, nullptr, nullptr, piv, segmat, dstart);
-      check_launch("k_transpose");
-    }
-    std::vector<uint32_t> out(k);
-    for (uint32_t b = 0; b < k; b++) out[b] = start[b] + hcnt[b];
-    uint32_t* dout = ar.upload(out);
-    SQ_CUDA(cudaMemcpyAsync(p->buc_out, dout, uint64_t(k) * 4, cudaMemcpyDeviceToDevice, st));
-    SQ_CUDA(cudaStreamSynchronize(st));
+    skew_entry<uint32_t>(src, dst, rows, cols, p->pivots, p->k, p->n, p->buc_in, p->buc_out, p->naive_threshold,
+                         p->flags, (cudaStream_t)stream);
+  });
+}
+
+int sq_skew_transpose_u64(const uint64_t* src, uint64_t* dst, size_t rows, size_t cols,
+                          const sq_skew_params_u64* p, void* stream) {
+  return guarded([&] {
+    need(p != nullptr, "params is NULL");
+    skew_entry<uint64_t>(src, dst, rows, cols, p->pivots, p->k, p->n, p->buc_in, p->buc_out, p->naive_threshold,
+                         p->flags, (cudaStream_t)stream);
   });
 }
 

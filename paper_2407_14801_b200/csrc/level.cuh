@@ -218,8 +218,10 @@ template <typename K, bool PAIRS, int NT, int S, int G>
 __global__ void __launch_bounds__(NT)
 k_transpose(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tiles, const K* __restrict__ src,
             K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-            const K* __restrict__ piv, const uint32_t* __restrict__ segmat, const uint32_t* __restrict__ bstart) {
+            const K* __restrict__ piv, const uint32_t* __restrict__ segmat, const uint32_t* __restrict__ bstart,
+            const uint32_t* __restrict__ bad) {
   using C = TransposeCfg<K, PAIRS, NT, S, G>;
+  if (bad && (*bad & 4u)) return;  // caller cursors out of range: nothing is written
   static_assert(G <= 256, "fragment index is a byte");
   static_assert(S % NT == 0 && NT % 32 == 0 && NT >= G, "shape");
   static_assert(S <= 65535, "u16 table");
@@ -409,13 +411,49 @@ __global__ void k_copy_ranges(const SegDesc* __restrict__ r, const K* __restrict
 
 // Precondition check for the standalone SkewTranspose (SQ_FLAG_VALIDATE):
 // columns sorted and pivots non-decreasing.
-static __global__ void k_validate(const uint32_t* __restrict__ src, uint64_t rows, uint64_t n,
-                           const uint32_t* __restrict__ piv, uint32_t np, uint32_t* __restrict__ bad) {
+template <typename K>
+__global__ void k_validate(const K* __restrict__ src, uint64_t rows, uint64_t n, const K* __restrict__ piv,
+                           uint32_t np, uint32_t* __restrict__ bad) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
     if (i % rows != 0 && src[i - 1] > src[i]) atomicOr(bad, 1u);
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x + 1; i < np; i += stride)
     if (piv[i - 1] > piv[i]) atomicOr(bad, 2u);
+}
+
+// Standalone SkewTranspose cursors, on the device (no host round trip): with
+// buc_in == NULL the bucket starts are the exclusive prefix of the counts
+// (analysis convention); otherwise the caller's cursors are checked
+// (every range [buc_in[j], buc_in[j] + size_j) inside [0, n); bad[0] |= 4 if
+// not).  One CTA of 1024 threads.
+static __global__ void __launch_bounds__(1024)
+k_skew_cursors(const uint32_t* __restrict__ cnt, uint32_t k, uint64_t n, const uint32_t* __restrict__ buc_in,
+               uint32_t* __restrict__ start, uint32_t* __restrict__ bad) {
+  __shared__ uint32_t misc[64];
+  if (buc_in) {
+    for (uint32_t j = threadIdx.x; j < k; j += 1024) {
+      const uint64_t b = buc_in[j];
+      if (b + cnt[j] > n) atomicOr(bad, 4u);
+      start[j] = uint32_t(b);
+    }
+    return;
+  }
+  const uint32_t per = (k + 1023) / 1024, j0 = min(k, threadIdx.x * per), j1 = min(k, j0 + per);
+  uint32_t sum = 0;
+  for (uint32_t j = j0; j < j1; j++) sum += cnt[j];
+  uint32_t tot;
+  uint32_t o = block_excl_sum<32>(sum, misc, &tot);
+  for (uint32_t j = j0; j < j1; j++) {
+    start[j] = o;
+    o += cnt[j];
+  }
+}
+
+// buc_out[j] = start[j] + size_j (the final cursors)
+static __global__ void k_skew_finish(const uint32_t* __restrict__ start, const uint32_t* __restrict__ cnt, uint32_t k,
+                                     uint32_t* __restrict__ buc_out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+    buc_out[j] = start[j] + cnt[j];
 }
 
 }  // namespace sq

@@ -381,6 +381,53 @@ def test_cfg2_skew_transpose_check(T):
     assert np.array_equal(gbo.astype(np.uint64), wbo)
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_skew_transpose_u64_random_shapes(seed):
+    """sq_skew_transpose_u64 (f1) against the oracle's Alg 2 and the closed form: ragged and
+    empty columns, duplicate pivots, keys above 2^32, caller cursors."""
+    rng = np.random.default_rng(1000 + seed)
+    rows, cols = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+    n = int(rng.integers(0, rows * cols + 1))
+    card = [2**64, 2**40, 50][seed % 3]
+    if card == 2**64:
+        x = rng.integers(0, 2**63, rows * cols, dtype=np.uint64) * 2 + 1
+    else:
+        x = rng.integers(0, card, rows * cols, dtype=np.uint64)
+    x = _sorted_cols(x, rows, n)
+    k = int(rng.integers(1, 70))
+    P = np.sort(rng.choice(x[: max(n, 1)], k - 1)) if n and k > 1 else np.sort(rng.integers(0, card, k - 1, dtype=np.uint64))
+    want, _, wbo = O.skew_transpose_matrix(x, rows, cols, P, k, n=n, T=int(rng.integers(2, 6)))
+    dc, _, bc = CF.skew_transpose(x, P, k, n=n)
+    assert (want[:n] == dc[:n]).all() and (wbo == bc).all()
+    s = to_dev(x)
+    d = torch.zeros_like(s)
+    pv = to_dev(P.astype(np.uint64)) if k > 1 else None
+    bi = None
+    if seed % 2:  # caller cursors: buckets in reverse order
+        sizes = bc - np.concatenate([[0], bc[:-1]]).astype(np.uint64)
+        bi = np.concatenate([[0], np.cumsum(sizes[::-1])[:-1]])[::-1].astype(np.uint32)
+        want, _, wbo = O.skew_transpose_matrix(x, rows, cols, P, k, n=n, buc_in=bi.astype(np.uint64))
+    bo = sq.skew_transpose(s, d, rows, cols, pv, k, n, to_dev(bi) if bi is not None else None)
+    assert np.array_equal(to_host(d)[:n], want[:n])
+    assert np.array_equal(to_host(bo).astype(np.uint64), wbo)
+    st = sq.get_stats()
+    assert st["host_syncs"] == 1  # cursors scanned / checked on the device
+
+
+def test_skew_transpose_bad_cursors_rejected():
+    rows = cols = 64
+    x = _sorted_cols(np.arange(rows * cols, dtype=np.uint64)[::-1].copy(), rows, rows * cols)
+    P = np.arange(1, cols, dtype=np.uint64) * rows
+    bi = np.full(cols, rows * cols - 1, np.uint32)  # every range but one leaves dst
+    for dt in (np.uint32, np.uint64):
+        s = to_dev(x.astype(dt))
+        d = torch.zeros_like(s)
+        with pytest.raises(sq.SqError) as e:
+            sq.skew_transpose(s, d, rows, cols, to_dev(P.astype(dt)), cols, 0, to_dev(bi))
+        assert e.value.code == 1
+        assert int(to_host(d).astype(np.uint64).sum()) == 0  # nothing was written
+
+
 def test_skew_transpose_special_case_is_transpose():
     m = 300  # P:217-218: one item of every bucket per column -> plain transpose
     src = np.array([c + r * m for c in range(m) for r in range(m)], np.uint64)
