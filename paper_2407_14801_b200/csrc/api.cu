@@ -56,25 +56,32 @@ void skew_entry(const K* src, K* dst, size_t rows, size_t cols, const K* pivots,
   const K* piv = pivots;
   if (k == 1) piv = (const K*)ar.alloc(sizeof(K));
   uint32_t* segmat = (uint32_t*)ar.alloc(std::max<uint64_t>(uint64_t(cols) * (nbt + 1), 1) * 4);
-  uint32_t* cnt = (uint32_t*)ar.alloc(uint64_t(k) * 4);
-  uint32_t* start = (uint32_t*)ar.alloc(uint64_t(k) * 4);
-  SQ_CUDA(cudaMemsetAsync(cnt, 0, uint64_t(k) * 4, st));
+  // column ranges of 64 columns: the count runs one CTA per range, the transpose one CTA
+  // per (bucket tile, range), each range's cursors offset by the ranges before it
   std::vector<TaskDesc> ct, tt;
-  const uint64_t cg = std::max<uint64_t>(1, (cols + 295) / 296);
+  const uint64_t cg = std::max<uint64_t>(64, (cols + 1023) / 1024);
   for (uint64_t c0 = 0; c0 < cols; c0 += cg) ct.push_back({0, (uint32_t)c0, (uint32_t)std::min<uint64_t>(cols, c0 + cg)});
   for (uint32_t bt = 0; bt < nbt; bt++) tt.push_back({0, bt, 0});
+  const uint32_t nr = std::max<uint32_t>(1, (uint32_t)ct.size());
+  uint32_t* cnt = (uint32_t*)ar.alloc(uint64_t(nr) * k * 4);  // (range, bucket) counts, then prefixes
+  uint32_t* tot = (uint32_t*)ar.alloc(uint64_t(k) * 4);
+  uint32_t* start = (uint32_t*)ar.alloc(uint64_t(k) * 4);
+  SQ_CUDA(cudaMemsetAsync(cnt, 0, uint64_t(nr) * k * 4, st));
+  if (ct.empty()) ct.push_back({0, 0, 0});
   const std::vector<void*> up = ar.upload_all({Arena::part(std::vector<LevelSeg>{l}), Arena::part(ct), Arena::part(tt)});
   const LevelSeg* dL = (const LevelSeg*)up[0];
-  if (!ct.empty()) {
+  if (cols) {
     using CC = CountCfg<K>;
     const size_t smem = CC::STAGE * sizeof(K) + CC::KSMEM * 4;
     set_smem(k_count<K, CC::NT, CC::STAGE, CC::KSMEM>, smem);
     ProfScope ps("count", st);
-    k_count<K, CC::NT, CC::STAGE, CC::KSMEM><<<(uint32_t)ct.size(), CC::NT, smem, st>>>(
-        dL, (const TaskDesc*)up[1], src, piv, segmat, cnt);
+    k_count<K, CC::NT, CC::STAGE, CC::KSMEM><<<nr, CC::NT, smem, st>>>(dL, (const TaskDesc*)up[1], src, piv, segmat,
+                                                                     cnt);
     check_launch("k_count");
   }
-  k_skew_cursors<<<1, 1024, 0, st>>>(cnt, k, n, buc_in, start, bad);
+  k_skew_range_prefix<<<std::max<uint32_t>(1, std::min<uint32_t>((k + 255) / 256, 1184)), 256, 0, st>>>(cnt, nr, k, tot);
+  check_launch("k_skew_range_prefix");
+  k_skew_cursors<<<1, 1024, 0, st>>>(tot, k, n, buc_in, start, bad);
   check_launch("k_skew_cursors");
   if (n > 0) {
     using TC = TrCfg<K, false>;
@@ -82,11 +89,11 @@ void skew_entry(const K* src, K* dst, size_t rows, size_t cols, const K* pivots,
     auto f = k_transpose<K, false, TC::NT, TC::S, TC::G>;
     set_smem(f, CF::SMEM);
     ProfScope ps("transpose", st);
-    f<<<(uint32_t)tt.size(), TC::NT, CF::SMEM, st>>>(dL, (const TaskDesc*)up[2], src, dst, nullptr, nullptr, piv,
-                                                       segmat, start, bad);
+    f<<<dim3((uint32_t)tt.size(), nr), TC::NT, CF::SMEM, st>>>(dL, (const TaskDesc*)up[2], src, dst, nullptr, nullptr,
+                                                               piv, segmat, start, bad, (const TaskDesc*)up[1], cnt);
     check_launch("k_transpose");
   }
-  k_skew_finish<<<std::max<uint32_t>(1, std::min<uint32_t>((k + 255) / 256, 1184)), 256, 0, st>>>(start, cnt, k,
+  k_skew_finish<<<std::max<uint32_t>(1, std::min<uint32_t>((k + 255) / 256, 1184)), 256, 0, st>>>(start, tot, k,
                                                                                                   buc_out);
   check_launch("k_skew_finish");
   uint32_t* hb = (uint32_t*)ar.pinned(4);

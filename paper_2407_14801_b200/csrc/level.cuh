@@ -62,9 +62,10 @@ __global__ void k_colmin(const LevelSeg* __restrict__ segs, const K* __restrict_
 // ------------------------------------------------------------------------------
 // Bucket count: for each sorted column, a simultaneous scan
 // of the column and the pivots gives the position of every bucket boundary;
-// bucket sizes accumulate per CTA in shared memory (flushed with one atomic
-// per bucket), and the positions of the tile boundaries (every kTB-th bucket)
-// are stored for the SkewTranspose.  CTA = (segment, column range).
+// bucket sizes accumulate per CTA in shared memory and go to the CTA's row of a
+// (column range, bucket) count matrix (zeroed by the caller), and the positions
+// of the tile boundaries (every kTB-th bucket) are stored for the SkewTranspose.
+// CTA = (segment, column range).
 // Boundary j (1..k-1): x lies before it iff x < P[j-1], or x == P[j-1] when
 // P[j-1] == P[j-2] (single-value bucket rule, L4).
 template <typename K, int NT, int STAGE, int KSMEM>
@@ -118,16 +119,15 @@ k_count(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tasks, c
         }
         const uint32_t n_b = nxt - pos;
         if (smem_cnt) cnt[b] += n_b;
-        else if (n_b) atomicAdd(&gcnt[sg.buck_base + b], n_b);
+        else if (n_b) atomicAdd(&gcnt[uint64_t(blockIdx.x) * k + b], n_b);
         pos = nxt;
       }
     }
     if (threadIdx.x == 0) row[sg.nbt] = L;
   }
-  if (smem_cnt) {
+  if (smem_cnt) {  // this task's row of the (task, bucket) count matrix
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < k; b += NT)
-      if (cnt[b]) atomicAdd(&gcnt[sg.buck_base + b], cnt[b]);
+    for (uint32_t b = threadIdx.x; b < k; b += NT) gcnt[uint64_t(blockIdx.x) * k + b] = cnt[b];
   }
 }
 
@@ -219,7 +219,11 @@ __global__ void __launch_bounds__(NT)
 k_transpose(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tiles, const K* __restrict__ src,
             K* __restrict__ dst, const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
             const K* __restrict__ piv, const uint32_t* __restrict__ segmat, const uint32_t* __restrict__ bstart,
-            const uint32_t* __restrict__ bad) {
+            const uint32_t* __restrict__ bad, const TaskDesc* __restrict__ cranges,
+            const uint32_t* __restrict__ cpre) {
+  // CTA (tile, column range r): columns cranges[r] of bucket tile tiles[.]; the
+  // cursor of bucket j starts at bstart[j] + cpre[r][j] (the keys of bucket j in
+  // the column ranges before r)
   using C = TransposeCfg<K, PAIRS, NT, S, G>;
   if (bad && (*bad & 4u)) return;  // caller cursors out of range: nothing is written
   static_assert(G <= 256, "fragment index is a byte");
@@ -245,14 +249,17 @@ k_transpose(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tile
   K* bval = reinterpret_cast<K*>(sm + C::off_bval);
 
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t nr = gridDim.y, r = blockIdx.y;
   const TaskDesc tk = tiles[blockIdx.x];
+  const TaskDesc cr = cranges[r];
   const LevelSeg sg = segs[tk.seg];
   const uint32_t bt = tk.a;
   const uint32_t b0 = bt * kTB;
   const uint32_t nb = min((uint32_t)kTB, sg.k - b0);
   const uint32_t nint = nb - 1;  // internal boundaries b0+1 .. b0+nb-1
   const K* P = piv + sg.piv_base;
-  if (t < (int)nb) cursor[t] = bstart[sg.buck_base + b0 + t];
+  (void)nr;
+  if (t < (int)nb) cursor[t] = bstart[sg.buck_base + b0 + t] + cpre[uint64_t(r) * sg.k + b0 + t];
   if (t < (int)nint) {
     const uint32_t j = b0 + 1 + t;
     bval[t] = P[j - 1];
@@ -261,8 +268,8 @@ k_transpose(const LevelSeg* __restrict__ segs, const TaskDesc* __restrict__ tile
   __syncthreads();
   const int i0 = t * C::VS;
 
-  for (uint32_t g0 = 0; g0 < sg.ncols; g0 += G) {
-    const uint32_t ng = min((uint32_t)G, sg.ncols - g0);
+  for (uint32_t g0 = cr.a; g0 < cr.b; g0 += G) {
+    const uint32_t ng = min((uint32_t)G, cr.b - g0);
     // ---- this tile's run in each column g0 .. g0+ng-1; exclusive scan of the lengths
     uint32_t len = 0;
     if (t < (int)ng) {
@@ -419,6 +426,21 @@ __global__ void k_validate(const K* __restrict__ src, uint64_t rows, uint64_t n,
     if (i % rows != 0 && src[i - 1] > src[i]) atomicOr(bad, 1u);
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x + 1; i < np; i += stride)
     if (piv[i - 1] > piv[i]) atomicOr(bad, 2u);
+}
+
+// Column-range prefix of the (range, bucket) count matrix, in place (exclusive,
+// per bucket), and each bucket's total.  Thread per bucket.
+static __global__ void k_skew_range_prefix(uint32_t* __restrict__ cnt, uint32_t nr, uint32_t k,
+                                           uint32_t* __restrict__ tot) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    uint32_t run = 0;
+    for (uint32_t r = 0; r < nr; r++) {
+      const uint32_t c = cnt[uint64_t(r) * k + j];
+      cnt[uint64_t(r) * k + j] = run;
+      run += c;
+    }
+    tot[j] = run;
+  }
 }
 
 // Standalone SkewTranspose cursors, on the device (no host round trip): with

@@ -42,9 +42,15 @@ for m, dt in ((1024, torch.uint32), (8192, torch.uint32), (8192, torch.uint64)):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     ms = statistics.median(ts)
+    sq.profile(True)
+    sq.profile_read()
+    sq.skew_transpose(x, dst, m, m, piv, buc_out=bo)
+    torch.cuda.synchronize()
+    sq.profile(False)
+    roles = {k: round(v[1], 4) for k, v in sq.profile_read().items()}
     w = x.element_size()
     gbs = 2 * w * n / (ms / 1e3) / 1e9
     ok = int(bo[-1].item()) == n
     out.append({"m": m, "dtype": str(dt), "n": n, "ms": ms, "alg_gbs": gbs, "frac_of_measured": gbs / HBM,
-                "buc_out_last_ok": ok, "host_syncs": sq.get_stats()["host_syncs"]})
+                "buc_out_last_ok": ok, "host_syncs": sq.get_stats()["host_syncs"], "roles_ms": roles})
     print(json.dumps(out[-1]), flush=True)
