@@ -20,6 +20,7 @@
 #include <string>
 #include <type_traits>
 #include <vector>
+#include <chrono>
 #include <set>
 #include <tuple>
 
@@ -157,6 +158,16 @@ inline void prof_collect() {  // after a stream sync
     pool_return(e.dev, e.b);
   }
   g_prof_pending.clear();
+}
+
+// ------------------------------------------------------------------ host trace
+// SQ_HOST_TRACE=1 prints host timestamps of the level phases to stderr (diagnostics).
+inline bool g_trace = getenv("SQ_HOST_TRACE") != nullptr;
+inline void htrace(const char* what, size_t a = 0, size_t b = 0) {
+  if (!g_trace) return;
+  static const auto t0 = std::chrono::steady_clock::now();
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  fprintf(stderr, "[sq %10.1f us] %s %zu %zu\n", us, what, a, b);
 }
 
 // ------------------------------------------------------------------ options
@@ -762,7 +773,6 @@ struct Engine {
           allcols.push_back({uint32_t(g.off + uint64_t(c) * m), c < fc ? m : rem, child_key(g.node, 0, c)});
       } else {
         std::vector<ColDesc>& full = colcls[std::max<uint32_t>(64, tile_for(m))];
-        full.reserve(full.size() + fc);
         for (uint32_t c = 0; c < fc; c++) full.push_back({uint32_t(g.off + uint64_t(c) * m), m, s, c});
         if (rem) colcls[std::max<uint32_t>(64, tile_for(rem))].push_back({uint32_t(g.off + uint64_t(fc) * m), rem, s, fc});
       }
@@ -779,7 +789,9 @@ struct Engine {
                                                         Arena::part(mtasks)};
     if (!generic)
       for (auto& kv : colcls) parts.push_back(Arena::part(kv.second));
+    htrace("level: descriptors built", ns, depth);
     const std::vector<void*> up = ar.upload_all(parts);
+    htrace("level: uploaded");
     LevelSeg* dL = (LevelSeg*)up[0];
     TileInfo* dTiles = (TileInfo*)up[1];
     uint32_t* dTileBase = (uint32_t*)up[2];
@@ -819,6 +831,7 @@ struct Engine {
       launch_pdl(k_select_round<K>, ns, 256, 0, st, dL, ns, (const K*)cand, (const uint8_t*)flags, (const K*)p0s,
                  (const K*)segmin, piv, info, fix, 0);
     }
+    htrace("level: sampler launched");
     // 2. sort every column in place + tile boundaries + min(D).  The first
     // class launches as a programmatic dependent: its CTAs load and sort while the
     // sampler and the round selection still run, and wait for them (griddepcontrol)
@@ -860,6 +873,7 @@ struct Engine {
         check_launch("k_segmat");
       }
     }
+    htrace("level: columns launched");
     // 3. min-exclusion: final round; repair the boundaries if it changed
     {
       ProfScope ps("select", st);
@@ -905,6 +919,7 @@ struct Engine {
       ar.release(pcount);
       ar.release(pieces);
     }
+    htrace("level: transpose launched");
     // 5. bucket plan: sizes, final offsets, work lists
     PlanOut po{};
     po.ncls = 0;
@@ -1071,6 +1086,7 @@ struct Engine {
       ar.release(nun);
       ar.release(units);
     }
+    htrace("level: bucket sorts launched");
     // 7. one host read per level: the oversize list (and the round, for stats)
     uint32_t* hcnt = (uint32_t*)ar.pinned((po.ncls + 2) * 4);
     uint32_t* hinfo = (uint32_t*)ar.pinned(4);
@@ -1103,6 +1119,7 @@ struct Engine {
     for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)po.mlist, (void*)piv,
                     (void*)flags, (void*)p0s, (void*)info, (void*)fix, (void*)segmin})
       ar.release(p);
+    htrace("level: done, oversize segments", over.size(), depth);
     if (!over.empty()) sort_batch(over, X, X, depth + 1, "bucketsort");
   }
 };
