@@ -180,6 +180,19 @@ int sq_skew_transpose_u64(const uint64_t *src, uint64_t *dst, size_t rows, size_
                           const sq_skew_params_u64 *params, void *stream);
 
 /* ------------------------------------------------------------------------- */
+/* The sampler's counter-based RNG, on the host, for callers    */
+/* that run a SquareSort level across several GPUs (paper_2407_14801_b200.dist):*/
+/* every rank derives the same sample positions of the global level.         */
+/* ------------------------------------------------------------------------- */
+/* Root node key of a sort with this seed (mix(seed)). */
+uint64_t sq_root_key(uint64_t seed);
+/* out[r*count + i] = floor(draw(node, r, i) * n / 2^64): position i of sampling
+ * round r of a level of n keys at `node` (the positions the
+ * single-GPU sampler draws).  out is HOST memory of rounds*count entries.
+ * SQ_ERR_INVALID_ARGUMENT for NULL out or n = 0 with work to do.  No GPU use. */
+int sq_draw_positions(uint64_t node, uint32_t rounds, uint32_t count, uint64_t n, uint64_t *out);
+
+/* ------------------------------------------------------------------------- */
 /* Introspection and test hooks.                                             */
 /* ------------------------------------------------------------------------- */
 const char *sq_status_string(int status);

@@ -26,7 +26,7 @@ EXPORTS = ["sq_sort_u32", "sq_sort_u64", "sq_sort_pairs_u32_u32", "sq_sort_u32_h
            "sq_status_string", "sq_last_error_message", "sq_get_stats", "sq_set_max_tile",
            "sq_debug_level_u32", "sq_profile", "sq_profile_read", "sq_set_big_bucket_mode",
            "sq_trim_memory", "sq_set_base_case", "sq_debug_level_u64", "sq_sort_pairs_u64_u32",
-           "sq_sort_pairs_u64_u32_host", "sq_skew_transpose_u64"]
+           "sq_sort_pairs_u64_u32_host", "sq_skew_transpose_u64", "sq_root_key", "sq_draw_positions"]
 
 
 class SqError(RuntimeError):
@@ -101,6 +101,10 @@ def lib():
         L.sq_debug_level_u64.restype = ctypes.c_int
         L.sq_set_base_case.argtypes = [ctypes.c_int]
         L.sq_set_base_case.restype = ctypes.c_int
+        L.sq_root_key.argtypes = [u64]
+        L.sq_root_key.restype = u64
+        L.sq_draw_positions.argtypes = [u64, u32, u32, u64, vp]
+        L.sq_draw_positions.restype = ctypes.c_int
         L.sq_trim_memory.argtypes = []
         L.sq_trim_memory.restype = ctypes.c_int
         _lib = L
@@ -303,6 +307,19 @@ def sort_u32_host_batch(ins, outs, seed: int = 0, stream=None):
 def sort_u64_host_batch(ins, outs, seed: int = 0, stream=None):
     import numpy as np
     return _host_batch(lib().sq_sort_u64_host_batch, ins, outs, np.uint64, seed, stream)
+
+
+# ------------------------------------------------------------------ sampler RNG (host)
+def root_key(seed: int) -> int:
+    return int(lib().sq_root_key(_seed(seed)))
+
+
+def draw_positions(node: int, rounds: int, count: int, n: int):
+    """numpy uint64 [rounds, count]: the sample positions of a level of n keys (sq_draw_positions)."""
+    import numpy as np
+    out = np.zeros((rounds, count), np.uint64)
+    _check(lib().sq_draw_positions(ctypes.c_uint64(node), rounds, count, n, ctypes.c_void_p(out.ctypes.data)))
+    return out
 
 
 # ------------------------------------------------------------------ introspection

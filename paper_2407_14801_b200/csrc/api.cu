@@ -186,6 +186,16 @@ const char* sq_status_string(int s) {
 
 const char* sq_last_error_message(void) { return g_errmsg.c_str(); }
 
+uint64_t sq_root_key(uint64_t seed) { return root_key(seed); }
+
+int sq_draw_positions(uint64_t node, uint32_t rounds, uint32_t count, uint64_t n, uint64_t* out) {
+  if (!out && rounds && count) return SQ_ERR_INVALID_ARGUMENT;
+  if (n == 0 && rounds && count) return SQ_ERR_INVALID_ARGUMENT;
+  for (uint32_t r = 0; r < rounds; r++)
+    for (uint32_t i = 0; i < count; i++) out[uint64_t(r) * count + i] = draw_index_host(draw(node, r, i), n);
+  return SQ_OK;
+}
+
 int sq_trim_memory(void) {
   return guarded([&] {
     check_device();

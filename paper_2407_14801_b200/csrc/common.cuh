@@ -48,6 +48,7 @@ __host__ __device__ __forceinline__ uint64_t draw(uint64_t key, uint32_t round, 
 }
 // floor(d * len / 2^64): a uniform position in [0, len).
 __device__ __forceinline__ uint64_t draw_index(uint64_t d, uint64_t len) { return __umul64hi(d, len); }
+inline uint64_t draw_index_host(uint64_t d, uint64_t len) { return (uint64_t)(((unsigned __int128)d * len) >> 64); }
 
 // ---------------------------------------------------------------- m = ceil(sqrt(n))
 __host__ __device__ inline uint64_t ceil_sqrt(uint64_t n) {
