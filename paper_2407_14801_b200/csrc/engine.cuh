@@ -499,6 +499,9 @@ template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16,
 // largest bucket one CTA sorts when clusters are on (2 CTAs per SM stay resident)
 // (the counting-sort base case sorts up to 32K 32-bit keys per CTA at full rate;
 // SQ_ONE_CAP overrides it for experiments)
+// largest unit of packed small buckets (SQ_UNIT_MAX; 0 = the largest one-CTA class)
+// (measured: 16K units 4.41 ms vs 32K 4.47 ms at cfg5 -- the 16K class runs two CTAs per SM)
+inline uint32_t g_unit_max = getenv("SQ_UNIT_MAX") ? (uint32_t)atoi(getenv("SQ_UNIT_MAX")) : 16384u;
 inline uint32_t g_one_cap = getenv("SQ_ONE_CAP") ? (uint32_t)atoi(getenv("SQ_ONE_CAP")) : 32768u;
 template <typename SK> uint32_t single_cap() {
   return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : (sizeof(SK) == 8 ? 8192u : 4096u);
@@ -956,6 +959,7 @@ struct Engine {
     po.unit_max = 0;
     for (uint32_t c = 0; c < po.ncls; c++)
       if (!cls_cl[c]) po.unit_max = std::max(po.unit_max, po.cls_tile[c]);
+    if (g_unit_max) po.unit_max = std::min(po.unit_max, g_unit_max);
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     // (u64 pairs have no cluster kernel: mode 2 runs the merge base case for them)
