@@ -24,6 +24,8 @@
 //      one block, where pass 1 sorts it, or straddles one block boundary and lies
 //      inside the window pass 2 merges.  A larger bin (skewed input) falls back to
 //      the merge sort of blocksort.cuh on the bin-ordered tile.
+// The tile lives in shared memory in an XOR-swizzled row layout (swz32, see pad()),
+// so the fix-up passes move 16-byte vectors without bank conflicts.
 // The result is the sorted tile; keys are unique values, so the unstable scatter
 // does not matter (pairs keep the stable merge sort).
 #pragma once
@@ -53,7 +55,32 @@ struct BinSort {
     return p + ((16u - mis) & 15u) / 4u;
   }
 
-  __device__ __forceinline__ static uint32_t pad(uint32_t i) { return pad32(i); }
+  // Tile layout: rows of 32 keys (128 bytes); the 16-byte chunk c of the tile (keys
+  // [4c, 4c+4)) is stored at chunk slot c ^ ((c / 8) % 8) of its row.  Per-thread
+  // blocks of consecutive keys are then read and written with conflict-free 16-byte
+  // accesses (8 threads of a phase hit 8 different slots), warp-contiguous scalar
+  // accesses stay conflict-free, and the tile takes exactly TILE words.
+  __device__ __forceinline__ static uint32_t pad(uint32_t i) { return swz32(i); }
+  __device__ __forceinline__ static uint4& chunk(uint32_t* s, uint32_t c) {
+    return reinterpret_cast<uint4*>(s)[c ^ ((c >> 3) & 7)];
+  }
+  // keys [b, b + N) (b a multiple of 4) to r[0..N) / from r[0..N)
+  template <int N>
+  __device__ __forceinline__ static void ld_block(const uint32_t* s, uint32_t b, uint32_t* r) {
+#pragma unroll
+    for (int q = 0; q < N / 4; q++) {
+      const uint4 v = chunk(const_cast<uint32_t*>(s), (b >> 2) + q);
+      r[4 * q] = v.x;
+      r[4 * q + 1] = v.y;
+      r[4 * q + 2] = v.z;
+      r[4 * q + 3] = v.w;
+    }
+  }
+  template <int N>
+  __device__ __forceinline__ static void st_block(uint32_t* s, uint32_t b, const uint32_t* r) {
+#pragma unroll
+    for (int q = 0; q < N / 4; q++) chunk(s, (b >> 2) + q) = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+  }
 
   template <bool SCATTER>
   __device__ __forceinline__ static void bin_op(uint32_t* s, uint32_t* cnt, uint32_t x, uint32_t b) {
@@ -96,13 +123,13 @@ struct BinSort {
   }
 
   // Sort the TILE keys at s[pad(0..TILE-1)]; positions >= len hold 0xFFFFFFFF
-  // padding (left in place).  cnt: CNT_WORDS words of shared memory.  On return
-  // the sorted tile is in s and a __syncthreads() has been executed.
+  // padding (left in place).  cnt: CNT_WORDS words of shared memory; s must have room
+  // for the padded layout of BlockSort<uint32_t, NT, V> (the skewed-input fallback).
+  // On return the sorted tile is in s and a __syncthreads() has been executed.
   __device__ static void sort_smem(uint32_t* s, uint32_t* cnt, uint32_t len = TILE) {
     const uint32_t b0 = uint32_t(threadIdx.x) * V;
     uint32_t r[V];
-#pragma unroll
-    for (int j = 0; j < V; j++) r[j] = s[pad(b0 + j)];
+    ld_block<V>(s, b0, r);
     sort_regs(r, s, cnt, len, [&](int j) { return b0 + j; });
   }
 
@@ -217,27 +244,39 @@ struct BinSort {
     hist_or_scatter<true>(s, cnt, r, mn, f, exact, full, len, pos);
     __syncthreads();
     if (exact) return;  // every bin is one value
-    if (gbig > RUNMAX) {  // a bin too long for the fix-up (skewed input): merge sort
-      BlockSort<uint32_t, NT, V>::sort_smem(s, len);
+    if (gbig > RUNMAX) {  // a bin too long for the fix-up (skewed input): merge sort,
+      // in the merge sort's padded layout (converted there and back through registers)
+      using MS = BlockSort<uint32_t, NT, V>;
+      ld_block<V>(s, b0, r);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < V; j++) s[MS::pad(b0 + j)] = r[j];
+      __syncthreads();
+      MS::sort_smem(s, len);
+#pragma unroll
+      for (int j = 0; j < V; j++) r[j] = s[MS::pad(b0 + j)];
+      __syncthreads();
+      st_block<V>(s, b0, r);
+      __syncthreads();
       return;
     }
     // ---- 4a. fix-up pass 1: every thread sorts its block of V consecutive keys
     const bool live = (uint32_t(t) & ~31u) * V < len;  // warp-uniform: padding-only warps skip
     if (live) {
-#pragma unroll
-      for (int j = 0; j < V; j++) r[j] = s[pad(b0 + j)];
+      ld_block<V>(s, b0, r);
       thread_sort<uint32_t, V>(r);
-#pragma unroll
-      for (int j = 0; j < V; j++) s[pad(b0 + j)] = r[j];
+      st_block<V>(s, b0, r);
     }
     __syncthreads();
     // ---- 4b. fix-up pass 2: merge [b0 + V/2, b0 + V) with [b0 + V, b0 + 3V/2)
     constexpr int H = V / 2;
     if (t < NT - 1 && b0 + H < len) {
+      ld_block<H>(s, b0 + H, r);
+      {
+        uint32_t u[H];
+        ld_block<H>(s, b0 + V, u);
 #pragma unroll
-      for (int j = 0; j < H; j++) {
-        r[j] = s[pad(b0 + H + j)];
-        r[H + j] = s[pad(b0 + V + H - 1 - j)];  // descending: a bitonic sequence
+        for (int j = 0; j < H; j++) r[H + j] = u[H - 1 - j];  // descending: a bitonic sequence
       }
       const uint32_t one = (uint32_t)c_one, mone = (uint32_t)c_mone;
 #pragma unroll
@@ -248,8 +287,7 @@ struct BinSort {
             if (i & 1) cas_fma(r[i], r[i + d], one, mone);
             else cas(r[i], r[i + d]);
           }
-#pragma unroll
-      for (int j = 0; j < V; j++) s[pad(b0 + H + j)] = r[j];
+      st_block<V>(s, b0 + H, r);
     }
     __syncthreads();
   }

@@ -104,6 +104,10 @@ __host__ __device__ __forceinline__ bool before_boundary(K x, K pj, bool dup) {
 // One pad word per 32 words keeps blocked per-thread accesses conflict-free.
 __host__ __device__ __forceinline__ uint32_t pad32(uint32_t i) { return i + (i >> 5); }
 
+// XOR-swizzled rows of 32 words: the 16-byte chunk c (words [4c, 4c+4)) sits at
+// chunk slot c ^ ((c / 8) % 8) of its 128-byte row (the counting sort's tile layout).
+__host__ __device__ __forceinline__ uint32_t swz32(uint32_t i) { return i ^ (((i >> 5) & 7) << 2); }
+
 __host__ __device__ constexpr uint32_t ilog2c(uint32_t x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
 
 }  // namespace sq

@@ -81,6 +81,13 @@ __host__ __device__ constexpr size_t bin_smem() {
   if constexpr (BIN && bin_ok<K, V, PAIRS>()) return BinSort<NT, V>::CNT_BYTES;
   else return 0;
 }
+// Physical slot of tile position i in the sort kernels' shared-memory tile: the
+// counting sort's swizzled rows, else the merge sort's padded layout.
+template <typename K, int NT, int V, bool PAIRS, bool BIN>
+__device__ __forceinline__ uint32_t tpos(uint32_t i) {
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) return swz32(i);
+  else return BlockSort<sortkey_t<K, PAIRS>, NT, V>::pad(i);
+}
 // Sort the tile in shared memory with the selected base case.
 template <typename K, int NT, int V, bool PAIRS, bool BIN, typename SK>
 __device__ __forceinline__ void tile_sort(SK* s, uint32_t* cnt, uint32_t len) {
@@ -189,6 +196,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SK* s = reinterpret_cast<SK*>(smem_raw);
   uint32_t* vs = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  auto TP = [](uint32_t i) { return tpos<K, NT, V, PAIRS, BIN>(i); };
   const ColDesc d = cols[blockIdx.x];
   const LevelSeg sg = segs[d.seg];
   constexpr int VW = 16 / sizeof(K), NV = BS::TILE / (NT * VW);  // 16-byte vectors per thread
@@ -225,7 +233,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
         const uint32_t i0 = (threadIdx.x + q * NT) * VW;
         const K* e = reinterpret_cast<const K*>(&v[q]);
 #pragma unroll
-        for (int j = 0; j < VW; j++) s[BS::pad(i0 + j)] = SK(e[j]);
+        for (int j = 0; j < VW; j++) s[TP(i0 + j)] = SK(e[j]);
       }
     } else {
       for (int i = threadIdx.x; i < BS::TILE; i += NT) {
@@ -238,7 +246,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
             x = keys[d.off + i];
           }
         }
-        s[BS::pad(i)] = x;
+        s[TP(i)] = x;
       }
     }
     __syncthreads();
@@ -248,11 +256,21 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   // input, and the pivots must be selected, before this CTA writes or reads them
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   auto key_at = [&](int i) -> K {
-    if constexpr (PAIRS) return K(s[BS::pad(i)] >> 32);
-    else return s[BS::pad(i)];
+    if constexpr (PAIRS) return K(s[TP(i)] >> 32);
+    else return s[TP(i)];
   };
+  bool stored = false;
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) {
+    if (vec_ok) {  // 16-byte chunks of the swizzled tile
+      uint4* g = reinterpret_cast<uint4*>(keys + d.off);
+      for (uint32_t c = threadIdx.x; c < uint32_t(BS::TILE) / 4; c += NT)
+        g[c] = BinSort<NT, V>::chunk(reinterpret_cast<uint32_t*>(s), c);
+      stored = true;
+    }
+  }
+  if (!stored)
   for (int i = threadIdx.x; i < (int)d.len; i += NT) {
-    const SK x = s[BS::pad(i)];
+    const SK x = s[TP(i)];
     if constexpr (PAIRS) {
       keys[d.off + i] = K(x >> 32);
       vals[d.off + i] = vs[uint32_t(x)];
@@ -842,6 +860,7 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
   uint32_t* s_dst = s_len + NT;
   uint32_t* misc = s_dst + NT;
   uint32_t* cnt = misc + 64;  // counting-sort counters (BIN)
+  auto TP = [](uint32_t i) { return tpos<K, NT, V, PAIRS, BIN>(i); };
   const uint32_t total = *count;
   for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
     const uint32_t e = list[it];
@@ -869,17 +888,17 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     const uint32_t len = hi - lo;
     K* out = (passes & 1) ? dst_odd : dst;
     uint32_t* vout = (passes & 1) ? vdst_odd : vdst;
-    for (int i = threadIdx.x + len; i < BS::TILE; i += NT) s[BS::pad(i)] = KeyTraits<SK>::kMax;
+    for (int i = threadIdx.x + len; i < BS::TILE; i += NT) s[TP(i)] = KeyTraits<SK>::kMax;
     gather_bucket<NT>(ti, lane0, pout, ppre, s_off, s_len, s_dst, misc, lo, hi,
                       [&](uint32_t o, uint32_t l, uint32_t d, int ln) {
                         SQ_CHECK(d + l <= uint32_t(BS::TILE) && o >= ti.out && o + l <= ti.out + ti.size);
                         for (uint32_t q = ln; q < l; q += 32) {
                           if constexpr (PAIRS) {
                             // key into the low half of the composite slot, fixed up below
-                            cp_async_elem(reinterpret_cast<K*>(&s[BS::pad(d + q)]), &src[o + q]);
+                            cp_async_elem(reinterpret_cast<K*>(&s[TP(d + q)]), &src[o + q]);
                             cp_async_elem(&vs[d + q], &vsrc[o + q]);
                           } else {
-                            cp_async_elem(&s[BS::pad(d + q)], &src[o + q]);
+                            cp_async_elem(&s[TP(d + q)], &src[o + q]);
                           }
                         }
                       },
@@ -888,15 +907,15 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
     __syncthreads();
     if constexpr (PAIRS) {  // composite = key << 32 | position (stable order)
       for (int i = threadIdx.x; i < (int)len; i += NT) {
-        const K key = *reinterpret_cast<K*>(&s[BS::pad(i)]);
-        s[BS::pad(i)] = (SK(key) << 32) | SK(uint32_t(i));
+        const K key = *reinterpret_cast<K*>(&s[TP(i)]);
+        s[TP(i)] = (SK(key) << 32) | SK(uint32_t(i));
       }
       __syncthreads();
     }
     SQ_CHECK(len <= uint32_t(BS::TILE));
     tile_sort<K, NT, V, PAIRS, BIN>(s, cnt, len);
     for (int i = threadIdx.x; i < (int)len; i += NT) {
-      const SK x = s[BS::pad(i)];
+      const SK x = s[TP(i)];
       if constexpr (PAIRS) {
         out[outpos + lo + i] = K(x >> 32);
         vout[outpos + lo + i] = vs[uint32_t(x)];

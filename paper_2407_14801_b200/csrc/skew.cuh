@@ -128,6 +128,11 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t* total) 
   return x - v;
 }
 
+// cache operator of the producer's 16-byte copies (.ca: the two 16-byte halves of a
+// 32-byte sector are one L2 request; .cg: two)
+#ifndef SQ_TR_CACHE
+#define SQ_TR_CACHE "cg"
+#endif
 template <typename K, bool PAIRS, int S, int F>
 __global__ void __launch_bounds__(WsCfg<K, PAIRS, S, F>::NT, 2)
 k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict__ pcount, const K* __restrict__ src,
@@ -236,7 +241,7 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
           const uint32_t sdst = smem_addr(slot) + so;
           const unsigned char* g = reinterpret_cast<const unsigned char*>(src + srcpos) - mis;
           for (uint32_t v = 0; v < sbytes; v += 16)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
+            asm volatile("cp.async." SQ_TR_CACHE ".shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
           if (PAIRS) {
             const uint32_t* gv = vsrc + srcpos;
             for (uint32_t kk = 0; kk < flen; kk++) cp_async_elem(&vslot[e0 + kk], &gv[kk]);
