@@ -199,6 +199,7 @@ int sq_draw_positions(uint64_t node, uint32_t rounds, uint32_t count, uint64_t n
 int sq_trim_memory(void) {
   return guarded([&] {
     check_device();
+    graph_clear_all();
     SQ_CUDA(cudaMemPoolTrimTo(lib_pool(), 0));
   });
 }

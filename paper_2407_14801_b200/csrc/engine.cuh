@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -241,6 +242,13 @@ static __global__ void k_xfer(const uint8_t* __restrict__ src, uint8_t* __restri
   }
 }
 
+// a level's read-back: the class counts, then the round word, into pinned memory
+static __global__ void k_readback(const uint32_t* __restrict__ count, uint32_t nc, const uint32_t* __restrict__ info,
+                                  uint32_t* __restrict__ out) {
+  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) out[i] = count[i];
+  if (threadIdx.x == 0) out[nc] = info[0];
+}
+
 inline void xfer(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return;
   const uint32_t g = (uint32_t)std::min<size_t>((bytes + 4095) / 4096, 148);
@@ -278,16 +286,35 @@ struct PinnedPool {
 };
 inline thread_local PinnedPool g_pinned;
 
+// Per-call memory: stream-ordered scratch from the library pool and pinned staging
+// from the thread's bump pool.  A bump Arena (graph capture of a level, see
+// GraphCache) instead hands out consecutive pieces of two caller-owned regions and
+// never frees; every Arena counts the bytes it hands out, so that a level's needs
+// are known after one ordinary run.
 struct Arena {
   cudaStream_t st;
   std::vector<void*> dev;
   bool used_host = false;
   cudaMemPool_t pool;
+  size_t dev_bytes = 0, pin_bytes = 0;  // handed out so far (rounded up to 256 bytes)
+  char* bump_dev = nullptr;             // bump mode: regions and capacities
+  char* bump_pin = nullptr;
+  size_t bump_dev_cap = 0, bump_pin_cap = 0;
+  static size_t rnd(size_t b) { return ((b ? b : 16) + 255) & ~size_t(255); }
   explicit Arena(cudaStream_t s) : st(s), pool(lib_pool()) {}
+  Arena(cudaStream_t s, char* d, size_t dcap, char* h, size_t hcap)
+      : st(s), pool(nullptr), bump_dev(d), bump_pin(h), bump_dev_cap(dcap), bump_pin_cap(hcap) {}
   void* alloc(size_t bytes) {
+    if (bump_dev) {
+      if (dev_bytes + rnd(bytes) > bump_dev_cap) throw Error(SQ_ERR_CUDA, "graph scratch region exhausted");
+      void* p = bump_dev + dev_bytes;
+      dev_bytes += rnd(bytes);
+      return p;
+    }
     void* p = nullptr;
     SQ_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, st));
     dev.push_back(p);
+    dev_bytes += rnd(bytes);
     return p;
   }
   void release(void* p) {
@@ -298,7 +325,14 @@ struct Arena {
     }
   }
   void* pinned(size_t bytes) {
+    if (bump_pin) {
+      if (pin_bytes + rnd(bytes) > bump_pin_cap) throw Error(SQ_ERR_CUDA, "graph staging region exhausted");
+      void* p = bump_pin + pin_bytes;
+      pin_bytes += rnd(bytes);
+      return p;
+    }
     used_host = true;
+    pin_bytes += rnd(bytes);
     return g_pinned.get(bytes);
   }
   // Several host arrays in one staging block and one transfer (one k_xfer launch
@@ -604,6 +638,7 @@ struct Engine {
   uint32_t* vb[3];
   size_t n;
   uint32_t cap;
+  int big_mode = g_big_mode;  // this engine's mode for buckets beyond one CTA
 
   Engine(cudaStream_t s, Arena& a, K* keys, uint32_t* vals, size_t n_) : st(s), ar(a), n(n_) {
     kb[0] = keys;
@@ -728,6 +763,59 @@ struct Engine {
   // their final place.  The SkewTranspose writes into the other buffer T; the
   // bucket sorts gather from T and write the sorted buckets back into X.
   void run_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg) {
+    LevelTail lt;
+    if (!launch_level(segs, X, depth, dbg, lt)) return;  // (debug: state copied out)
+    finish_level(lt, X);
+  }
+
+  // What the host needs after a level's launches: the pinned read-back of the class
+  // counts and the round, and where the oversize list lives.
+  struct LevelTail {
+    uint32_t* hcnt = nullptr;
+    uint32_t* hinfo = nullptr;
+    uint32_t ncls = 0, cap_per_list = 0, top_m = 0;
+    const uint32_t* list = nullptr;
+    const BucketRec* recs = nullptr;
+    uint64_t buck_tot = 0;
+    int depth = 0;
+    std::vector<void*> rel;  // scratch released after the read-back
+  };
+
+  // 7. one host read per level: the oversize list (and the round, for stats);
+  // oversize buckets become the next level's batch.
+  void finish_level(LevelTail& lt, int X) {
+    SQ_CUDA(cudaStreamSynchronize(st));
+    g_stats.host_syncs++;
+    if (lt.depth == 0) {
+      g_stats.top_round = lt.hinfo[0] & 0x7fffffffu;
+      g_stats.top_degenerate = lt.hinfo[0] >> 31;
+      g_stats.top_m = lt.top_m;
+    }
+    const uint32_t nos = lt.hcnt[lt.ncls + 1];
+    std::vector<Seg> over;
+    if (nos) {
+      uint32_t* hl = (uint32_t*)ar.pinned(nos * 4);
+      xfer(hl, lt.list + uint64_t(lt.ncls + 1) * lt.cap_per_list, nos * 4, st);
+      BucketRec* hr = (BucketRec*)ar.pinned(lt.buck_tot * sizeof(BucketRec));
+      xfer(hr, lt.recs, lt.buck_tot * sizeof(BucketRec), st);
+      SQ_CUDA(cudaStreamSynchronize(st));
+      g_stats.host_syncs++;
+      for (uint32_t q = 0; q < nos; q++) {
+        const uint32_t e = hl[q];
+        const uint32_t i = item_bucket(e);
+        over.push_back({hr[i].out, hr[i].size, hr[i].node});
+        g_stats.oversize_keys += hr[i].size;
+      }
+    }
+    for (void* p : lt.rel) ar.release(p);
+    htrace("level: done, oversize segments", over.size(), lt.depth);
+    if (!over.empty()) sort_batch(over, X, X, lt.depth + 1, "bucketsort");
+  }
+
+  // Launch every kernel of one level (steps 1-6 and the read-back transfers of step
+  // 7); nothing here waits for the device, so the sequence can be captured in a
+  // CUDA graph.  Returns false when dbg is given (the level state was copied out).
+  bool launch_level(const std::vector<Seg>& segs, int X, int depth, DebugOut* dbg, LevelTail& lt) {
     using TC = PmTr<K, PAIRS>;
     ensure_scratch();
     g_stats.levels++;
@@ -928,14 +1016,14 @@ struct Engine {
     po.ncls = 0;
     int cls_cl[20] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
     {
-      const uint32_t one = g_big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
+      const uint32_t one = big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
       // smallest bucket-sort class 1K keys: smaller chunks share it (their padding is
       // skipped), instead of a latency-bound launch per tiny class
       const uint32_t lower = std::min<uint32_t>(1024u, one);
       for (uint32_t t : kTiles)
         if (t >= lower && t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
       po.max_tile = one;
-      if constexpr (sizeof(SK) <= 8) if (g_big_mode == 2) {  // beyond one CTA: clusters of 4, 8, 16 CTAs
+      if constexpr (sizeof(SK) <= 8) if (big_mode == 2) {  // beyond one CTA: clusters of 4, 8, 16 CTAs
         const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
         for (int cl : {4, 8, 16}) {
           if (cl * ct <= po.max_tile) continue;
@@ -960,10 +1048,18 @@ struct Engine {
     for (uint32_t c = 0; c < po.ncls; c++)
       if (!cls_cl[c]) po.unit_max = std::max(po.unit_max, po.cls_tile[c]);
     if (g_unit_max) po.unit_max = std::min(po.unit_max, g_unit_max);
+    {  // small levels: units small enough that most SMs get one (but >= 4K keys: a
+       // CTA of fewer than 128 threads sorts too slowly to be worth the spread)
+      uint64_t lvl = 0;
+      for (const Seg& g : segs) lvl += g.len;
+      uint32_t u = 4096;
+      while (u < po.unit_max && uint64_t(u) * 2 * num_sms() < lvl) u *= 2;
+      po.unit_max = std::min(po.unit_max, u);
+    }
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     // (u64 pairs have no cluster kernel: mode 2 runs the merge base case for them)
-    const bool merge = g_big_mode == 1 || (g_big_mode == 2 && sizeof(SK) == 16);
+    const bool merge = big_mode == 1 || (big_mode == 2 && sizeof(SK) == 16);
     if (merge) {  // multi-CTA merge sort for buckets of up to 16 chunks
       po.msort_max = 16u * po.max_tile;
       po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
@@ -1001,7 +1097,7 @@ struct Engine {
       uint32_t* dinf = ar.upload(inf);
       SQ_CUDA(cudaMemcpyAsync(dbg->bucend, dbe, buck_tot * 4, cudaMemcpyDeviceToDevice, st));
       SQ_CUDA(cudaMemcpyAsync(dbg->info, dinf, 8, cudaMemcpyDeviceToDevice, st));
-      return;
+      return false;
     }
     // 6. bucket sorts: gather from T, sort on chip, write to X.  The
     // size classes are independent: their kernels run concurrently on side streams.
@@ -1054,15 +1150,18 @@ struct Engine {
       }
     };
 
+    // (the chunk lists are filled only for merge-sorted buckets)
     if (!g_concurrent_classes) {
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, st);
+      if (merge)
+        for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, st);
       for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, st);
       if (merge) launch_merges(st);
     } else {
       // streams 0-1: the chunks of merge-sorted buckets, then (stream 0) the merge
       // passes; streams 2-3: whole buckets and units, which the merges overlap
       int rc = 0, rw = 0;
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, ss.s[rc++ % 2]);
+      if (merge)
+        for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, ss.s[rc++ % 2]);
       for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, ss.s[2 + rw++ % 2]);
       if (merge) {
         stream_wait(ss.s[0], ss.s[1]);
@@ -1078,53 +1177,34 @@ struct Engine {
       const uint64_t ucap = buck_tot + level_keys / kGatherKeys + 16;
       uint2* units = (uint2*)ar.alloc(ucap * sizeof(uint2));
       uint32_t* nun = (uint32_t*)ar.alloc(16);
-      for (uint32_t c = po.ncls; c < po.ncls + 2; c++) {
-        const uint32_t* lst = po.list + uint64_t(c) * po.cap_per_list;
-        k_gather_units<<<1, 1024, 0, st>>>(recs, lst, po.count + c, units, nun);
-        check_launch("k_gather_units");
-        k_bucket_gather_units<K, 256><<<4 * num_sms(), 256, 0, st>>>(
-            recs, dTiles, lst, units, nun, kb[T], kb[X], PAIRS ? vb[T] : nullptr, PAIRS ? vb[X] : nullptr, pout,
-            ppre);
-        check_launch("k_bucket_gather_units");
-      }
+      // both lists (ncls: single-value, ncls + 1: oversize) in one pass
+      const uint32_t* lst = po.list + uint64_t(po.ncls) * po.cap_per_list;
+      k_gather_units<<<1, 1024, 0, st>>>(recs, lst, po.count + po.ncls, 2, po.cap_per_list, units, nun);
+      check_launch("k_gather_units");
+      k_bucket_gather_units<K, 256><<<4 * num_sms(), 256, 0, st>>>(
+          recs, dTiles, lst, po.cap_per_list, units, nun, kb[T], kb[X], PAIRS ? vb[T] : nullptr,
+          PAIRS ? vb[X] : nullptr, pout, ppre);
+      check_launch("k_bucket_gather_units");
       ar.release(nun);
       ar.release(units);
     }
     htrace("level: bucket sorts launched");
-    // 7. one host read per level: the oversize list (and the round, for stats)
-    uint32_t* hcnt = (uint32_t*)ar.pinned((po.ncls + 2) * 4);
-    uint32_t* hinfo = (uint32_t*)ar.pinned(4);
-    xfer(hcnt, po.count, (po.ncls + 2) * 4, st);
-    xfer(hinfo, info, 4, st);
-    SQ_CUDA(cudaStreamSynchronize(st));
-    g_stats.host_syncs++;
-    if (depth == 0) {
-      g_stats.top_round = hinfo[0] & 0x7fffffffu;
-      g_stats.top_degenerate = hinfo[0] >> 31;
-      g_stats.top_m = L[0].k;
-    }
-    const uint32_t nos = hcnt[po.ncls + 1];
-    std::vector<Seg> over;
-    if (nos) {
-      uint32_t* hl = (uint32_t*)ar.pinned(nos * 4);
-      xfer(hl, po.list + uint64_t(po.ncls + 1) * po.cap_per_list, nos * 4, st);
-      BucketRec* hr = (BucketRec*)ar.pinned(buck_tot * sizeof(BucketRec));
-      xfer(hr, recs, buck_tot * sizeof(BucketRec), st);
-      SQ_CUDA(cudaStreamSynchronize(st));
-      g_stats.host_syncs++;
-      for (uint32_t q = 0; q < nos; q++) {
-        const uint32_t e = hl[q];
-        const uint32_t i = item_bucket(e);
-        over.push_back({hr[i].out, hr[i].size, hr[i].node});
-        g_stats.oversize_keys += hr[i].size;
-      }
-    }
-    for (void* p : {(void*)po.units, (void*)po.nunits}) ar.release(p);
-    for (void* p : {(void*)segmat, (void*)pout, (void*)ppre, (void*)recs, (void*)po.list, (void*)po.mlist, (void*)piv,
-                    (void*)flags, (void*)p0s, (void*)info, (void*)fix, (void*)segmin})
-      ar.release(p);
-    htrace("level: done, oversize segments", over.size(), depth);
-    if (!over.empty()) sort_batch(over, X, X, depth + 1, "bucketsort");
+    // 7. the read-back (finish_level): class counts (the oversize list's length) and the round
+    lt.hcnt = (uint32_t*)ar.pinned((po.ncls + 3) * 4);
+    lt.hinfo = lt.hcnt + po.ncls + 2;
+    k_readback<<<1, 64, 0, st>>>(po.count, po.ncls + 2, info, lt.hcnt);
+    check_launch("k_readback");
+    lt.ncls = po.ncls;
+    lt.cap_per_list = po.cap_per_list;
+    lt.list = po.list;
+    lt.recs = recs;
+    lt.buck_tot = buck_tot;
+    lt.top_m = L[0].k;
+    lt.depth = depth;
+    lt.rel = {(void*)po.units, (void*)po.nunits, (void*)segmat, (void*)pout, (void*)ppre, (void*)recs,
+              (void*)po.list, (void*)po.mlist, (void*)piv, (void*)flags, (void*)p0s, (void*)info,
+              (void*)fix, (void*)segmin};
+    return true;
   }
 };
 
@@ -1159,8 +1239,190 @@ inline bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
+// ------------------------------------------------------------------ graph replay of small levels
+// A one-level sort of a small array is bound by the host: the level's ~40 launches,
+// events and stream waits cost ~250 us of API time while its kernels run for a few
+// tens of microseconds.  A call that repeats an earlier one's (device, pointers, n,
+// seed, knobs) replays the level as one CUDA graph: the first call runs normally
+// and records the level's scratch and staging needs, the second captures the
+// level's launches (on a library stream, over entry-owned scratch: a bump Arena)
+// and instantiates the graph, and every later call launches it and does the
+// level's read-back (and any oversize recursion, with ordinary scratch) as usual.
+// Captured levels put buckets beyond one CTA into the next level (mode 0; rare at
+// these sizes) instead of the merge passes.  SQ_GRAPH_MAX_N (default 2^22; 0 = off)
+// bounds n; at most kGraphEntries levels are cached per engine instantiation.
+inline size_t g_graph_max_n = getenv("SQ_GRAPH_MAX_N") ? (size_t)atoll(getenv("SQ_GRAPH_MAX_N")) : (size_t(1) << 22);
+constexpr int kGraphEntries = 4;
+// every instantiation's clear(), for sq_trim_memory
+inline std::mutex g_graph_reg_mu;
+inline std::vector<void (*)()> g_graph_clearers;
+inline void graph_register(void (*f)()) {
+  std::lock_guard<std::mutex> g(g_graph_reg_mu);
+  if (std::find(g_graph_clearers.begin(), g_graph_clearers.end(), f) == g_graph_clearers.end())
+    g_graph_clearers.push_back(f);
+}
+inline void graph_clear_all() {
+  std::vector<void (*)()> fs;
+  {
+    std::lock_guard<std::mutex> g(g_graph_reg_mu);
+    fs = g_graph_clearers;
+  }
+  for (auto f : fs) f();
+}
+
+template <typename K, bool PAIRS, bool BIN>
+struct GraphCache {
+  using E = Engine<K, PAIRS, BIN>;
+  struct Entry {
+    int dev = -1;
+    const void* keys = nullptr;
+    const void* vals = nullptr;
+    size_t n = 0;
+    uint64_t seed = 0, knobs = 0, last = 0;
+    size_t dev_need = 0, pin_need = 0;
+    char* dmem = nullptr;
+    char* hmem = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool busy = false;
+    uint32_t launches = 0;
+    typename E::LevelTail tail;
+    ~Entry() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (dmem) cudaFree(dmem);
+      if (hmem) cudaFreeHost(hmem);
+    }
+  };
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<std::unique_ptr<Entry>>& entries() {
+    static std::vector<std::unique_ptr<Entry>> v;
+    return v;
+  }
+  static uint64_t knobs() {
+    return uint64_t(g_max_tile) ^ (uint64_t(g_unit_max) << 20) ^ (uint64_t(g_concurrent_classes) << 52) ^
+           (uint64_t(g_big_mode) << 56) ^ (uint64_t(g_one_cap) << 1);
+  }
+  static std::vector<Seg> top(size_t n, uint64_t seed) { return {{0, (uint32_t)n, root_key(seed)}}; }
+
+  // true: sorted here; false: the caller runs the ordinary path
+  static bool run(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
+    static const bool reg = (graph_register(&clear), true);
+    (void)reg;
+    const int dev = cur_device();
+    const uint64_t kn = knobs();
+    static uint64_t clock = 0;
+    std::unique_lock<std::mutex> lk(mu());
+    auto& v = entries();
+    Entry* e = nullptr;
+    for (auto& p : v)
+      if (p->dev == dev && p->keys == keys && p->vals == vals && p->n == n && p->seed == seed && p->knobs == kn)
+        e = p.get();
+    if (!e) {  // first call: an ordinary run that records the level's needs
+      lk.unlock();
+      Arena ar(st);
+      E eng(st, ar, keys, vals, n);
+      eng.big_mode = 0;
+      typename E::LevelTail lt;
+      eng.launch_level(top(n, seed), 0, 0, nullptr, lt);
+      const size_t dn = ar.dev_bytes, pn = ar.pin_bytes;
+      eng.finish_level(lt, 0);
+      lk.lock();
+      if (v.size() >= (size_t)kGraphEntries) {  // evict the least recently used idle entry
+        auto it = std::min_element(v.begin(), v.end(), [](auto& a, auto& b) {
+          return (a->busy ? UINT64_MAX : a->last) < (b->busy ? UINT64_MAX : b->last);
+        });
+        if ((*it)->busy) return true;
+        { int cd = cur_device(); cudaSetDevice((*it)->dev); it->reset(); cudaSetDevice(cd); }
+        v.erase(it);
+      }
+      auto ne = std::make_unique<Entry>();
+      ne->dev = dev;
+      ne->keys = keys;
+      ne->vals = vals;
+      ne->n = n;
+      ne->seed = seed;
+      ne->knobs = kn;
+      ne->dev_need = dn;
+      ne->pin_need = pn;
+      ne->last = ++clock;
+      v.push_back(std::move(ne));
+      return true;
+    }
+    if (e->busy) return false;  // another thread replays it: take the ordinary path
+    e->busy = true;
+    e->last = ++clock;
+    lk.unlock();
+    struct Release {
+      Entry* e;
+      ~Release() {
+        std::lock_guard<std::mutex> g(mu());
+        e->busy = false;
+      }
+    } rel{e};
+    if (!e->exec) capture(e, keys, vals, n, seed);
+    SQ_CUDA(cudaGraphLaunch(e->exec, st));
+    g_stats.levels++;
+    g_stats.kernel_launches += e->launches;
+    Arena ar(st);
+    E eng(st, ar, keys, vals, n);
+    typename E::LevelTail lt = e->tail;
+    eng.finish_level(lt, 0);
+    return true;
+  }
+
+  static void capture(Entry* e, K* keys, uint32_t* vals, size_t n, uint64_t seed) {
+    SQ_CUDA(cudaMalloc((void**)&e->dmem, e->dev_need));
+    SQ_CUDA(cudaMallocHost((void**)&e->hmem, e->pin_need));
+    // captured on a library stream of its own (the caller's may be the legacy stream)
+    static thread_local std::map<int, cudaStream_t> cap_stream;
+    cudaStream_t& cs = cap_stream[e->dev];
+    if (!cs) SQ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    SQ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    typename E::LevelTail lt;
+    const uint64_t l0 = g_stats.kernel_launches, lv0 = g_stats.levels;
+    cudaGraph_t g = nullptr;
+    try {
+      Arena ar(cs, e->dmem, e->dev_need, e->hmem, e->pin_need);
+      E eng(cs, ar, keys, vals, n);
+      eng.big_mode = 0;
+      eng.launch_level(top(n, seed), 0, 0, nullptr, lt);
+    } catch (...) {
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    SQ_CUDA(cudaStreamEndCapture(cs, &g));
+    const cudaError_t r = cudaGraphInstantiate(&e->exec, g, 0);
+    cudaGraphDestroy(g);
+    SQ_CUDA(r);
+    e->launches = uint32_t(g_stats.kernel_launches - l0);
+    g_stats.kernel_launches = l0;  // counted again when the graph is launched
+    g_stats.levels = lv0;
+    lt.rel.clear();  // bump scratch: nothing to release
+    e->tail = lt;
+  }
+
+  static void clear() {
+    std::lock_guard<std::mutex> g(mu());
+    auto& v = entries();
+    const int cd = cur_device();
+    for (auto it = v.begin(); it != v.end();) {
+      if ((*it)->busy) { ++it; continue; }
+      cudaSetDevice((*it)->dev);
+      it = v.erase(it);
+    }
+    cudaSetDevice(cd);
+  }
+};
+
 template <typename K, bool PAIRS, bool BIN>
 void sort_engine(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
+  // (levels with the default knobs only: a forced tile or big-bucket mode runs as asked)
+  if (n <= g_graph_max_n && !g_prof.load() && n > key_max_tile<sortkey_t<K, PAIRS>>() && !g_max_tile &&
+      g_big_mode == 1 && GraphCache<K, PAIRS, BIN>::run(keys, vals, n, seed, st))
+    return;
   Arena ar(st);
   Engine<K, PAIRS, BIN> eng(st, ar, keys, vals, n);
   std::vector<Seg> top = {{0, (uint32_t)n, root_key(seed)}};

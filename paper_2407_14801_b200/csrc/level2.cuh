@@ -1151,18 +1151,24 @@ constexpr uint32_t kGatherKeys = 65536;
 
 static __global__ void __launch_bounds__(1024)
 k_gather_units(const BucketRec* __restrict__ recs, const uint32_t* __restrict__ list,
-               const uint32_t* __restrict__ count, uint2* __restrict__ units, uint32_t* __restrict__ nunits) {
+               const uint32_t* __restrict__ count, uint32_t nlists, uint32_t list_stride, uint2* __restrict__ units,
+               uint32_t* __restrict__ nunits) {
+  // units of the lists [0, nlists) (list l at list + l * list_stride, count[l] items):
+  // unit = (item | l << 31, part)
   __shared__ uint32_t misc[64];
-  const uint32_t total = *count;
   uint32_t carry = 0;
-  for (uint32_t c0 = 0; c0 < total; c0 += 1024) {
-    const uint32_t it = c0 + threadIdx.x;
-    uint32_t parts = 0;
-    if (it < total) parts = max(1u, (recs[item_bucket(list[it])].size + kGatherKeys - 1) / kGatherKeys);
-    uint32_t tot;
-    const uint32_t ex = block_excl_sum<32>(parts, misc, &tot);
-    for (uint32_t q = 0; q < parts; q++) units[carry + ex + q] = make_uint2(it, q);
-    carry += tot;
+  for (uint32_t l = 0; l < nlists; l++) {
+    const uint32_t total = count[l];
+    const uint32_t* li = list + uint64_t(l) * list_stride;
+    for (uint32_t c0 = 0; c0 < total; c0 += 1024) {
+      const uint32_t it = c0 + threadIdx.x;
+      uint32_t parts = 0;
+      if (it < total) parts = max(1u, (recs[item_bucket(li[it])].size + kGatherKeys - 1) / kGatherKeys);
+      uint32_t tot;
+      const uint32_t ex = block_excl_sum<32>(parts, misc, &tot);
+      for (uint32_t q = 0; q < parts; q++) units[carry + ex + q] = make_uint2(it | (l << 31), q);
+      carry += tot;
+    }
   }
   if (threadIdx.x == 0) *nunits = carry;
 }
@@ -1172,7 +1178,7 @@ k_gather_units(const BucketRec* __restrict__ recs, const uint32_t* __restrict__ 
 template <typename K, int NT>
 __global__ void __launch_bounds__(NT)
 k_bucket_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ tiles,
-                      const uint32_t* __restrict__ list, const uint2* __restrict__ units,
+                      const uint32_t* __restrict__ list, uint32_t list_stride, const uint2* __restrict__ units,
                       const uint32_t* __restrict__ nunits, const K* __restrict__ src, K* __restrict__ dst,
                       const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
                       const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
@@ -1180,7 +1186,7 @@ k_bucket_gather_units(const BucketRec* __restrict__ recs, const TileInfo* __rest
   const uint32_t total = *nunits;
   for (uint32_t u = blockIdx.x; u < total; u += gridDim.x) {
     const uint2 un = units[u];
-    const BucketRec rc = recs[item_bucket(list[un.x])];
+    const BucketRec rc = recs[item_bucket(list[uint64_t(un.x >> 31) * list_stride + (un.x & 0x7fffffffu)])];
     const TileInfo ti = tiles[rc.tile];
     const uint32_t lo = un.y * kGatherKeys, hi = min(rc.size, lo + kGatherKeys);
     K* out = dst + rc.out + lo;
