@@ -29,6 +29,13 @@
  *    and freed into that pool before return.  The pool keeps freed scratch
  *    reserved so a repeated sort does not re-map it; sq_trim_memory() returns
  *    it to the system.
+ *  - Repeated small sorts (n <= 2^22 by default, env SQ_GRAPH_MAX_N; default
+ *    knobs): the second call with the same device, key/value pointers, n and
+ *    seed captures the level's launches into a CUDA graph over scratch the
+ *    library keeps for it (about 3n keys + metadata, at most 4 levels per key
+ *    type), and later such calls replay it -- the result is the same sort of
+ *    the buffer's current contents, with ~40 fewer host API calls.
+ *    sq_trim_memory() drops those graphs and their scratch.
  *  - Errors are return codes only (sq_status); nothing is printed, no
  *    exception crosses the ABI.  sq_last_error_message() gives detail for the
  *    calling thread's last non-OK return.
@@ -209,8 +216,10 @@ typedef struct {
 } sq_stats;
 
 /* Release the scratch the library's pool on the current device keeps reserved
- * between calls (cudaMemPoolTrimTo 0).  Safe to call at any time; memory of
- * calls still in flight on other streams stays mapped until they finish. */
+ * between calls (cudaMemPoolTrimTo 0), and the cached graphs of small levels
+ * with their scratch (graphs being replayed by another thread stay).  Safe to
+ * call at any time; memory of calls still in flight on other streams stays
+ * mapped until they finish. */
 int sq_trim_memory(void);
 
 /* Statistics of the calling thread's last sort / transpose call. */
