@@ -180,9 +180,11 @@ inline int g_big_mode = 1;
 // serialises them on the caller's stream; measured 6.47 vs 6.61 ms at cfg5)
 inline int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv("SQ_CONCURRENT_CLASSES")) : 1;
 
-// on-chip base case for keys-only 32-bit sorts: 1 = counting sort + network
-// fix-up (binsort.cuh, default), 0 = merge sort (blocksort.cuh)
+// on-chip base case for 32- and 64-bit sort keys (keys, u32-key pairs): 1 = counting
+// sort + network fix-up (binsort.cuh, default, where its shared memory fits),
+// 0 = merge sort (blocksort.cuh)
 inline int g_base_case = getenv("SQ_BASE_CASE") ? atoi(getenv("SQ_BASE_CASE")) : 1;
+constexpr size_t kMaxSmem = 232448;  // dynamic shared memory per CTA on sm_100 (227 KB)
 template <bool B, typename F>
 void with_bin(F&& f) {
   f(std::integral_constant<bool, B>{});
@@ -935,9 +937,10 @@ struct Engine {
         with_tile<SK>(cd.first, [&](auto nt, auto v) {
           constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
           using BS = BlockSort<SK, NT, V>;
-          with_bin<BIN && std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
+          constexpr size_t base = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
+          with_bin<BIN && base + bin_smem<K, NT, V, PAIRS, BIN>() <= kMaxSmem>([&](auto bin) {
           constexpr bool UB = decltype(bin)::value;
-          const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + bin_smem<K, NT, V, PAIRS, UB>();
+          const size_t smem = base + bin_smem<K, NT, V, PAIRS, UB>();
           set_smem(k_colsort<K, NT, V, PAIRS, UB>, smem);
           ProfScope ps("colsort", st);
           auto f = k_colsort<K, NT, V, PAIRS, UB>;
@@ -1118,10 +1121,10 @@ struct Engine {
       with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
         constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
         using BS = BlockSort<SK, NT, V>;
-        with_bin<BIN && std::is_same<K, uint32_t>::value && !PAIRS>([&](auto bin) {
+        constexpr size_t base = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4;
+        with_bin<BIN && base + bin_smem<K, NT, V, PAIRS, BIN>() <= kMaxSmem>([&](auto bin) {
         constexpr bool UB = decltype(bin)::value;
-        const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4 +
-                            bin_smem<K, NT, V, PAIRS, UB>();
+        const size_t smem = base + bin_smem<K, NT, V, PAIRS, UB>();
         auto f = k_bucketsort<K, NT, V, PAIRS, UB>;
         const int grid = wave_grid(f, NT, smem);
         std::optional<ProfScope> ps;
@@ -1450,7 +1453,9 @@ void debug_level_engine(const K* src, K* dst, size_t n, uint64_t seed, K* pivots
   X template void sort_engine<uint32_t, false, true>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint32_t, false, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint64_t, false, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void sort_engine<uint64_t, false, true>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint32_t, true, false>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
+  X template void sort_engine<uint32_t, true, true>(uint32_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void sort_engine<uint64_t, true, false>(uint64_t*, uint32_t*, size_t, uint64_t, cudaStream_t); \
   X template void debug_level_engine<uint32_t, true>(const uint32_t*, uint32_t*, size_t, uint64_t, uint32_t*,   \
                                                      uint32_t*, uint32_t*, cudaStream_t);                     \
@@ -1463,7 +1468,7 @@ SQ_ENGINE_INSTANCES(extern)
 // Sort on the device with the selected base case (sq_set_base_case).
 template <typename K, bool PAIRS>
 void sort_device(K* keys, uint32_t* vals, size_t n, uint64_t seed, cudaStream_t st) {
-  if constexpr (std::is_same<K, uint32_t>::value && !PAIRS) {
+  if constexpr (sizeof(sortkey_t<K, PAIRS>) <= 8) {
     if (g_base_case) return sort_engine<K, PAIRS, true>(keys, vals, n, seed, st);
   }
   sort_engine<K, PAIRS, false>(keys, vals, n, seed, st);

@@ -69,29 +69,34 @@ constexpr int kMaxPasses = 4;  // 16 chunks
 
 constexpr int kPP = kTB + 1;  // prefix entries per piece
 
-// The counting-sort base case (binsort.cuh) serves keys-only 32-bit sorts with 16
-// or 32 keys per thread; everything else uses the merge sort (blocksort.cuh).
+// The counting-sort base case (binsort.cuh) serves 32-bit sort keys with 16 or 32
+// keys per thread and 64-bit sort keys (u64 keys, u32-key pair composites) with 16;
+// everything else (fewer keys per thread, u64-key pair composites) uses the merge
+// sort (blocksort.cuh).
 template <typename K, int V, bool PAIRS>
 __host__ __device__ constexpr bool bin_ok() {
-  return std::is_same<K, uint32_t>::value && !PAIRS && (V == 16 || V == 32);
+  using SK = sortkey_t<K, PAIRS>;
+  return sizeof(SK) == 4 ? (V == 16 || V == 32) : (sizeof(SK) == 8 && V == 16);
 }
+template <typename K, int NT, int V, bool PAIRS>
+using BinSortOf = BinSort<sortkey_t<K, PAIRS>, NT, V>;
 // shared memory of the counting sort's counters (0 when the merge sort runs)
 template <typename K, int NT, int V, bool PAIRS, bool BIN>
 __host__ __device__ constexpr size_t bin_smem() {
-  if constexpr (BIN && bin_ok<K, V, PAIRS>()) return BinSort<NT, V>::CNT_BYTES;
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) return BinSortOf<K, NT, V, PAIRS>::CNT_BYTES;
   else return 0;
 }
 // Physical slot of tile position i in the sort kernels' shared-memory tile: the
 // counting sort's swizzled rows, else the merge sort's padded layout.
 template <typename K, int NT, int V, bool PAIRS, bool BIN>
 __device__ __forceinline__ uint32_t tpos(uint32_t i) {
-  if constexpr (BIN && bin_ok<K, V, PAIRS>()) return swz32(i);
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) return BinSortOf<K, NT, V, PAIRS>::pad(i);
   else return BlockSort<sortkey_t<K, PAIRS>, NT, V>::pad(i);
 }
 // Sort the tile in shared memory with the selected base case.
 template <typename K, int NT, int V, bool PAIRS, bool BIN, typename SK>
 __device__ __forceinline__ void tile_sort(SK* s, uint32_t* cnt, uint32_t len) {
-  if constexpr (BIN && bin_ok<K, V, PAIRS>()) BinSort<NT, V>::sort_smem(reinterpret_cast<uint32_t*>(s), cnt, len);
+  if constexpr (BIN && bin_ok<K, V, PAIRS>()) BinSortOf<K, NT, V, PAIRS>::sort_smem(s, cnt, len);
   else BlockSort<SK, NT, V>::sort_smem(s, len);
 }
 
@@ -183,7 +188,8 @@ struct ColDesc {
 // resident CTAs per SM the counting-sort kernels are compiled for (64 registers)
 template <typename K, int NT, int V, bool PAIRS, bool BIN>
 __host__ __device__ constexpr int bin_min_blocks() {
-  return (BIN && bin_ok<K, V, PAIRS>()) ? (NT >= 1024 ? 1 : 1024 / NT) : 1;
+  // (64-bit sort keys: no register cap; their tiles' shared memory allows ~1 CTA per SM)
+  return (BIN && bin_ok<K, V, PAIRS>() && sizeof(sortkey_t<K, PAIRS>) == 4) ? (NT >= 1024 ? 1 : 1024 / NT) : 1;
 }
 
 template <typename K, int NT, int V, bool PAIRS, bool BIN>
@@ -203,21 +209,28 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
   constexpr bool VEC = !PAIRS && NV >= 1 && NV * NT * VW == BS::TILE;
   const bool vec_ok = VEC && d.len == BS::TILE && (reinterpret_cast<uintptr_t>(keys + d.off) & 15) == 0;
   bool sorted = false;
-  if constexpr (BIN && bin_ok<K, V, PAIRS>()) {
+  // the counting sort's counters follow the tile (and, for pairs, the values)
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0));
+  if constexpr (BIN && bin_ok<K, V, PAIRS>() && !PAIRS) {
     if (vec_ok) {  // full, aligned column: straight from 16-byte loads into the sort's registers
       static_assert(NV * VW == V, "vector loads fill the thread's keys");
-      uint32_t r[V];
+      K r[V];
       const uint4* g = reinterpret_cast<const uint4*>(keys + d.off);
 #pragma unroll
       for (int q = 0; q < NV; q++) {
         const uint4 x = g[threadIdx.x + q * NT];
-        r[4 * q] = x.x;
-        r[4 * q + 1] = x.y;
-        r[4 * q + 2] = x.z;
-        r[4 * q + 3] = x.w;
+        if constexpr (sizeof(K) == 4) {
+          r[4 * q] = x.x;
+          r[4 * q + 1] = x.y;
+          r[4 * q + 2] = x.z;
+          r[4 * q + 3] = x.w;
+        } else {
+          r[2 * q] = (uint64_t(x.y) << 32) | x.x;
+          r[2 * q + 1] = (uint64_t(x.w) << 32) | x.z;
+        }
       }
-      BinSort<NT, V>::sort_regs(r, reinterpret_cast<uint32_t*>(s), reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES),
-                                d.len, [&](int j) { return (threadIdx.x + (j / 4) * NT) * 4 + (j % 4); });
+      BinSortOf<K, NT, V, PAIRS>::sort_regs(r, s, cnt, d.len,
+                                            [&](int j) { return (threadIdx.x + (j / VW) * NT) * VW + (j % VW); });
       sorted = true;
     }
   }
@@ -250,7 +263,7 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
       }
     }
     __syncthreads();
-    tile_sort<K, NT, V, PAIRS, BIN>(s, reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES), d.len);
+    tile_sort<K, NT, V, PAIRS, BIN>(s, cnt, d.len);
   }
   // (programmatic dependent launch) the sampler must be done reading the unsorted
   // input, and the pivots must be selected, before this CTA writes or reads them
@@ -260,11 +273,11 @@ k_colsort(const ColDesc* __restrict__ cols, const LevelSeg* __restrict__ segs, K
     else return s[TP(i)];
   };
   bool stored = false;
-  if constexpr (BIN && bin_ok<K, V, PAIRS>()) {
+  if constexpr (BIN && bin_ok<K, V, PAIRS>() && !PAIRS) {
     if (vec_ok) {  // 16-byte chunks of the swizzled tile
       uint4* g = reinterpret_cast<uint4*>(keys + d.off);
-      for (uint32_t c = threadIdx.x; c < uint32_t(BS::TILE) / 4; c += NT)
-        g[c] = BinSort<NT, V>::chunk(reinterpret_cast<uint32_t*>(s), c);
+      for (uint32_t c = threadIdx.x; c < uint32_t(BS::TILE) / VW; c += NT)
+        g[c] = BinSortOf<K, NT, V, PAIRS>::chunk(s, c);
       stored = true;
     }
   }
