@@ -13,7 +13,8 @@ ROLE = [("k_tile_bucket_plan", "plan"), ("k_colsort", "colsort"), ("k_transpose"
         ("k_select", "select"), ("k_segmat", "segmat"), ("k_tile", "tiles"), ("k_piece_plan", "tiles"),
         ("k_bucket_sizes", "plan"), ("k_bucket_offsets", "plan"), ("k_bucket_plan", "plan"),
         ("k_bucket_gather", "gather"), ("k_blocksort", "smallsort"), ("k_colmin", "colmin"),
-        ("k_unit_plan", "plan"), ("k_xfer", "xfer"), ("k_gather_units", "gather")]
+        ("k_unit_plan", "plan"), ("k_xfer", "xfer"), ("k_readback", "xfer"), ("k_gather_units", "gather"),
+        ("k_binsort_cluster", "bucketsort")]
 
 
 def role_of(name):
