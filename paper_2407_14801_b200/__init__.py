@@ -333,11 +333,12 @@ def set_max_tile(t: int):
     _check(lib().sq_set_max_tile(t))
 
 
-BIG_LEVEL, BIG_MERGE, BIG_CLUSTER = 0, 1, 2
+BIG_LEVEL, BIG_MERGE, BIG_CLUSTER, BIG_BINCLUSTER = 0, 1, 2, 3
 
 
 def set_big_bucket_mode(mode: int):
-    """0: recurse into a SquareSort level, 1: multi-CTA merge sort (default), 2: clusters."""
+    """0: recurse into a SquareSort level, 1: multi-CTA merge sort (default), 2: clusters
+    merging through DSMEM, 3: clusters of counting-sort tiles (u32 keys; others: 1)."""
     _check(lib().sq_set_big_bucket_mode(mode))
 
 

@@ -14,7 +14,7 @@ OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libsquaresort.so")
 SOURCES = ["api.cu", "inst_u32.cu", "inst_u32m.cu", "inst_u64.cu", "inst_u64b.cu", "inst_pairs.cu", "inst_pairsb.cu",
            "inst_pairs64.cu"]
-HEADERS = ["engine.cuh", "common.cuh", "blocksort.cuh", "binsort.cuh", "level.cuh", "level2.cuh", "skew.cuh"]
+HEADERS = ["engine.cuh", "common.cuh", "blocksort.cuh", "binsort.cuh", "binclust.cuh", "level.cuh", "level2.cuh", "skew.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC"] + os.environ.get("SQ_NVCC_EXTRA", "").split()
 

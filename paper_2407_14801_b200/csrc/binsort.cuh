@@ -210,9 +210,11 @@ struct BinSort {
           mn = r[j] < mn ? r[j] : mn;
           mx = r[j] > mx ? r[j] : mx;
         }
-      // padding positions of the sorted tile (the scatter fills [0, len))
-      for (uint32_t i = t; i < uint32_t(TILE) - len; i += NT) s[pad(len + i)] = KeyTraits<K>::kMax;
     }
+    // padding positions of the sorted tile (the scatter fills [0, len)); every thread
+    // takes part, whichever of them hold keys past len
+    if (len < uint32_t(TILE))
+      for (uint32_t i = t; i < uint32_t(TILE) - len; i += NT) s[pad(len + i)] = KeyTraits<K>::kMax;
     mn = warp_min(mn);
     mx = warp_max(mx);
     if (lane == 0) {

@@ -27,6 +27,7 @@
 
 #include "../../include/squaresort.h"
 #include "skew.cuh"
+#include "binclust.cuh"
 
 namespace sq {
 
@@ -175,7 +176,7 @@ inline void htrace(const char* what, size_t a = 0, size_t b = 0) {
 inline uint32_t g_max_tile = 0;  // 0 = default
 // buckets larger than one CTA's tile: 0 = another SquareSort level,
 // 1 = multi-CTA merge sort (default), 2 = thread-block cluster sort
-inline int g_big_mode = 1;
+inline int g_big_mode = getenv("SQ_BIG_MODE") ? atoi(getenv("SQ_BIG_MODE")) : 1;
 // bucket-sort size classes run concurrently on side streams (SQ_CONCURRENT_CLASSES=0
 // serialises them on the caller's stream; measured 6.47 vs 6.61 ms at cfg5)
 inline int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv("SQ_CONCURRENT_CLASSES")) : 1;
@@ -376,6 +377,8 @@ struct Arena {
     }
   }
 };
+
+constexpr int kBinClusterTag = 100;  // cls_cl entries above it: counting-sort clusters of (entry - tag) CTAs
 
 // ------------------------------------------------------------------ size classes
 // On-chip tiles (threads x keys per thread) for 32-bit sort keys and for
@@ -745,6 +748,53 @@ struct Engine {
     check_launch("k_clustersort");
   }
 
+  // Clusters of CL counting-sort tiles (mode 3, 32-bit keys): one cluster per bucket,
+  // persistent over the class list; skewed buckets go to the oversize list.
+  template <int CL>
+  void launch_bincluster_t(cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
+                           const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
+                           uint32_t* ovl, uint32_t* ovc, uint32_t nbuck) {
+    if constexpr (std::is_same<K, uint32_t>::value && !PAIRS) {
+      auto f = k_binsort_cluster<CL>;
+      constexpr size_t smem = BinClusterCfg::SMEM;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.blockDim = dim3(BinClusterCfg::NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = cs;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      set_smem(f, smem);
+      static int max_clusters[64] = {0};  // per device ordinal
+      const int dev = cur_device();
+      int& mc = max_clusters[dev & 63];
+      if (mc <= 0) {
+        cfg.gridDim = dim3(CL * num_sms());
+        SQ_CUDA(cudaOccupancyMaxActiveClusters(&mc, f, &cfg));
+        if (mc <= 0) throw Error(SQ_ERR_CUDA, "cluster of " + std::to_string(CL) + " counting-sort tiles cannot be scheduled");
+      }
+      cfg.gridDim = dim3(CL * std::min<uint32_t>(mc, nbuck));
+      std::optional<ProfScope> ps;
+      if (!g_concurrent_classes) ps.emplace("bucketsort", cs);
+      SQ_CUDA(cudaLaunchKernelEx(&cfg, f, recs, tiles, lst, cnt, (const uint32_t*)kb[T], (uint32_t*)kb[X], pout, ppre,
+                                 ovl, ovc));
+      check_launch("k_binsort_cluster");
+    } else {
+      throw Error(SQ_ERR_CUDA, "counting-sort clusters serve 32-bit keys only");
+    }
+  }
+  void launch_bincluster(int cl, cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
+                         const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
+                         uint32_t* ovl, uint32_t* ovc, uint32_t nbuck) {
+    if (cl == 2) launch_bincluster_t<2>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, ovl, ovc, nbuck);
+    else if (cl == 4) launch_bincluster_t<4>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, ovl, ovc, nbuck);
+    else launch_bincluster_t<8>(cs, lst, cnt, recs, tiles, T, X, pout, ppre, ovl, ovc, nbuck);
+  }
+
   // cl > 0: clusters of `cl` small tiles; cl < 0: clusters of -cl big tiles
   void launch_cluster(int cl, cudaStream_t cs, const uint32_t* lst, const uint32_t* cnt, const BucketRec* recs,
                       const TileInfo* tiles, int T, int X, const uint32_t* pout, const uint16_t* ppre,
@@ -1015,18 +1065,29 @@ struct Engine {
     }
     htrace("level: transpose launched");
     // 5. bucket plan: sizes, final offsets, work lists
+    // mode 3 (clusters of counting-sort tiles) serves 32-bit keys with the counting
+    // sort; other engines and forced tiles run mode 1 instead
+    const bool bincl = big_mode == 3 && std::is_same<SK, uint32_t>::value && BIN && !g_max_tile;
+    const int mode = big_mode == 3 && !bincl ? 1 : big_mode;
     PlanOut po{};
     po.ncls = 0;
     int cls_cl[20] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
     {
-      const uint32_t one = big_mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap;
+      const uint32_t one = bincl ? std::min<uint32_t>(cap, BinClusterCfg::TILE)
+                           : (mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap);
       // smallest bucket-sort class 1K keys: smaller chunks share it (their padding is
       // skipped), instead of a latency-bound launch per tiny class
       const uint32_t lower = std::min<uint32_t>(1024u, one);
       for (uint32_t t : kTiles)
         if (t >= lower && t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
       po.max_tile = one;
-      if constexpr (sizeof(SK) <= 8) if (big_mode == 2) {  // beyond one CTA: clusters of 4, 8, 16 CTAs
+      if (bincl)  // beyond one CTA: clusters of 2, 4, 8 counting-sort tiles (binclust.cuh)
+        for (int cl : {2, 4, 8}) {
+          cls_cl[po.ncls] = kBinClusterTag + cl;
+          po.cls_tile[po.ncls++] = BinClusterCfg::cap(cl);
+          po.max_tile = BinClusterCfg::cap(cl);
+        }
+      if constexpr (sizeof(SK) <= 8) if (mode == 2) {  // beyond one CTA: clusters of 4, 8, 16 CTAs
         const uint32_t ct = std::min<uint32_t>(ClusterCfg<SK>::TILE, cap);
         for (int cl : {4, 8, 16}) {
           if (cl * ct <= po.max_tile) continue;
@@ -1062,7 +1123,7 @@ struct Engine {
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     // (u64 pairs have no cluster kernel: mode 2 runs the merge base case for them)
-    const bool merge = big_mode == 1 || (big_mode == 2 && sizeof(SK) == 16);
+    const bool merge = mode == 1 || (mode == 2 && sizeof(SK) == 16);
     if (merge) {  // multi-CTA merge sort for buckets of up to 16 chunks
       po.msort_max = 16u * po.max_tile;
       po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
@@ -1114,6 +1175,12 @@ struct Engine {
     ForkJoin fj(st, ss);
     auto launch_class = [&](int c, uint32_t li, cudaStream_t cs) {
       const uint32_t* lst = po.list + uint64_t(li) * po.cap_per_list;
+      if (cls_cl[c] > kBinClusterTag) {
+        launch_bincluster(cls_cl[c] - kBinClusterTag, cs, lst, po.count + li, recs, dTiles, T, X, pout, ppre,
+                          po.list + uint64_t(po.ncls + 1) * po.cap_per_list, po.count + po.ncls + 1,
+                          (uint32_t)buck_tot);
+        return;
+      }
       if (cls_cl[c]) {
         launch_cluster(cls_cl[c], cs, lst, po.count + li, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
         return;

@@ -534,3 +534,34 @@ def test_concurrent_calls_two_threads():
     assert not errs
     for a, o in zip(arrs, outs):
         assert np.array_equal(o, np.sort(a))
+
+
+# ---------------------------------------------------------------- counting-sort clusters (mode 3)
+@pytest.mark.parametrize("lg", [24, 26])
+def test_bincluster_mode_uniform(lg):
+    # m = 4096 / 8192: buckets of 16K-128K keys go to clusters of 2, 4, 8 counting-sort tiles
+    sq.set_big_bucket_mode(sq.BIG_BINCLUSTER)
+    keys = S.uniform_u32(1 << lg, 40 + lg)
+    assert np.array_equal(gpu_sort(keys, 3), np.sort(keys))
+
+
+def test_bincluster_mode_skewed_falls_back_to_next_level():
+    # heavy values inside buckets make a value range larger than one tile: those
+    # buckets go to the next SquareSort level (oversize), the sort stays exact
+    sq.set_big_bucket_mode(sq.BIG_BINCLUSTER)
+    n = 1 << 26
+    rng = np.random.default_rng(77)
+    keys = S.uniform_u32(n, 77)
+    heavy = rng.integers(0, 2**32, 200, dtype=np.uint64).astype(np.uint32)
+    pos = rng.choice(n, 200 * 12000, replace=False)
+    keys[pos] = np.repeat(heavy, 12000)
+    assert np.array_equal(gpu_sort(keys, 9), np.sort(keys))
+    assert sq.get_stats()["oversize_keys"] > 0
+
+
+def test_bincluster_mode_level_state_vs_oracle():
+    # the whole sort at cfg-like shape against the oracle itself (2^22: m = 2048)
+    sq.set_big_bucket_mode(sq.BIG_BINCLUSTER)
+    keys = S.uniform_u32(1 << 22, 12)
+    want, _ = oracle_sort(keys, 12)
+    assert np.array_equal(gpu_sort(keys, 12), want)
