@@ -237,7 +237,10 @@ int sq_set_max_tile(uint32_t max_tile);
  * (P:291-293); 1 (default): the multi-CTA base case -- chunks sorted on chip,
  * then merge passes through HBM, up to 16 chunks (larger buckets recurse);
  * 2: thread-block clusters of 4/8/16 CTAs merging through distributed shared
- * memory.  Process-wide; SQ_ERR_INVALID_ARGUMENT for other values. */
+ * memory; 3: for 32-bit keys with the counting-sort base case, thread-block
+ * clusters of 2/4/8 counting-sort tiles that split the bucket into value ranges
+ * through distributed shared memory (buckets up to 8 x 16128 keys; other key
+ * types run mode 1).  Process-wide; SQ_ERR_INVALID_ARGUMENT for other values. */
 int sq_set_big_bucket_mode(int mode);
 
 /* Tuning/test knob: the on-chip base case of keys-only 32-bit sorts (the GPU's
