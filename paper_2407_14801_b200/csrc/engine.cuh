@@ -964,9 +964,11 @@ struct Engine {
     with_tile<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
       constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
       using BS = BlockSort<K, NT, V>;
-      set_smem(k_sample_all<K, NT, V>, BS::SMEM_BYTES);
+      constexpr bool SB = BIN && BS::SMEM_BYTES + bin_smem<K, NT, V, false, BIN>() <= kMaxSmem;
+      constexpr size_t smem = BS::SMEM_BYTES + bin_smem<K, NT, V, false, SB>();
+      set_smem(k_sample_all<K, NT, V, SB>, smem);
       ProfScope ps("sample", st);
-      k_sample_all<K, NT, V><<<ns * kCap, NT, BS::SMEM_BYTES, st>>>(dL, kb[X], cand, flags, p0s);
+      k_sample_all<K, NT, V, SB><<<ns * kCap, NT, smem, st>>>(dL, kb[X], cand, flags, p0s);
       check_launch("k_sample_all");
     });
     {

@@ -104,34 +104,43 @@ __device__ __forceinline__ void tile_sort(SK* s, uint32_t* cnt, uint32_t len) {
 // All kCap sampling rounds of every segment in parallel (CTA = (segment, round)),
 // drawn from the level input A before the column sort (L9).  Stores the sorted
 // candidates, whether they are strictly increasing, and their smallest value.
-template <typename K, int NT, int V>
+// BIN: the candidates are sorted by the counting sort (binsort.cuh) where it serves
+// the key type and shape, else by the merge sort.
+template <typename K, int NT, int V, bool BIN = false>
 __global__ void __launch_bounds__(NT)
 k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* __restrict__ cand,
              uint8_t* __restrict__ flags, K* __restrict__ p0s) {
   using BS = BlockSort<K, NT, V>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  auto TP = [](uint32_t i) { return tpos<K, NT, V, false, BIN>(i); };
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the selection may launch now
   const uint32_t seg = blockIdx.x / kCap, r = blockIdx.x % kCap;
   const LevelSeg sg = segs[seg];
   const uint32_t np = sg.k - 1;
   const K* lvl = data + sg.off;
-  for (int i = threadIdx.x; i < BS::TILE; i += NT) {
-    K x = KeyTraits<K>::kMax;
-    if (i < (int)np) x = lvl[draw_index(draw(sg.node, r, (uint32_t)i), sg.len)];
-    s[BS::pad(i)] = x;
+  {  // every random read of the thread in flight at once (they are DRAM-latency bound)
+    K x[V];
+#pragma unroll
+    for (int j = 0; j < V; j++) {
+      const uint32_t i = threadIdx.x + uint32_t(j) * NT;
+      x[j] = i < np ? __ldg(&lvl[draw_index(draw(sg.node, r, i), sg.len)]) : KeyTraits<K>::kMax;
+    }
+#pragma unroll
+    for (int j = 0; j < V; j++) s[TP(threadIdx.x + uint32_t(j) * NT)] = x[j];
   }
   __syncthreads();
-  BS::sort_smem(s, np);
+  tile_sort<K, NT, V, false, BIN>(s, cnt, np);
   int viol = 0;
   for (int i = threadIdx.x + 1; i < (int)np; i += NT)
-    if (!(s[BS::pad(i - 1)] < s[BS::pad(i)])) viol = 1;
+    if (!(s[TP(i - 1)] < s[TP(i)])) viol = 1;
   const bool distinct = !__syncthreads_or(viol);
   K* out = cand + sg.cand_base + uint64_t(r) * np;
-  for (int i = threadIdx.x; i < (int)np; i += NT) out[i] = s[BS::pad(i)];
+  for (int i = threadIdx.x; i < (int)np; i += NT) out[i] = s[TP(i)];
   if (threadIdx.x == 0) {
     flags[uint64_t(seg) * kCap + r] = distinct ? 1 : 2;
-    p0s[uint64_t(seg) * kCap + r] = np ? s[BS::pad(0)] : KeyTraits<K>::kMax;
+    p0s[uint64_t(seg) * kCap + r] = np ? s[TP(0)] : KeyTraits<K>::kMax;
   }
 }
 
