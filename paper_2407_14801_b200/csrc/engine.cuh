@@ -902,7 +902,7 @@ struct Engine {
       segmat_tot += uint64_t(m) * (l.nbt + 1);
       cand_tot += uint64_t(kCap) * np;
       tile_base[s] = (uint32_t)tiles.size();
-      for (uint32_t bt = 0; bt < l.nbt; bt++) tiles.push_back({s, bt, 0, 0, 0, 0});
+      for (uint32_t bt = 0; bt < l.nbt; bt++) tiles.push_back({s, bt, 0, 0, 0, 0, 0});
       // windows per tile (plan_fw): at most ceil(m / kPlanFW) + size * 32 / (31 S) + 2
       const uint32_t gpt = (m + kPlanFW - 1) / kPlanFW + 2;
       piece_seg_base[s] = (uint32_t)piece_tot;
@@ -1038,23 +1038,21 @@ struct Engine {
     SQ_CUDA(cudaMemsetAsync(bsize, 0, buck_tot * 4, st));
     {
       ProfScope ps("tiles", st);
-      k_tile_sizes<<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat);
+      k_tile_sizes<TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat);
       check_launch("k_tile_sizes");
       k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, kPlanFW, dPieceBase);
       check_launch("k_tile_scan");
     }
     {
       PieceDesc* pieces = (PieceDesc*)ar.alloc(piece_tot * sizeof(PieceDesc));
-      uint32_t* pcount = (uint32_t*)ar.alloc(16);  // [0] pieces, [1] tile tickets
-      SQ_CUDA(cudaMemsetAsync(pcount, 0, 8, st));
-      unsigned long long* pstatus = (unsigned long long*)ar.alloc(uint64_t(ntiles) * 8);
-      SQ_CUDA(cudaMemsetAsync(pstatus, 0, uint64_t(ntiles) * 8, st));
+      uint32_t* pcount = (uint32_t*)ar.alloc(16);  // [0] pieces
       {
         ProfScope ps("tiles", st);
-        k_piece_plan2<1024, TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat, pieces, pcount, pout, pstatus);
+        k_piece_dense<<<1, 1024, 0, st>>>(dTiles, ntiles, pcount);
+        check_launch("k_piece_dense");
+        k_piece_plan2<1024, TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat, pieces, pout);
         check_launch("k_piece_plan2");
       }
-      ar.release(pstatus);
       using XC = WsCfg<K, PAIRS, TC::S, TC::F>;
       auto f = k_transpose_ws<K, PAIRS, TC::S, TC::F>;
       const int grid = wave_grid(f, XC::NT, XC::SMEM);

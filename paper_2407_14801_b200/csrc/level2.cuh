@@ -42,7 +42,8 @@ struct TileInfo {
   uint32_t out;          // absolute output offset of the tile's region
   uint32_t size;         // keys in the tile
   uint32_t piece_base;   // first entry in the piece tables
-  uint32_t npieces;      // pieces written (set by the transpose)
+  uint32_t npieces;      // pieces written (set by the piece plan)
+  uint32_t dense;        // piece count, then (k_piece_dense) first position in the dense piece list
 };
 
 // Per-bucket record for the bucket phase.
@@ -362,25 +363,70 @@ __global__ void k_segmat(const LevelSeg* __restrict__ segs, const TaskDesc* __re
   }
 }
 
-// Keys per bucket tile (sum of the tile's run in every column).  CTA per tile.
-static __global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
+// Keys per bucket tile (sum of the tile's run in every column), and the tile's piece
+// count: the piece plan's windows (plan_fw columns each) cut into pieces of at most
+// S keys -- counted here so that k_piece_dense can give every tile its place in the
+// dense piece list before the plan runs.  CTA per tile.
+__host__ __device__ __forceinline__ uint32_t plan_fw(uint32_t size, uint32_t ncols, uint32_t S, uint32_t FWMAX);
+template <int S, int FW>
+__global__ void k_tile_sizes(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles,
                              const uint32_t* __restrict__ segmat) {
+  constexpr int PL = (FW + 31) / 32;
   TileInfo ti = tiles[blockIdx.x];
   const LevelSeg sg = segs[ti.seg];
+  const uint32_t* rows = segmat + sg.segmat_base + uint64_t(ti.bt) * sg.ncols;  // tile-major
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint32_t sum = 0;
-  for (uint32_t c = threadIdx.x; c < sg.ncols; c += blockDim.x) {
-    const uint32_t* row = segmat + sg.segmat_base + uint64_t(ti.bt) * sg.ncols + c;  // tile-major
-    sum += row[sg.ncols] - row[0];
-  }
+  for (uint32_t c = threadIdx.x; c < sg.ncols; c += blockDim.x) sum += rows[c + sg.ncols] - rows[c];
   __shared__ uint32_t red[32];
+  __shared__ uint32_t tsize;
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  if (lane == 0) red[w] = sum;
   __syncthreads();
   if (threadIdx.x < 32) {
-    sum = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+    sum = threadIdx.x < nw ? red[threadIdx.x] : 0;
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (threadIdx.x == 0) tiles[blockIdx.x].size = sum;
+    if (threadIdx.x == 0) tsize = sum;
   }
+  __syncthreads();
+  const uint32_t size = tsize;
+  const uint32_t fw = plan_fw(size, sg.ncols, S, FW), nwin = (sg.ncols + fw - 1) / fw;
+  uint32_t cnt = 0;
+  for (uint32_t win = w; win < nwin; win += nw) {  // warp per window, as in the plan
+    uint32_t ws = 0;
+#pragma unroll
+    for (int q = 0; q < PL; q++) {
+      const uint32_t j = lane * PL + q, c = win * fw + j;
+      if (j < fw && c < sg.ncols) ws += rows[c + sg.ncols] - rows[c];
+    }
+    for (int o = 16; o; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    cnt += (ws + S - 1) / S;
+  }
+  __syncthreads();
+  if (lane == 0) red[w] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t c = 0;
+    for (int q = 0; q < nw; q++) c += red[q];
+    tiles[blockIdx.x].size = size;
+    tiles[blockIdx.x].dense = c;
+  }
+}
+
+// Dense piece list: exclusive scan of the tiles' piece counts in tile order (one
+// CTA); the total is the transpose's piece count.
+static __global__ void k_piece_dense(TileInfo* __restrict__ tiles, uint32_t ntiles, uint32_t* __restrict__ pcount) {
+  __shared__ uint32_t misc[64];
+  uint32_t carry = 0;
+  for (uint32_t c0 = 0; c0 < ntiles; c0 += blockDim.x) {
+    const uint32_t i = c0 + threadIdx.x;
+    const uint32_t v = i < ntiles ? tiles[i].dense : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<32>(v, misc, &tot);
+    if (i < ntiles) tiles[i].dense = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) pcount[0] = carry;
 }
 
 // Per segment: tile output offsets (exclusive scan of sizes) and piece-table
@@ -514,30 +560,6 @@ struct __align__(16) PieceDesc {
 // consecutive columns; a window of T keys gives ceil(T / S) pieces (one for the
 // usual T <= S), cut at stream positions that are multiples of S.  CTA per tile;
 // warps work on windows independently (no serial chain over the tile).
-// Dense list position of a tile's pieces: decoupled look-back over the tiles in
-// ticket order (status[i] = flag << 62 | value; flag 1 = aggregate, 2 = inclusive
-// prefix).  Tickets are taken at CTA start, so every lower ticket belongs to a CTA
-// that is already running and never waits on a higher one.
-__device__ __forceinline__ uint32_t piece_lookback(unsigned long long* status, uint32_t idx, uint32_t agg) {
-  constexpr unsigned long long A = 1ull << 62, P = 2ull << 62, M = (1ull << 62) - 1;
-  if (idx == 0) {
-    atomicExch(&status[0], P | agg);
-    return 0;
-  }
-  atomicExch(&status[idx], A | agg);
-  unsigned long long sum = 0;
-  for (int j = int(idx) - 1;; j--) {
-    unsigned long long v;
-    do {
-      v = *reinterpret_cast<volatile unsigned long long*>(&status[j]);
-    } while (!(v >> 62));
-    sum += v & M;
-    if ((v >> 62) == 2) break;
-  }
-  atomicExch(&status[idx], P | (sum + agg));
-  return uint32_t(sum);
-}
-
 // The pieces are listed in tile order: the transpose takes list positions in
 // order, so the two pieces that share a column's boundary sectors (tiles bt and
 // bt+1 of one window) run close together in time and the shared sectors are read
@@ -545,19 +567,17 @@ __device__ __forceinline__ uint32_t piece_lookback(unsigned long long* status, u
 template <int NT, int S, int FW>
 __global__ void __launch_bounds__(NT)
 k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, const uint32_t* __restrict__ segmat,
-              PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pcount, uint32_t* __restrict__ pout,
-              unsigned long long* __restrict__ status) {
+              PieceDesc* __restrict__ pieces, uint32_t* __restrict__ pout) {
   constexpr int NW = NT / 32, PL = (FW + 31) / 32;  // columns per lane within a window
   constexpr uint32_t MAXW = 1024;                    // windows per chunk
   static_assert(FW <= 128, "window");
   __shared__ uint32_t wtot[MAXW], wpc[MAXW], woff[MAXW], wpb[MAXW];
   __shared__ uint32_t misc[64];
-  __shared__ uint32_t base, carry_o, carry_p, tix;
+  __shared__ uint32_t carry_o, carry_p;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t == 0) tix = atomicAdd(&pcount[1], 1u);
-  __syncthreads();
-  const uint32_t me = tix;
+  const uint32_t me = blockIdx.x;
   const TileInfo ti = tiles[me];
+  const uint32_t base = ti.dense;  // the tile's first position in the dense piece list
   const LevelSeg sg = segs[ti.seg];
   const uint32_t bt = ti.bt, rstride = sg.ncols;  // tile-major segmat: (bt+1, c) is ncols after (bt, c)
   const uint32_t* rows = segmat + sg.segmat_base + uint64_t(bt) * sg.ncols;
@@ -572,26 +592,7 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
     carry_o = 0;
     carry_p = 0;
   }
-  if (nwin > MAXW) {  // several chunks: the tile's piece count first
-    uint32_t cnt = 0;
-    for (uint32_t win = w; win < nwin; win += NW) {
-      uint32_t sum = 0;
-#pragma unroll
-      for (int q = 0; q < PL; q++) {
-        const uint32_t j = lane * PL + q;
-        if (j < fw) sum += run_len(win * fw + j);
-      }
-      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      cnt += (sum + S - 1) / S;
-    }
-    uint32_t tot;
-    block_excl_sum<NW>(lane == 0 ? cnt : 0u, misc, &tot);
-    if (t == 0) {
-      base = piece_lookback(status, me, tot);
-      atomicAdd(pcount, tot);
-    }
-    __syncthreads();
-  }
+  __syncthreads();
   for (uint32_t w0 = 0; w0 < nwin; w0 += MAXW) {
     const uint32_t nw = min(MAXW, nwin - w0);
     for (uint32_t wi = w; wi < nw; wi += NW) {  // window totals
@@ -626,10 +627,6 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
       }
       __syncthreads();
       if (t == 0) {
-        if (nwin <= MAXW) {  // one chunk: cp is the tile's piece count
-          base = piece_lookback(status, me, cp);
-          atomicAdd(pcount, cp);
-        }
         carry_o = co;
         carry_p = cp;
       }
@@ -684,6 +681,7 @@ k_piece_plan2(const LevelSeg* __restrict__ segs, TileInfo* __restrict__ tiles, c
     }
     __syncthreads();
   }
+  SQ_CHECK(t != 0 || me + 1 >= gridDim.x || carry_p == tiles[me + 1].dense - base);
   if (t == 0) tiles[me].npieces = carry_p;
 }
 
