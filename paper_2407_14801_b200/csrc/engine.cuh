@@ -1445,9 +1445,19 @@ struct GraphCache {
   static void capture(Entry* e, K* keys, uint32_t* vals, size_t n, uint64_t seed) {
     SQ_CUDA(cudaMalloc((void**)&e->dmem, e->dev_need));
     SQ_CUDA(cudaMallocHost((void**)&e->hmem, e->pin_need));
-    // captured on a library stream of its own (the caller's may be the legacy stream)
-    static thread_local std::map<int, cudaStream_t> cap_stream;
-    cudaStream_t& cs = cap_stream[e->dev];
+    // captured on a library stream of its own (the caller's may be the legacy stream),
+    // one per host thread and device, destroyed when the thread exits
+    struct CapStreams {
+      std::map<int, cudaStream_t> s;
+      ~CapStreams() {
+        for (auto& kv : s) {
+          cudaSetDevice(kv.first);
+          cudaStreamDestroy(kv.second);
+        }
+      }
+    };
+    static thread_local CapStreams cap_stream;
+    cudaStream_t& cs = cap_stream.s[e->dev];
     if (!cs) SQ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     SQ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     typename E::LevelTail lt;
