@@ -542,6 +542,10 @@ template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16,
 // (measured: 16K units 4.41 ms vs 32K 4.47 ms at cfg5 -- the 16K class runs two CTAs per SM)
 inline uint32_t g_unit_max = getenv("SQ_UNIT_MAX") ? (uint32_t)atoi(getenv("SQ_UNIT_MAX")) : 16384u;
 inline uint32_t g_one_cap = getenv("SQ_ONE_CAP") ? (uint32_t)atoi(getenv("SQ_ONE_CAP")) : 32768u;
+// a bucket-sort class to leave out (its buckets go to the next larger class): the 24K
+// class runs 24 warps per SM (80 registers), the 32K class 32 -- measured 4.392 vs
+// 4.413-4.424 ms at cfg5 without it (SQ_SKIP_TILE=0 restores it)
+inline uint32_t g_skip_tile = getenv("SQ_SKIP_TILE") ? (uint32_t)atoi(getenv("SQ_SKIP_TILE")) : 24576u;
 template <typename SK> uint32_t single_cap() {
   return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : (sizeof(SK) == 8 ? 8192u : 4096u);
 }
@@ -1079,7 +1083,8 @@ struct Engine {
       // skipped), instead of a latency-bound launch per tiny class
       const uint32_t lower = std::min<uint32_t>(1024u, one);
       for (uint32_t t : kTiles)
-        if (t >= lower && t <= one && t <= key_max_tile<SK>()) po.cls_tile[po.ncls++] = t;
+        if (t >= lower && t <= one && t <= key_max_tile<SK>() && !(g_skip_tile && t == g_skip_tile))
+          po.cls_tile[po.ncls++] = t;
       po.max_tile = one;
       if (bincl)  // beyond one CTA: clusters of 2, 4, 8 counting-sort tiles (binclust.cuh)
         for (int cl : {2, 4, 8}) {
