@@ -542,12 +542,16 @@ template <> struct ClusterBig<uint64_t> { static constexpr int NT = 512, V = 16,
 // (measured: 16K units 4.41 ms vs 32K 4.47 ms at cfg5 -- the 16K class runs two CTAs per SM)
 inline uint32_t g_unit_max = getenv("SQ_UNIT_MAX") ? (uint32_t)atoi(getenv("SQ_UNIT_MAX")) : 16384u;
 inline uint32_t g_one_cap = getenv("SQ_ONE_CAP") ? (uint32_t)atoi(getenv("SQ_ONE_CAP")) : 32768u;
+// largest bucket one CTA sorts for 64-bit sort keys (u64 keys, u32-key pairs): the 12K
+// counting-sort tile (cfg5p 7.27 -> 6.47 ms against 8K; a 16K pair tile does not fit
+// the counting sort and runs the merge sort: 7.81 ms)
+inline uint32_t g_one_cap8 = getenv("SQ_ONE_CAP8") ? (uint32_t)atoi(getenv("SQ_ONE_CAP8")) : 12288u;
 // a bucket-sort class to leave out (its buckets go to the next larger class): the 24K
 // class runs 24 warps per SM (80 registers), the 32K class 32 -- measured 4.392 vs
 // 4.413-4.424 ms at cfg5 without it (SQ_SKIP_TILE=0 restores it)
 inline uint32_t g_skip_tile = getenv("SQ_SKIP_TILE") ? (uint32_t)atoi(getenv("SQ_SKIP_TILE")) : 24576u;
 template <typename SK> uint32_t single_cap() {
-  return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : (sizeof(SK) == 8 ? 8192u : 4096u);
+  return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : (sizeof(SK) == 8 ? g_one_cap8 : 4096u);
 }
 
 // merge passes: threads x outputs per thread (tile = NT * VM keys)
