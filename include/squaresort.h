@@ -240,7 +240,11 @@ int sq_set_max_tile(uint32_t max_tile);
  * memory; 3: for 32-bit keys with the counting-sort base case, thread-block
  * clusters of 2/4/8 counting-sort tiles that split the bucket into value ranges
  * through distributed shared memory (buckets up to 8 x 16128 keys; other key
- * types run mode 1).  Process-wide; SQ_ERR_INVALID_ARGUMENT for other values. */
+ * types run mode 1); 4: keys-only sorts split an inner bucket b (keys in
+ * [P[b-1], P[b]), readings L2/L4) into up to 16 value ranges, each sorted on chip
+ * by one CTA that reads the whole bucket and keeps its range (no merge passes;
+ * pairs and the outer buckets run mode 1).  Process-wide;
+ * SQ_ERR_INVALID_ARGUMENT for other values. */
 int sq_set_big_bucket_mode(int mode);
 
 /* Tuning/test knob: the on-chip base case of keys-only 32-bit sorts (the GPU's

@@ -333,7 +333,7 @@ def set_max_tile(t: int):
     _check(lib().sq_set_max_tile(t))
 
 
-BIG_LEVEL, BIG_MERGE, BIG_CLUSTER, BIG_BINCLUSTER = 0, 1, 2, 3
+BIG_LEVEL, BIG_MERGE, BIG_CLUSTER, BIG_BINCLUSTER, BIG_SPLIT = 0, 1, 2, 3, 4
 
 
 def set_big_bucket_mode(mode: int):

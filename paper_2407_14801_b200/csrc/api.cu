@@ -233,7 +233,7 @@ int sq_profile_read(char* buf, size_t cap) {
 }
 
 int sq_set_big_bucket_mode(int mode) {
-  if (mode < 0 || mode > 3) return SQ_ERR_INVALID_ARGUMENT;
+  if (mode < 0 || mode > 4) return SQ_ERR_INVALID_ARGUMENT;
   g_big_mode = mode;
   return SQ_OK;
 }

@@ -550,6 +550,36 @@ inline uint32_t g_one_cap8 = getenv("SQ_ONE_CAP8") ? (uint32_t)atoi(getenv("SQ_O
 // class runs 24 warps per SM (80 registers), the 32K class 32 -- measured 4.392 vs
 // 4.413-4.424 ms at cfg5 without it (SQ_SKIP_TILE=0 restores it)
 inline uint32_t g_skip_tile = getenv("SQ_SKIP_TILE") ? (uint32_t)atoi(getenv("SQ_SKIP_TILE")) : 24576u;
+// value-split sorts of big buckets (mode 4): the CTA tile and how full its ranges
+// are planned (SQ_SPLIT_TILE: 0 = per key type default; SQ_SPLIT_FILL percent;
+// SQ_SPLIT_QMAX: most ranges per bucket, larger buckets take the merge path)
+inline uint32_t g_split_tile = getenv("SQ_SPLIT_TILE") ? (uint32_t)atoi(getenv("SQ_SPLIT_TILE")) : 0u;
+inline uint32_t g_split_fill = getenv("SQ_SPLIT_FILL") ? (uint32_t)atoi(getenv("SQ_SPLIT_FILL")) : 85u;
+inline uint32_t g_split_qmax = getenv("SQ_SPLIT_QMAX") ? (uint32_t)atoi(getenv("SQ_SPLIT_QMAX")) : 16u;
+// the split kernel's tiles (a few shapes, to bound the instantiations)
+inline constexpr uint32_t kSplitTiles[] = {256, 1024, 4096, 8192, 12288, 16384, 32768};
+template <typename SK> uint32_t split_tile(uint32_t one) {
+  uint32_t want = g_split_tile ? g_split_tile : (sizeof(SK) == 4 ? 16384u : 8192u);
+  want = std::min(want, std::max(256u, one));
+  uint32_t t = 256;
+  for (uint32_t c : kSplitTiles)
+    if (c <= want && c <= key_max_tile<SK>()) t = c;
+  return t;
+}
+template <typename SK, typename F>
+void with_split_tile(uint32_t tile, F&& f) {
+  switch (tile) {
+    case 256: return with_tile<SK>(256, f);
+    case 1024: return with_tile<SK>(1024, f);
+    case 4096: return with_tile<SK>(4096, f);
+    case 8192: return with_tile<SK>(8192, f);
+    case 12288: return with_tile<SK>(12288, f);
+    case 16384: if constexpr (sizeof(SK) <= 8) return with_tile<SK>(16384, f); break;
+    case 32768: if constexpr (sizeof(SK) == 4) return with_tile<SK>(32768, f); break;
+  }
+  throw Error(SQ_ERR_CUDA, "no split tile " + std::to_string(tile));
+}
+
 template <typename SK> uint32_t single_cap() {
   return sizeof(SK) == 4 ? (g_base_case ? g_one_cap : 16384u) : (sizeof(SK) == 8 ? g_one_cap8 : 4096u);
 }
@@ -1132,7 +1162,7 @@ struct Engine {
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     // (u64 pairs have no cluster kernel: mode 2 runs the merge base case for them)
-    const bool merge = mode == 1 || (mode == 2 && sizeof(SK) == 16);
+    const bool merge = mode == 1 || mode == 4 || (mode == 2 && sizeof(SK) == 16);
     if (merge) {  // multi-CTA merge sort for buckets of up to 16 chunks
       po.msort_max = 16u * po.max_tile;
       po.mcap = (uint32_t)(level_keys / po.mtile + 9 * buck_tot + 16);
@@ -1141,11 +1171,19 @@ struct Engine {
     po.mlist = (MTile*)ar.alloc(uint64_t(kMaxPasses) * po.mcap * sizeof(MTile));
     po.mcount = (uint32_t*)ar.alloc(kMaxPasses * 4);
     SQ_CUDA(cudaMemsetAsync(po.mcount, 0, kMaxPasses * 4, st));
-    po.cap_per_list = (uint32_t)(buck_tot + level_keys / std::max<uint32_t>(po.max_tile, 1) + 16);
+    // value split (mode 4, keys only): inner buckets of up to split_qmax ranges
+    const uint32_t stile = split_tile<SK>(po.max_tile);
+    if (mode == 4 && !PAIRS) {
+      po.split_part = std::max<uint32_t>(1, uint32_t(uint64_t(stile) * std::min<uint32_t>(g_split_fill, 100) / 100));
+      po.split_max = std::min<uint32_t>(std::max<uint32_t>(1, std::min<uint32_t>(g_split_qmax, 16)) * po.split_part,
+                                        po.msort_max);
+    }
+    po.cap_per_list = (uint32_t)(buck_tot + level_keys / std::max<uint32_t>(std::min(po.max_tile, po.split_max ? po.split_part : ~0u), 1) + 16);
     // lists: [0, ncls) classes, ncls copy, ncls+1 oversize, ncls+2 pair, then the
     // chunks of merge-sorted buckets per class at ncls+3+c (sorted first, so that
-    // the merge passes can overlap the other classes)
-    const uint32_t nlists = 2 * po.ncls + 3;
+    // the merge passes can overlap the other classes), then the value-split items
+    const uint32_t nlists = 2 * po.ncls + 4;
+    po.split_list = 2 * po.ncls + 3;
     po.list = (uint32_t*)ar.alloc(uint64_t(nlists) * po.cap_per_list * 4);
     po.count = (uint32_t*)ar.alloc(nlists * 4);
     SQ_CUDA(cudaMemsetAsync(po.count, 0, nlists * 4, st));
@@ -1212,6 +1250,28 @@ struct Engine {
         });
       });
     };
+    auto launch_split = [&](cudaStream_t cs) {  // value-split items (k_bucketsplit)
+      if constexpr (!PAIRS) {
+        if (!po.split_max) return;
+        with_split_tile<SK>(stile, [&](auto nt, auto v) {
+          constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
+          using BS = BlockSort<SK, NT, V>;
+          constexpr size_t base = BS::SMEM_BYTES + (3 * NT + 64) * 4;
+          with_bin<BIN && base + bin_smem<K, NT, V, false, BIN>() <= kMaxSmem>([&](auto bin) {
+            constexpr bool UB = decltype(bin)::value;
+            const size_t smem = base + bin_smem<K, NT, V, false, UB>();
+            auto f = k_bucketsplit<K, NT, V, UB>;
+            const int grid = wave_grid(f, NT, smem);
+            std::optional<ProfScope> ps;
+            if (!g_concurrent_classes) ps.emplace("bucketsort", cs);
+            f<<<(uint32_t)std::min<uint64_t>(grid, po.cap_per_list), NT, smem, cs>>>(
+                dL, piv, recs, dTiles, po.list + uint64_t(po.split_list) * po.cap_per_list, po.count + po.split_list,
+                kb[T], kb[X], pout, ppre);
+            check_launch("k_bucketsplit");
+          });
+        });
+      }
+    };
     auto launch_merges = [&](cudaStream_t ms) {  // merge passes of the multi-CTA base case (X <-> U)
       using MC = MergeCfg<K, PAIRS>;
       using BS = BlockSort<K, MC::NT, MC::VM>;
@@ -1233,12 +1293,14 @@ struct Engine {
     if (!g_concurrent_classes) {
       if (merge)
         for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, st);
+      launch_split(st);
       for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, st);
       if (merge) launch_merges(st);
     } else {
       // streams 0-1: the chunks of merge-sorted buckets, then (stream 0) the merge
       // passes; streams 2-3: whole buckets and units, which the merges overlap
       int rc = 0, rw = 0;
+      launch_split(ss.s[1]);
       if (merge)
         for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, ss.s[rc++ % 2]);
       for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, ss.s[2 + rw++ % 2]);

@@ -714,6 +714,11 @@ struct PlanOut {
   Unit* units;
   uint32_t* nunits;
   uint32_t unit_max;  // largest unit (and bucket packed into units): the biggest one-CTA class
+  // value split (mode 4): inner buckets of max_tile < size <= split_max keys go to
+  // list split_list as ceil(size / split_part) value-range items (k_bucketsplit)
+  uint32_t split_max;
+  uint32_t split_part;
+  uint32_t split_list;
 };
 
 // Bucket plan, one warp per bucket tile: lane j takes bucket j of the tile; its final offset is the tile's
@@ -749,9 +754,14 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
     rc.chunk = size;
     rc.passes = 0;
     const bool single = b >= 1 && b + 1 < sg.k && P[b - 1] == P[b];
+    const bool vsplit = !single && b >= 1 && b + 1 < sg.k && size > po.max_tile && size <= po.split_max;
     uint32_t q = 1;  // chunks
     const uint32_t chunk_len = po.max_tile;
-    if (size && !single && size > po.max_tile && size <= po.msort_max) {
+    if (vsplit) {
+      rc.chunk = (size + po.split_part - 1) / po.split_part;  // value ranges
+      const uint32_t slot = atomicAdd(&po.count[po.split_list], rc.chunk);
+      for (uint32_t k = 0; k < rc.chunk; k++) po.list[uint64_t(po.split_list) * po.cap_per_list + slot + k] = gi * 16 + k;
+    } else if (size && !single && size > po.max_tile && size <= po.msort_max) {
       q = (size + chunk_len - 1) / chunk_len;
       rc.chunk = chunk_len;  // full chunks; the last one takes the remainder
       uint32_t np = 0;
@@ -771,7 +781,7 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
       }
     }
     recs[gi] = rc;
-    if (size && !(po.units && size <= po.unit_max)) {  // else packed into a unit below
+    if (size && !vsplit && !(po.units && size <= po.unit_max)) {  // else packed into a unit below
       if (single || size > po.msort_max) {
         const int cls = single ? po.ncls : po.ncls + 1;
         const uint32_t slot = atomicAdd(&po.count[cls], 1u);
@@ -944,6 +954,112 @@ k_bucketsort(const BucketRec* __restrict__ recs, const TileInfo* __restrict__ ti
       }
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Value-split sort of a bucket beyond one CTA (big-bucket mode 4, keys only).  An
+// inner bucket b holds keys in [P[b-1], P[b]) (L2, L4: a single-value bucket b-1
+// has taken x = P[b-1]), so the bucket is sorted by sorting q value ranges
+// separately (P:291-293 applied to a split of the bucket's range instead of a
+// second sample).  Item (bucket, j) owns [s_j, s_{j+1}), s_j = P[b-1] +
+// floor(j (P[b] - P[b-1]) / q): its CTA reads the whole bucket (the q readers of a
+// bucket run together, so the re-reads are L2 hits), keeps the keys of its range
+// and counts the smaller ones (its output offset), sorts its keys on chip and
+// writes them to their final place: every key crosses HBM twice and no merge pass
+// runs.  A range with more keys than the tile is halved and re-read until it
+// fits; a range of one value is written as copies of that value.
+template <typename K>
+__device__ __forceinline__ K split_point(K lo, K hi, uint32_t j, uint32_t q) {
+  const K d = hi - lo;  // floor(j d / q) without overflow (j <= q <= 16)
+  return lo + (d / q) * j + ((d % q) * j) / q;
+}
+
+template <typename K, int NT, int V, bool BIN>
+__global__ void __launch_bounds__(NT, (bin_min_blocks<K, NT, V, false, BIN>()))
+k_bucketsplit(const LevelSeg* __restrict__ segs, const K* __restrict__ piv, const BucketRec* __restrict__ recs,
+              const TileInfo* __restrict__ tiles, const uint32_t* __restrict__ list,
+              const uint32_t* __restrict__ count, const K* __restrict__ src, K* __restrict__ dst,
+              const uint32_t* __restrict__ pout, const uint16_t* __restrict__ ppre) {
+  using BS = BlockSort<K, NT, V>;
+  constexpr int NW = NT / 32;
+  constexpr uint32_t TILE = BS::TILE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  K* s = reinterpret_cast<K*>(smem_raw);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + BS::SMEM_BYTES);
+  uint32_t* s_len = s_off + NT;
+  uint32_t* s_dst = s_len + NT;
+  uint32_t* misc = s_dst + NT;
+  uint32_t* cnt = misc + 64;  // counting-sort counters (BIN)
+  __shared__ uint32_t s_fill;
+  auto TP = [](uint32_t i) { return tpos<K, NT, V, false, BIN>(i); };
+  const uint32_t total = *count;
+  for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const uint32_t e = list[it];
+    const BucketRec rc = recs[item_bucket(e)];
+    const TileInfo ti = tiles[rc.tile];
+    const LevelSeg sg = segs[ti.seg];
+    const K* P = piv + sg.piv_base;
+    const uint32_t b = ti.bt * kTB + rc.lane, q = rc.chunk, j = item_chunk(e);
+    const K plo = P[b - 1], phi = P[b];
+    K a = split_point(plo, phi, j, q), c = split_point(plo, phi, j + 1, q);
+    K stk_a[8 * sizeof(K)], stk_c[8 * sizeof(K)];  // halves still to do (thread-uniform)
+    int sp = 0;
+    while (true) {
+      if (a < c) {
+        if (threadIdx.x == 0) s_fill = 0;
+        __syncthreads();
+        uint32_t below = 0;
+        gather_bucket<NT>(ti, rc.lane, pout, ppre, s_off, s_len, s_dst, misc, 0u, rc.size,
+                          [&](uint32_t o, uint32_t l, uint32_t, int ln) {
+                            for (uint32_t q0 = 0; q0 < l; q0 += 128) {  // 4 loads in flight per lane
+                              K x[4];
+#pragma unroll
+                              for (int u = 0; u < 4; u++) {
+                                const uint32_t qq = q0 + u * 32 + ln;
+                                x[u] = qq < l ? src[o + qq] : c;
+                              }
+#pragma unroll
+                              for (int u = 0; u < 4; u++) {
+                                below += x[u] < a;
+                                const bool in = x[u] >= a && x[u] < c;
+                                const uint32_t m = __ballot_sync(0xffffffffu, in);
+                                if (!m) continue;
+                                uint32_t base = 0;
+                                if (ln == 0) base = atomicAdd(&s_fill, __popc(m));
+                                base = __shfl_sync(0xffffffffu, base, 0);
+                                const uint32_t pos = base + __popc(m & ((1u << ln) - 1u));
+                                if (in && pos < TILE) s[TP(pos)] = x[u];
+                              }
+                            }
+                          });
+        uint32_t off;
+        block_excl_sum<NW>(below, misc, &off);  // (its barriers also publish s_fill and the tile)
+        const uint32_t len = s_fill;
+        K* out = dst + rc.out + off;
+        if (len <= TILE) {
+          for (uint32_t i = threadIdx.x + len; i < TILE; i += NT) s[TP(i)] = KeyTraits<K>::kMax;
+          __syncthreads();
+          tile_sort<K, NT, V, false, BIN>(s, cnt, len);
+          for (uint32_t i = threadIdx.x; i < len; i += NT) out[i] = s[TP(i)];
+        } else if (c - a == 1) {
+          for (uint32_t i = threadIdx.x; i < len; i += NT) out[i] = a;
+        } else {  // too many keys: the lower half now, the upper half later
+          const K mid = a + (c - a) / 2;
+          stk_a[sp] = mid;
+          stk_c[sp] = c;
+          sp++;
+          c = mid;
+          __syncthreads();
+          continue;
+        }
+        __syncthreads();
+      }
+      if (!sp) break;
+      sp--;
+      a = stk_a[sp];
+      c = stk_c[sp];
+    }
   }
 }
 

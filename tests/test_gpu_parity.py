@@ -207,7 +207,7 @@ def test_sizes_u64(n):
     assert np.array_equal(gpu_sort(keys, 7), np.sort(keys))
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 4])
 @pytest.mark.parametrize("tile", [64, 256, 1024])
 @pytest.mark.parametrize("n", [5000, 70001, 300000])
 def test_forced_multilevel_vs_oracle(tile, n, mode):
@@ -225,7 +225,7 @@ def test_forced_multilevel_vs_oracle(tile, n, mode):
             assert sq.get_stats()["levels"] >= 2
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 4])
 @pytest.mark.parametrize("tile", [64, 512])
 def test_forced_multilevel_pairs_and_u64(tile, mode):
     sq.set_max_tile(tile)
@@ -263,7 +263,7 @@ def test_pairs_stability_with_duplicates():
         assert np.array_equal(gk, ek) and np.array_equal(gv, ev)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 4])
 def test_big_bucket_modes_full_tile(mode):
     # default tiles, 2^24 keys: buckets of ~4K with a tail beyond 16K exercise each mode
     sq.set_big_bucket_mode(mode)
@@ -565,3 +565,42 @@ def test_bincluster_mode_level_state_vs_oracle():
     keys = S.uniform_u32(1 << 22, 12)
     want, _ = oracle_sort(keys, 12)
     assert np.array_equal(gpu_sort(keys, 12), want)
+
+
+# ---------------------------------------------------------------- value-split big buckets (mode 4)
+@pytest.mark.parametrize("lg", [24, 26])
+def test_split_mode_uniform(lg):
+    # m = 4096 / 8192: inner buckets beyond one CTA are sorted as value ranges
+    sq.set_big_bucket_mode(sq.BIG_SPLIT)
+    keys = S.uniform_u32(1 << lg, 50 + lg)
+    assert np.array_equal(gpu_sort(keys, 3), np.sort(keys))
+    k64 = S.stream(60 + lg, 1 << (lg - 2))
+    assert np.array_equal(gpu_sort(k64, 3), np.sort(k64))
+
+
+def test_split_mode_heavy_values_halve_ranges():
+    # heavy values inside buckets overflow a value range: the range is halved (and
+    # re-read) down to one-value ranges written as copies; the sort stays exact
+    sq.set_big_bucket_mode(sq.BIG_SPLIT)
+    n = 1 << 26
+    rng = np.random.default_rng(78)
+    keys = S.uniform_u32(n, 78)
+    heavy = rng.integers(0, 2**32, 100, dtype=np.uint64).astype(np.uint32)
+    pos = rng.choice(n, 100 * 30000, replace=False)
+    keys[pos] = np.repeat(heavy, 30000)
+    assert np.array_equal(gpu_sort(keys, 9), np.sort(keys))
+    # narrow ranges: values clustered near a few points inside wide buckets
+    keys = S.uniform_u32(n, 79)
+    keys[: n // 4] = (keys[: n // 4] % 64) + np.uint32(123456789)
+    assert np.array_equal(gpu_sort(keys, 9), np.sort(keys))
+
+
+def test_split_mode_vs_oracle():
+    sq.set_big_bucket_mode(sq.BIG_SPLIT)
+    keys = S.uniform_u32(1 << 22, 13)
+    want, _ = oracle_sort(keys, 13)
+    assert np.array_equal(gpu_sort(keys, 13), want)
+    sq.set_max_tile(256)
+    keys = S.uniform_u32(300001, 14)
+    want, _ = oracle_sort(keys, 14)
+    assert np.array_equal(gpu_sort(keys, 14), want)
