@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsquaresort.so")
+# (SQ_LIB_PATH: an experiment build of the same library, for A/B runs)
+LIB_PATH = os.environ.get("SQ_LIB_PATH") or os.path.join(_HERE, "libsquaresort.so")
 _lib = None
 
 SQ_OK = 0
