@@ -184,6 +184,9 @@ inline int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv(
 // on-chip base case for 32- and 64-bit sort keys (keys, u32-key pairs): 1 = counting
 // sort + network fix-up (binsort.cuh, default, where its shared memory fits),
 // 0 = merge sort (blocksort.cuh)
+// small levels (graph replay, two bucket-sort classes): n at most this; see GraphCache below
+inline size_t g_graph_max_n = getenv("SQ_GRAPH_MAX_N") ? (size_t)atoll(getenv("SQ_GRAPH_MAX_N")) : (size_t(1) << 22);
+inline int g_small_classes = getenv("SQ_SMALL_CLASSES") ? atoi(getenv("SQ_SMALL_CLASSES")) : 1;
 inline int g_base_case = getenv("SQ_BASE_CASE") ? atoi(getenv("SQ_BASE_CASE")) : 1;
 constexpr size_t kMaxSmem = 232448;  // dynamic shared memory per CTA on sm_100 (227 KB)
 template <bool B, typename F>
@@ -478,6 +481,21 @@ void with_tile(uint32_t tile, F&& f) {
     }
   }
   throw Error(SQ_ERR_CUDA, "no block shape for tile " + std::to_string(tile));
+}
+
+// Latency shapes for the tiles of small levels (32-bit sort keys): a 512-2048 key
+// tile sorted by 2-8 warps of 8 keys per thread (merge sort) instead of one or two
+// warps of 32 -- a small level runs few CTAs, so a CTA's own latency is the level's.
+template <typename SK, typename F>
+void with_tile_lat(bool lat, uint32_t tile, F&& f) {
+  if constexpr (sizeof(SK) == 4) {
+    if (lat) switch (tile) {
+      case 512: return f(IC<64>{}, IC<8>{});
+      case 1024: return f(IC<128>{}, IC<8>{});
+      case 2048: return f(IC<256>{}, IC<8>{});
+    }
+  }
+  return with_tile<SK>(tile, std::forward<F>(f));
 }
 
 inline int num_sms() {
@@ -999,7 +1017,10 @@ struct Engine {
       for (auto& kv : colcls) coldesc.push_back({kv.first, (const ColDesc*)up[q++]});
     }
     // 1. pivots: all rounds in parallel from the level input (L9)
-    with_tile<K>(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
+    uint64_t level_total = 0;
+    for (const Seg& g : segs) level_total += g.len;
+    const bool lat = level_total <= g_graph_max_n && g_small_classes;  // small level: latency shapes
+    with_tile_lat<K>(lat, std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
       constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
       using BS = BlockSort<K, NT, V>;
       constexpr bool SB = BIN && BS::SMEM_BYTES + bin_smem<K, NT, V, false, BIN>() <= kMaxSmem;
@@ -1011,7 +1032,7 @@ struct Engine {
     });
     {
       ProfScope ps("select", st);
-      launch_pdl(k_select_round<K>, ns, 256, 0, st, dL, ns, (const K*)cand, (const uint8_t*)flags, (const K*)p0s,
+      launch_pdl(k_select_round<K>, ns, 1024, 0, st, dL, ns, (const K*)cand, (const uint8_t*)flags, (const K*)p0s,
                  (const K*)segmin, piv, info, fix, 0);
     }
     htrace("level: sampler launched");
@@ -1024,7 +1045,7 @@ struct Engine {
       bool first = true;
       for (auto& cd : coldesc) {
         const uint32_t ncol = (uint32_t)colcls[cd.first].size();
-        with_tile<SK>(cd.first, [&](auto nt, auto v) {
+        with_tile_lat<SK>(lat, cd.first, [&](auto nt, auto v) {
           constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
           using BS = BlockSort<SK, NT, V>;
           constexpr size_t base = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
@@ -1061,7 +1082,7 @@ struct Engine {
     // 3. min-exclusion: final round; repair the boundaries if it changed
     {
       ProfScope ps("select", st);
-      k_select_round<K><<<ns, 256, 0, st>>>(dL, ns, cand, flags, p0s, segmin, piv, info, fix, 1);
+      k_select_round<K><<<ns, 1024, 0, st>>>(dL, ns, cand, flags, p0s, segmin, piv, info, fix, 1);
       check_launch("k_select_round");
     }
     {
@@ -1110,6 +1131,16 @@ struct Engine {
     PlanOut po{};
     po.ncls = 0;
     int cls_cl[20] = {0};  // 0 = one CTA; > 0 clusters of small tiles; < 0 clusters of big tiles
+    uint64_t level_keys = 0, longest_seg = 0;
+    for (const Seg& g : segs) {
+      level_keys += g.len;
+      longest_seg = std::max<uint64_t>(longest_seg, g.len);
+    }
+    const bool small_level = level_keys <= g_graph_max_n && (mode == 0 || mode == 1) && !g_max_tile;
+    // small levels: units small enough that most SMs get one (but CTAs of >= 128
+    // threads: 4K keys, or 1K keys in the latency shape of with_tile_lat)
+    uint32_t small_unit = small_level && g_small_classes ? 1024 : 4096;
+    while (small_unit < (1u << 15) && uint64_t(small_unit) * 2 * num_sms() < level_keys) small_unit *= 2;
     {
       const uint32_t one = bincl ? std::min<uint32_t>(cap, BinClusterCfg::TILE)
                            : (mode != 0 && !g_max_tile ? std::min(cap, single_cap<SK>()) : cap);
@@ -1119,6 +1150,18 @@ struct Engine {
       for (uint32_t t : kTiles)
         if (t >= lower && t <= one && t <= key_max_tile<SK>() && !(g_skip_tile && t == g_skip_tile))
           po.cls_tile[po.ncls++] = t;
+      // small levels are bound by the number of dependent launches, not by the sorting:
+      // three classes only -- the units' tile, four times it (the tail of the bucket
+      // sizes, so that a bucket just above a unit is not sorted in a 32K tile) and
+      // the one-CTA cap
+      if (small_level && g_small_classes && po.ncls > 3) {
+        uint32_t ut = po.cls_tile[0];
+        for (uint32_t c = 0; c < po.ncls; c++)
+          if (po.cls_tile[c] <= small_unit) ut = po.cls_tile[c];
+        po.ncls = 0;
+        for (uint32_t t : {ut, 4 * ut, one})
+          if (t <= one && (!po.ncls || t > po.cls_tile[po.ncls - 1])) po.cls_tile[po.ncls++] = t;
+      }
       po.max_tile = one;
       if (bincl)  // beyond one CTA: clusters of 2, 4, 8 counting-sort tiles (binclust.cuh)
         for (int cl : {2, 4, 8}) {
@@ -1141,8 +1184,6 @@ struct Engine {
         }
       }
     }
-    uint64_t level_keys = 0;
-    for (const Seg& g : segs) level_keys += g.len;
     po.msort_max = po.max_tile;
     po.mtile = MergeCfg<K, PAIRS>::NT * MergeCfg<K, PAIRS>::VM;
     po.mcap = 1;
@@ -1151,14 +1192,7 @@ struct Engine {
     for (uint32_t c = 0; c < po.ncls; c++)
       if (!cls_cl[c]) po.unit_max = std::max(po.unit_max, po.cls_tile[c]);
     if (g_unit_max) po.unit_max = std::min(po.unit_max, g_unit_max);
-    {  // small levels: units small enough that most SMs get one (but >= 4K keys: a
-       // CTA of fewer than 128 threads sorts too slowly to be worth the spread)
-      uint64_t lvl = 0;
-      for (const Seg& g : segs) lvl += g.len;
-      uint32_t u = 4096;
-      while (u < po.unit_max && uint64_t(u) * 2 * num_sms() < lvl) u *= 2;
-      po.unit_max = std::min(po.unit_max, u);
-    }
+    po.unit_max = std::min(po.unit_max, small_unit);
     po.nunits = (uint32_t*)ar.alloc(16);
     SQ_CUDA(cudaMemsetAsync(po.nunits, 0, 4, st));
     // (u64 pairs have no cluster kernel: mode 2 runs the merge base case for them)
@@ -1232,7 +1266,7 @@ struct Engine {
         launch_cluster(cls_cl[c], cs, lst, po.count + li, recs, dTiles, T, X, pout, ppre, (uint32_t)buck_tot);
         return;
       }
-      with_tile<SK>(po.cls_tile[c], [&](auto nt, auto v) {
+      with_tile_lat<SK>(small_level && g_small_classes, po.cls_tile[c], [&](auto nt, auto v) {
         constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
         using BS = BlockSort<SK, NT, V>;
         constexpr size_t base = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0) + (3 * NT + 64) * 4;
@@ -1272,13 +1306,17 @@ struct Engine {
         });
       }
     };
+    // a bucket is no longer than its segment: passes that no bucket of this level can
+    // need are not launched (small levels: each launch is latency on the critical path)
+    uint32_t npasses = 0;
+    while (npasses < (uint32_t)kMaxPasses && (uint64_t(po.max_tile) << npasses) < longest_seg) npasses++;
     auto launch_merges = [&](cudaStream_t ms) {  // merge passes of the multi-CTA base case (X <-> U)
       using MC = MergeCfg<K, PAIRS>;
       using BS = BlockSort<K, MC::NT, MC::VM>;
       const size_t smem = BS::SMEM_BYTES + (PAIRS ? size_t(BS::TILE) * 4 : 0);
       auto f = k_merge_pass<K, PAIRS, MC::NT, MC::VM>;
       const int grid = wave_grid(f, MC::NT, smem);
-      for (uint32_t p = 0; p < (uint32_t)kMaxPasses; p++) {
+      for (uint32_t p = 0; p < npasses; p++) {
         ProfScope ps("merge", ms);
         const MTile* items = po.mlist + uint64_t(p) * po.mcap;
         k_merge_split<K><<<2 * num_sms(), 256, 0, ms>>>(recs, items, po.mcount + p, p, po.mtile, kb[X], kb[2], splits);
@@ -1392,7 +1430,7 @@ inline bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 // Captured levels put buckets beyond one CTA into the next level (mode 0; rare at
 // these sizes) instead of the merge passes.  SQ_GRAPH_MAX_N (default 2^22; 0 = off)
 // bounds n; at most kGraphEntries levels are cached per engine instantiation.
-inline size_t g_graph_max_n = getenv("SQ_GRAPH_MAX_N") ? (size_t)atoll(getenv("SQ_GRAPH_MAX_N")) : (size_t(1) << 22);
+// (g_graph_max_n is defined with the other knobs above)
 constexpr int kGraphEntries = 4;
 // every instantiation's clear(), for sq_trim_memory
 inline std::mutex g_graph_reg_mu;

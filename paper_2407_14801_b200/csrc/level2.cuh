@@ -163,26 +163,30 @@ __global__ void k_select_round(const LevelSeg* __restrict__ segs, uint32_t nseg,
   const uint32_t seg = blockIdx.x;
   const LevelSeg sg = segs[seg];
   __shared__ uint32_t sel, change;
-  if (threadIdx.x == 0) {
-    uint32_t r = kCap;
-    for (uint32_t q = 0; q < kCap; q++) {
-      const bool ok = flags[uint64_t(seg) * kCap + q] == 1 &&
-                      (mode == 0 || sg.k == 1 || p0s[uint64_t(seg) * kCap + q] > segmin[seg]);
-      if (ok) { r = q; break; }
+  static_assert(kCap <= 32, "one lane per round");
+  if (threadIdx.x < 32) {  // lane q tests round q; the first accepted round wins
+    const uint32_t q = threadIdx.x;
+    const bool ok = q < kCap && flags[uint64_t(seg) * kCap + q] == 1 &&
+                    (mode == 0 || sg.k == 1 || p0s[uint64_t(seg) * kCap + q] > segmin[seg]);
+    const uint32_t acc = __ballot_sync(0xffffffffu, ok);
+    const uint32_t r = acc ? uint32_t(__ffs(acc) - 1) : kCap;
+    if (q == 0) {
+      const uint32_t inf = r < kCap ? r : ((kCap - 1) | 0x80000000u);
+      change = mode == 0 || info[seg] != inf;
+      if (mode == 1 && change) {
+        fix[seg] = 1;
+        fix[nseg] = 1;
+      }
+      info[seg] = inf;
+      sel = r < kCap ? r : kCap - 1;
     }
-    const uint32_t inf = r < kCap ? r : ((kCap - 1) | 0x80000000u);
-    change = mode == 0 || info[seg] != inf;
-    if (mode == 1 && change) {
-      fix[seg] = 1;
-      fix[nseg] = 1;
-    }
-    info[seg] = inf;
-    sel = r < kCap ? r : kCap - 1;
   }
   __syncthreads();
   if (!change) return;
   const uint32_t np = sg.k - 1;
   const K* in = cand + sg.cand_base + uint64_t(sel) * np;
+  // (on the column sort's critical path: 1024 threads, several loads in flight each)
+#pragma unroll 8
   for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) piv[sg.piv_base + i] = in[i];
 }
 
