@@ -248,13 +248,6 @@ static __global__ void k_xfer(const uint8_t* __restrict__ src, uint8_t* __restri
   }
 }
 
-// a level's read-back: the class counts, then the round word, into pinned memory
-static __global__ void k_readback(const uint32_t* __restrict__ count, uint32_t nc, const uint32_t* __restrict__ info,
-                                  uint32_t* __restrict__ out) {
-  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) out[i] = count[i];
-  if (threadIdx.x == 0) out[nc] = info[0];
-}
-
 inline void xfer(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return;
   const uint32_t g = (uint32_t)std::min<size_t>((bytes + 4095) / 4096, 148);
@@ -1095,20 +1088,23 @@ struct Engine {
     // transpose also accumulates the bucket sizes
     uint32_t* bsize = (uint32_t*)ar.alloc(buck_tot * 4);
     SQ_CUDA(cudaMemsetAsync(bsize, 0, buck_tot * 4, st));
+    uint32_t* pcount = (uint32_t*)ar.alloc(16);  // [0] pieces
     {
       ProfScope ps("tiles", st);
       k_tile_sizes<TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat);
       check_launch("k_tile_sizes");
-      k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, kPlanFW, dPieceBase);
+      // (one segment: the scan also builds the dense piece list)
+      k_tile_scan<<<ns, 256, 0, st>>>(dL, dTileBase, dTiles, TC::S, kPlanFW, dPieceBase, ns == 1 ? pcount : nullptr);
       check_launch("k_tile_scan");
     }
     {
       PieceDesc* pieces = (PieceDesc*)ar.alloc(piece_tot * sizeof(PieceDesc));
-      uint32_t* pcount = (uint32_t*)ar.alloc(16);  // [0] pieces
       {
         ProfScope ps("tiles", st);
-        k_piece_dense<<<1, 1024, 0, st>>>(dTiles, ntiles, pcount);
-        check_launch("k_piece_dense");
+        if (ns != 1) {
+          k_piece_dense<<<1, 1024, 0, st>>>(dTiles, ntiles, pcount);
+          check_launch("k_piece_dense");
+        }
         k_piece_plan2<1024, TC::S, kPlanFW><<<ntiles, 1024, 0, st>>>(dL, dTiles, segmat, pieces, pout);
         check_launch("k_piece_plan2");
       }
@@ -1341,7 +1337,9 @@ struct Engine {
       launch_split(ss.s[1]);
       if (merge)
         for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, po.ncls + 3 + c, ss.s[rc++ % 2]);
-      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, ss.s[2 + rw++ % 2]);
+      // (without chunk lists -- recursion mode, the captured small levels -- the whole
+      // classes take all four streams)
+      for (int c = (int)po.ncls - 1; c >= 0; c--) launch_class(c, c, merge ? ss.s[2 + rw++ % 2] : ss.s[rw++ % 4]);
       if (merge) {
         stream_wait(ss.s[0], ss.s[1]);
         launch_merges(ss.s[0]);
@@ -1350,6 +1348,8 @@ struct Engine {
     fj.join();
     span.reset();
     if (splits) ar.release(splits);
+    lt.hcnt = (uint32_t*)ar.pinned((po.ncls + 3) * 4);
+    lt.hinfo = lt.hcnt + po.ncls + 2;
     {  // single-value buckets (copied) and oversize buckets (made contiguous),
        // in units of kGatherKeys keys so that huge buckets are copied by many CTAs
       ProfScope ps("gather", st);
@@ -1358,7 +1358,9 @@ struct Engine {
       uint32_t* nun = (uint32_t*)ar.alloc(16);
       // both lists (ncls: single-value, ncls + 1: oversize) in one pass
       const uint32_t* lst = po.list + uint64_t(po.ncls) * po.cap_per_list;
-      k_gather_units<<<1, 1024, 0, st>>>(recs, lst, po.count + po.ncls, 2, po.cap_per_list, units, nun);
+      // (with the level's read-back: class counts (the oversize list's length) and the round)
+      k_gather_units<<<1, 1024, 0, st>>>(recs, lst, po.count + po.ncls, 2, po.cap_per_list, units, nun, po.count,
+                                         po.ncls + 2, info, lt.hcnt);
       check_launch("k_gather_units");
       k_bucket_gather_units<K, 256><<<4 * num_sms(), 256, 0, st>>>(
           recs, dTiles, lst, po.cap_per_list, units, nun, kb[T], kb[X], PAIRS ? vb[T] : nullptr,
@@ -1368,11 +1370,7 @@ struct Engine {
       ar.release(units);
     }
     htrace("level: bucket sorts launched");
-    // 7. the read-back (finish_level): class counts (the oversize list's length) and the round
-    lt.hcnt = (uint32_t*)ar.pinned((po.ncls + 3) * 4);
-    lt.hinfo = lt.hcnt + po.ncls + 2;
-    k_readback<<<1, 64, 0, st>>>(po.count, po.ncls + 2, info, lt.hcnt);
-    check_launch("k_readback");
+    // 7. the read-back (finish_level) was written by k_gather_units
     lt.ncls = po.ncls;
     lt.cap_per_list = po.cap_per_list;
     lt.list = po.list;

@@ -448,7 +448,7 @@ __host__ __device__ __forceinline__ uint32_t plan_fw(uint32_t size, uint32_t nco
 
 static __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint32_t* __restrict__ tile_base,
                             TileInfo* __restrict__ tiles, uint32_t S, uint32_t G,
-                            const uint32_t* __restrict__ piece_seg_base) {
+                            const uint32_t* __restrict__ piece_seg_base, uint32_t* __restrict__ pcount) {
   const LevelSeg sg = segs[blockIdx.x];
   const uint32_t t0 = tile_base[blockIdx.x], nt = sg.nbt;
   __shared__ uint32_t carry_out, carry_piece;
@@ -497,6 +497,21 @@ static __global__ void k_tile_scan(const LevelSeg* __restrict__ segs, const uint
       carry_piece += ec + cp;
     }
     __syncthreads();
+  }
+  // one-segment levels (pcount given; 256 threads): the dense piece list too, so that
+  // k_piece_dense is not a launch of its own
+  if (pcount) {
+    __shared__ uint32_t misc[64];
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < nt; c0 += blockDim.x) {
+      const uint32_t i = c0 + threadIdx.x;
+      const uint32_t v = i < nt ? tiles[t0 + i].dense : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_sum<8>(v, misc, &tot);
+      if (i < nt) tiles[t0 + i].dense = carry + ex;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) pcount[0] = carry;
   }
 }
 
@@ -804,20 +819,22 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
     }
   }
   if (!po.units) return;
-  // units: greedy, in bucket order, at most unit_max keys each (lane 0, shuffles)
+  // units: greedy, in bucket order, at most unit_max keys each.  Every lane walks the
+  // same (warp-uniform) packing; the lane of a unit's first bucket keeps the unit, and
+  // the units are then published by their lanes in parallel (one atomic for the
+  // tile's unit count, one per unit for its class list) instead of serially by lane 0
+  // -- the plan is on the critical path of small levels.
   uint32_t j0 = 0, acc = 0, out0 = 0;
+  uint32_t my_j1 = 0, my_acc = 0, my_out = 0;  // the unit starting at this lane's bucket
   auto flush = [&](uint32_t j1) {  // buckets j0..j1-1
-    if (!acc) return;
-    const uint32_t u = atomicAdd(po.nunits, 1u);
-    po.units[u] = Unit{ti_idx, j0, j1 - 1, out0, acc};
-    int cls = 0;
-    while (po.cls_tile[cls] < acc) cls++;
-    const uint32_t slot = atomicAdd(&po.count[cls], 1u);
-    po.list[uint64_t(cls) * po.cap_per_list + slot] = kUnitFlag | u;
+    if (acc && lane == j0) {
+      my_j1 = j1 - 1;
+      my_acc = acc;
+      my_out = out0;
+    }
   };
   for (uint32_t j = 0; j < nb; j++) {
     const uint32_t sz = __shfl_sync(0xffffffffu, size, j), o = __shfl_sync(0xffffffffu, out, j);
-    if (lane != 0) continue;
     const bool small = sz <= po.unit_max;
     if (!small || acc + sz > po.unit_max) {
       flush(j);
@@ -831,7 +848,20 @@ __global__ void k_tile_bucket_plan(const LevelSeg* __restrict__ segs, const Tile
       acc += sz;
     }
   }
-  if (lane == 0) flush(nb);
+  flush(nb);
+  const uint32_t has = __ballot_sync(0xffffffffu, my_acc != 0);
+  if (!has) return;
+  uint32_t ubase = 0;
+  if (lane == 0) ubase = atomicAdd(po.nunits, (uint32_t)__popc(has));
+  ubase = __shfl_sync(0xffffffffu, ubase, 0);
+  if (my_acc) {
+    const uint32_t u = ubase + __popc(has & ((1u << lane) - 1));
+    po.units[u] = Unit{ti_idx, lane, my_j1, my_out, my_acc};
+    int cls = 0;
+    while (po.cls_tile[cls] < my_acc) cls++;
+    const uint32_t slot = atomicAdd(&po.count[cls], 1u);
+    po.list[uint64_t(cls) * po.cap_per_list + slot] = kUnitFlag | u;
+  }
 }
 
 // Gather the bucket positions [lo, hi) (piece order = the paper's order) of a
@@ -1292,7 +1322,12 @@ constexpr uint32_t kGatherKeys = 65536;
 static __global__ void __launch_bounds__(1024)
 k_gather_units(const BucketRec* __restrict__ recs, const uint32_t* __restrict__ list,
                const uint32_t* __restrict__ count, uint32_t nlists, uint32_t list_stride, uint2* __restrict__ units,
-               uint32_t* __restrict__ nunits) {
+               uint32_t* __restrict__ nunits, const uint32_t* __restrict__ rb_count, uint32_t rb_n,
+               const uint32_t* __restrict__ rb_info, uint32_t* __restrict__ rb_out) {
+  // the level's read-back (one launch fewer on a small level's critical path): the
+  // class counts, then the round word, into pinned memory
+  for (uint32_t i = threadIdx.x; i < rb_n; i += blockDim.x) rb_out[i] = rb_count[i];
+  if (threadIdx.x == 0) rb_out[rb_n] = rb_info[0];
   // units of the lists [0, nlists) (list l at list + l * list_stride, count[l] items):
   // unit = (item | l << 31, part)
   __shared__ uint32_t misc[64];

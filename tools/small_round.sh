@@ -8,7 +8,7 @@ for l in sys.stdin:
     except Exception: print(l.strip()[:200]); continue
     print(d['n'], d['ok'], d['median_ms'], d['min_ms'], d['stats']['kernel_launches'])
 "
-for lg in 16 20; do
+for lg in ${SIZES:-16 18 20}; do
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/small_launches_$lg.csv \
     python tools/small_once.py $lg > gpurun_out/small_ncu_$lg.log 2>&1
   python - <<PY
