@@ -186,6 +186,8 @@ inline int g_concurrent_classes = getenv("SQ_CONCURRENT_CLASSES") ? atoi(getenv(
 // 0 = merge sort (blocksort.cuh)
 // small levels (graph replay, two bucket-sort classes): n at most this; see GraphCache below
 inline size_t g_graph_max_n = getenv("SQ_GRAPH_MAX_N") ? (size_t)atoll(getenv("SQ_GRAPH_MAX_N")) : (size_t(1) << 22);
+// samples of at least this many pivots are gathered by k_sample_gather (a huge value turns it off)
+inline uint32_t g_sample_split = getenv("SQ_SAMPLE_SPLIT") ? (uint32_t)atoi(getenv("SQ_SAMPLE_SPLIT")) : 4096u;
 inline int g_small_classes = getenv("SQ_SMALL_CLASSES") ? atoi(getenv("SQ_SMALL_CLASSES")) : 1;
 inline int g_base_case = getenv("SQ_BASE_CASE") ? atoi(getenv("SQ_BASE_CASE")) : 1;
 constexpr size_t kMaxSmem = 232448;  // dynamic shared memory per CTA on sm_100 (227 KB)
@@ -1013,14 +1015,35 @@ struct Engine {
     uint64_t level_total = 0;
     for (const Seg& g : segs) level_total += g.len;
     const bool lat = level_total <= g_graph_max_n && g_small_classes;  // small level: latency shapes
-    with_tile_lat<K>(lat, std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
+    // (every round is one CTA alone on its SM: its latency is the sampler's, so the
+    // 8K/16K-candidate sorts of 32-bit keys run twice the warps with 16 keys per thread)
+    auto with_sample_tile = [&](uint32_t tile, auto&& f) {
+#ifndef SQ_SAMPLE_V32
+      if constexpr (sizeof(K) == 4) {
+        if (tile == 16384) return f(IC<1024>{}, IC<16>{});
+        if (tile == 8192) return f(IC<512>{}, IC<16>{});
+      }
+#endif
+      return with_tile_lat<K>(lat, tile, f);
+    };
+    with_sample_tile(std::max<uint32_t>(64, tile_for(std::max<uint32_t>(maxnp, 1))), [&](auto nt, auto v) {
       constexpr int NT = decltype(nt)::value, V = decltype(v)::value;
       using BS = BlockSort<K, NT, V>;
       constexpr bool SB = BIN && BS::SMEM_BYTES + bin_smem<K, NT, V, false, BIN>() <= kMaxSmem;
       constexpr size_t smem = BS::SMEM_BYTES + bin_smem<K, NT, V, false, SB>();
       set_smem(k_sample_all<K, NT, V, SB>, smem);
       ProfScope ps("sample", st);
-      k_sample_all<K, NT, V, SB><<<ns * kCap, NT, smem, st>>>(dL, kb[X], cand, flags, p0s);
+      // large samples: the random reads spread over many CTAs first (k_sample_gather)
+      const bool split = maxnp >= g_sample_split;
+      if (split) {
+        const uint32_t nchunk = (maxnp + kSampleChunk - 1) / kSampleChunk;
+        k_sample_gather<K><<<ns * kCap * nchunk, 256, 0, st>>>(dL, kb[X], cand, nchunk);
+        check_launch("k_sample_gather");
+        launch_pdl(k_sample_all<K, NT, V, SB>, ns * kCap, NT, smem, st, (const LevelSeg*)dL, (const K*)kb[X], cand,
+                   flags, p0s, true);
+      } else {
+        k_sample_all<K, NT, V, SB><<<ns * kCap, NT, smem, st>>>(dL, kb[X], cand, flags, p0s, false);
+      }
       check_launch("k_sample_all");
     });
     {

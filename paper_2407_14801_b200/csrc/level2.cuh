@@ -107,10 +107,41 @@ __device__ __forceinline__ void tile_sort(SK* s, uint32_t* cnt, uint32_t len) {
 // candidates, whether they are strictly increasing, and their smallest value.
 // BIN: the candidates are sorted by the counting sort (binsort.cuh) where it serves
 // the key type and shape, else by the merge sort.
+// Candidate gather for large samples: one round's m-1 random reads issued by a single
+// CTA are bound by that SM's outstanding misses (~40 us for 16383 reads), so they are
+// spread over CTAs of kSampleChunk candidates each; k_sample_all then reads the
+// round's candidates back contiguously.  Grid: (segment, round, chunk), chunk-minor.
+constexpr uint32_t kSampleChunk = 1024;
+template <typename K>
+__global__ void __launch_bounds__(256)
+k_sample_gather(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* __restrict__ cand,
+                uint32_t nchunk) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const uint32_t sr = blockIdx.x / nchunk, chunk = blockIdx.x % nchunk;
+  const uint32_t seg = sr / kCap, r = sr % kCap;
+  const LevelSeg sg = segs[seg];
+  const uint32_t np = sg.k - 1;
+  const K* lvl = data + sg.off;
+  K* out = cand + sg.cand_base + uint64_t(r) * np;
+  constexpr int J = kSampleChunk / 256;
+  K x[J];
+#pragma unroll
+  for (int j = 0; j < J; j++) {
+    const uint32_t i = chunk * kSampleChunk + threadIdx.x + uint32_t(j) * 256;
+    x[j] = i < np ? __ldg(&lvl[draw_index(draw(sg.node, r, i), sg.len)]) : K(0);
+  }
+#pragma unroll
+  for (int j = 0; j < J; j++) {
+    const uint32_t i = chunk * kSampleChunk + threadIdx.x + uint32_t(j) * 256;
+    if (i < np) out[i] = x[j];
+  }
+}
+
+// `gathered`: the round's candidates were already written to `cand` by k_sample_gather.
 template <typename K, int NT, int V, bool BIN = false>
 __global__ void __launch_bounds__(NT)
 k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* __restrict__ cand,
-             uint8_t* __restrict__ flags, K* __restrict__ p0s) {
+             uint8_t* __restrict__ flags, K* __restrict__ p0s, bool gathered) {
   using BS = BlockSort<K, NT, V>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
@@ -121,7 +152,18 @@ k_sample_all(const LevelSeg* __restrict__ segs, const K* __restrict__ data, K* _
   const LevelSeg sg = segs[seg];
   const uint32_t np = sg.k - 1;
   const K* lvl = data + sg.off;
-  {  // every random read of the thread in flight at once (they are DRAM-latency bound)
+  if (gathered) {  // (programmatic dependent of k_sample_gather)
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    const K* in = cand + sg.cand_base + uint64_t(r) * np;
+    K x[V];
+#pragma unroll
+    for (int j = 0; j < V; j++) {
+      const uint32_t i = threadIdx.x + uint32_t(j) * NT;
+      x[j] = i < np ? in[i] : KeyTraits<K>::kMax;
+    }
+#pragma unroll
+    for (int j = 0; j < V; j++) s[TP(threadIdx.x + uint32_t(j) * NT)] = x[j];
+  } else {  // every random read of the thread in flight at once (they are DRAM-latency bound)
     K x[V];
 #pragma unroll
     for (int j = 0; j < V; j++) {
