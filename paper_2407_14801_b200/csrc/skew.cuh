@@ -133,6 +133,11 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t* total) 
 #ifndef SQ_TR_CACHE
 #define SQ_TR_CACHE "cg"
 #endif
+// runs of at least this many staged bytes are copied by the whole producer warp
+#ifndef SQ_COOP_RUN_BYTES
+#define SQ_COOP_RUN_BYTES 1024
+#endif
+constexpr uint32_t kCoopRunBytes = SQ_COOP_RUN_BYTES;
 template <typename K, bool PAIRS, int S, int F>
 __global__ void __launch_bounds__(WsCfg<K, PAIRS, S, F>::NT, 2)
 k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict__ pcount, const K* __restrict__ src,
@@ -231,7 +236,37 @@ k_transpose_ws(const PieceDesc* __restrict__ pieces, const uint32_t* __restrict_
         uint32_t ts;
         const uint32_t so = warp_excl_scan(sbytes, &ts) + carry_sb;
         carry_sb += ts;
-        if (flen) {
+        // long runs (sorted or clustered input: a column's keys fall into a few buckets,
+        // so a run is hundreds of keys): the warp copies each run together instead of
+        // one lane walking it (warp-uniform choice)
+        const bool coop = __reduce_max_sync(0xffffffffu, sbytes) >= kCoopRunBytes;
+        if (coop) {
+          uint32_t live = __ballot_sync(0xffffffffu, flen != 0);
+          const uint32_t my_e0 = (so + mis) / EB;
+          const unsigned long long my_g =
+              (unsigned long long)(reinterpret_cast<uintptr_t>(src + srcpos) - mis);
+          while (live) {
+            const int L = __ffs(live) - 1;
+            live &= live - 1;
+            const uint32_t e0 = __shfl_sync(0xffffffffu, my_e0, L), fl = __shfl_sync(0xffffffffu, flen, L);
+            const uint32_t sb = __shfl_sync(0xffffffffu, sbytes, L), so_l = __shfl_sync(0xffffffffu, so, L);
+            const uint32_t sp = __shfl_sync(0xffffffffu, srcpos, L);
+            const unsigned char* g = reinterpret_cast<const unsigned char*>((uintptr_t)__shfl_sync(0xffffffffu, my_g, L));
+            const uint32_t e1 = e0 + fl;
+            for (uint32_t wd = (e0 >> 5) + lane; wd <= (e1 - 1) >> 5; wd += 32) {
+              const uint32_t lo = max(e0, wd * 32) - wd * 32, hi = min(e1, wd * 32 + 32) - wd * 32;
+              const uint32_t m = (hi == 32 ? 0xffffffffu : ((1u << hi) - 1)) & ~((1u << lo) - 1);
+              atomicOr(&bits[wd], m);
+            }
+            const uint32_t sdst = smem_addr(slot) + so_l;
+            for (uint32_t v = 16 * lane; v < sb; v += 512)
+              asm volatile("cp.async." SQ_TR_CACHE ".shared.global [%0], [%1], 16;\n" ::"r"(sdst + v), "l"(g + v));
+            if (PAIRS) {
+              const uint32_t* gv = vsrc + sp;
+              for (uint32_t kk = lane; kk < fl; kk += 32) cp_async_elem(&vslot[e0 + kk], &gv[kk]);
+            }
+          }
+        } else if (flen) {
           const uint32_t e0 = (so + mis) / EB, e1 = e0 + flen;
           for (uint32_t wd = e0 >> 5; wd <= (e1 - 1) >> 5; wd++) {
             const uint32_t lo = max(e0, wd * 32) - wd * 32, hi = min(e1, wd * 32 + 32) - wd * 32;
