@@ -117,7 +117,7 @@ template <typename K, int V, int G>
 __device__ __forceinline__ void warp_bitonic_merge(K (&r)[V]) {
   const int lane = threadIdx.x & 31;
   const bool upper = (lane & (G / 2)) != 0;
-  const uint32_t one = (uint32_t)c_one, mone = (uint32_t)c_mone, mtwo = (uint32_t)c_mtwo;
+  const uint32_t one = (uint32_t)c_one, mtwo = (uint32_t)c_mtwo;
   {
     K p[V];
 #pragma unroll
