@@ -968,7 +968,11 @@ struct Engine {
       } else {
         std::vector<ColDesc>& full = colcls[std::max<uint32_t>(64, tile_for(m))];
         for (uint32_t c = 0; c < fc; c++) full.push_back({uint32_t(g.off + uint64_t(c) * m), m, s, c});
-        if (rem) colcls[std::max<uint32_t>(64, tile_for(rem))].push_back({uint32_t(g.off + uint64_t(fc) * m), rem, s, fc});
+        // the ragged last column rides in the full columns' class (padded tile): a class
+        // of its own is one more launch, a lone CTA after the column sort's last wave
+        if (rem)
+          (fc ? full : colcls[std::max<uint32_t>(64, tile_for(rem))])
+              .push_back({uint32_t(g.off + uint64_t(fc) * m), rem, s, fc});
       }
       for (uint32_t c0 = 0; c0 < m; c0 += 64) mtasks.push_back({s, c0, std::min(m, c0 + 64)});
     }
